@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 rSVD-BKI / SVT hot path (BASELINE.json configs[1]).
+
+Step = one rsvd_bki call on cfg2: a 100,000 x 50,000 sparse matrix with
+5,000,000 uniformly placed N(0,1) entries (seeded synthetic stand-in; the
+paper's MovieLens matrices are not available), k=100, s=10, p=5 (W = 660).
+
+  value  : rSVD-BKI calls/s over the whole job (N ranks x K calls / max-rank
+           device time), matrix resident in HBM, Omega generated on the device
+  e2e    : the same metric through the public API rsvd_bki(A, params) with a
+           host SparseMatrix whose device mirror is dropped every step (CSR +
+           CSC + schedules + values uploaded, host numpy Omega uploaded,
+           U/S/V downloaded), wall clock with a device sync per step
+  roofline: dominant native call of the step (CUDA events around every call)
+  cpu_baseline: the oracle restatement of the reference (oracle/, numpy +
+           scipy + OpenBLAS with all host cores) on one full cfg2 call
+
+--impl reference times that CPU oracle alone (rank 0) on the same workload.
+Multi-GPU (torchrun, N > 1): independent replicas, one per GPU (weak scaling);
+device time is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+K_RANK, S_OVER, P_POW, SEED = 100, 10, 5, 0
+WORKLOAD = "cfg2: rsvd_bki on 100000x50000, 5,000,000 uniform nnz N(0,1), k=100 s=10 p=5 (W=660)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-baseline", choices=["full", "skip"], default="full")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """NVML samples of SM clock and throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as exc:  # pragma: no cover - NVML missing
+            self.err = str(exc)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": getattr(nv, "nvmlClocksEventReasonGpuIdle", 0x1),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def result(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_matrix():
+    from paper_1810_06860_b200 import workloads
+    from paper_1810_06860_b200.sparse import SparseMatrix
+
+    obs = workloads.cfg2()
+    return SparseMatrix.from_coo(obs.m, obs.n, obs.rows, obs.cols, obs.values), obs
+
+
+def fp64_peak_tflops():
+    """Measured fp64 GEMM peak on this GPU (cuBLAS DGEMM 8192^3, best of 3);
+    MEASURED_PEAKS.json only carries bf16 and HBM figures."""
+    import torch
+
+    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    a @ b
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, 2 * 8192 ** 3 / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    del a, b
+    torch.cuda.empty_cache()
+    return best
+
+
+def cpu_oracle_call(obs):
+    import oracle
+
+    A = oracle.csr_from_triples(obs.m, obs.n, obs.rows, obs.cols, obs.values)
+    A.transpose_index()  # built once per pattern, like the reference's lazy index
+    t0 = time.perf_counter()
+    res, _ = oracle.sketch_bki(A, oracle.SketchParams(k=K_RANK, p=P_POW, s=S_OVER, seed=SEED))
+    return time.perf_counter() - t0, res
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    from paper_1810_06860_b200 import workloads
+
+    obs = workloads.cfg2()
+    budget = 150.0
+    times = []
+    for i in range(max(1, args.steps)):
+        dt, _ = cpu_oracle_call(obs)
+        times.append(dt)
+        if sum(times) + dt > budget:
+            break
+    per = float(np.mean(times))
+    v = 1.0 / per
+    line = {
+        "metric": METRIC, "value": v, "unit": "rSVD-BKI calls/s (cfg2, k=100)", "impl": "reference",
+        "n_gpus": 0, "steps": len(times), "warmup": 0, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "none", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg2 generator)",
+        "config": {"workload": WORKLOAD, "backend": "oracle/ port of lowrank (numpy+scipy+OpenBLAS)"},
+        "cpu_baseline": {"value": v, "unit": "rSVD-BKI calls/s (cfg2, k=100)", "cores": os.cpu_count(),
+                         "kind": "port", "sample": f"{len(times)} full cfg2 rsvd_bki call(s), "
+                                                   f"{per:.1f} s each; warmup skipped (CPU, no JIT)"},
+        "e2e": {"value": v, "unit": "rSVD-BKI calls/s (cfg2, k=100)", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "note": f"requested --steps {args.steps} --warmup {args.warmup}; timed {len(times)} within a {budget:.0f} s budget",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    import torch
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1810_06860_b200 import _native, device, profiling
+    from paper_1810_06860_b200.rsvd import RsvdParams, rsvd_bki, rsvd_bki_dev
+
+    lib = _native.load()
+    A, obs = make_matrix()
+    params = RsvdParams(k=K_RANK, p=P_POW, s=S_OVER, seed=SEED)
+    A.pattern()
+    A.device_values()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
+
+    def step():
+        return rsvd_bki_dev(A, params, allow_fallback=False, omega="device")
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    prof = profiling.Profiler()
+    launches0 = lib.lr_launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        _native.PROFILER = prof
+        e0.record()
+        for _ in range(args.steps):
+            flush.zero_()
+            res, Q, _ = step()
+        e1.record()
+        torch.cuda.synchronize()
+        _native.PROFILER = None
+    barrier()
+    launches = lib.lr_launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = ws * args.steps / (ms * 1e-3)
+
+    summary = prof.summary()
+    step_ms = ms / args.steps
+
+    # ---- e2e through the public API with host buffers
+    e2e_times, h2d, d2h = [], [], []
+    for _ in range(args.e2e_steps + 1):
+        A._pattern = None
+        A._dvals = None
+        torch.cuda.synchronize()
+        t_h2d, t_d2h = device.TRAFFIC["h2d"], device.TRAFFIC["d2h"]
+        t0 = time.perf_counter()
+        r_host, sub = rsvd_bki(A, params)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+        h2d.append(device.TRAFFIC["h2d"] - t_h2d)
+        d2h.append(device.TRAFFIC["d2h"] - t_d2h)
+    e2e_times, h2d, d2h = e2e_times[1:], h2d[1:], d2h[1:]  # first call warms the upload path
+    e2e_ms = float(np.mean(e2e_times)) * 1e3
+    if ws > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    fp64_peak = fp64_peak_tflops()
+
+    kernels = []
+    for name, d in sorted(summary.items(), key=lambda kv: -kv[1]["ms"]):
+        entry = {"call": name, "calls_per_step": d["calls"] / args.steps, "ms_per_step": d["ms"] / args.steps,
+                 "share": d["ms"] / ms}
+        if name in profiling.MODELS and d["ms"] > 0:
+            bound = profiling.MODELS[name][0]
+            if bound == "hbm":
+                ach = d["bytes"] / (d["ms"] * 1e-3) / 1e9
+                entry.update(bound="hbm", achieved=ach, unit="GB/s", peak=hbm_peak, frac=ach / hbm_peak,
+                             gather_gbs=(d["flops"] / 2 * 8) / (d["ms"] * 1e-3) / 1e9)
+            else:
+                ach = d["flops"] / (d["ms"] * 1e-3) / 1e12
+                entry.update(bound="tensor", achieved=ach, unit="TFLOP/s", peak=fp64_peak, frac=ach / fp64_peak)
+        kernels.append(entry)
+    dominant = next((k for k in kernels if "bound" in k), None)
+    roofline = None
+    if dominant:
+        roofline = {"bound": dominant["bound"], "achieved": dominant["achieved"], "peak": dominant["peak"],
+                    "unit": dominant["unit"], "frac": dominant["frac"], "traffic": None,
+                    "kernel": dominant["call"], "share_of_step": dominant["share"],
+                    "peak_source": ("MEASURED_PEAKS.json hbm_gbs (measured)" if dominant["bound"] == "hbm"
+                                    else "fp64 cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json "
+                                         "has no fp64 figure)")}
+
+    cpu = None
+    if args.cpu_baseline == "full" and ws == 1:
+        dt, ref = cpu_oracle_call(obs)
+        rel_s = float(np.max(np.abs(res.S_host - ref.S) / ref.S))
+        cpu = {"value": 1.0 / dt, "unit": "rSVD-BKI calls/s (cfg2, k=100)", "cores": os.cpu_count(),
+               "kind": "port", "sample": f"one full cfg2 rsvd_bki call of oracle/ (numpy+scipy, OpenBLAS "
+                                         f"default threads): {dt:.2f} s", "max_rel_S_diff_vs_gpu": rel_s}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "rSVD-BKI calls/s (cfg2, k=100)", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg2 generator)",
+        "config": {"workload": WORKLOAD, "parallelism": f"replicas x{ws}", "omega": "device (Philox, value) / "
+                   "host numpy (e2e)", "l2": "256 MB flush between timed steps"},
+        "rsvd_bki_time_s": step_ms * 1e-3,
+        "e2e": {"value": ws / (e2e_ms * 1e-3), "unit": "rSVD-BKI calls/s (cfg2, k=100)",
+                "h2d_bytes_per_step": int(np.mean(h2d)), "d2h_bytes_per_step": int(np.mean(d2h)),
+                "ms_per_step": e2e_ms, "note": "public rsvd_bki(A, params) with pageable host numpy buffers"},
+        "roofline": roofline,
+        "roofline_kernels": kernels,
+        "cpu_baseline": cpu,
+        "gpu_launches": int(launches),
+        "clocks": clk.result(),
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

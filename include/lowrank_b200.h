@@ -1,0 +1,193 @@
+/*
+ * lowrank_b200.h -- C ABI of the B200-native SVT / rSVD hot path.
+ *
+ * Drop-in boundary for the reference package `lowrank`
+ * (/root/reference/pkg/src/lowrank).  The reference is pure Python over
+ * numpy/scipy/LAPACK, so its "FFI" is the set of module-global kernel calls
+ * its algorithms make; each entry point below replaces one of them and cites
+ * it.  The host mirror (paper_1810_06860_b200/) binds these through ctypes
+ * and re-exposes the reference's own Python names and error behaviour.
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer unless the name ends in _host;
+ *   - dense blocks are row-major fp64 with an explicit leading dimension
+ *     (ld >= columns), matching the reference's C-contiguous arrays;
+ *   - sparse patterns use int32 offsets/indices (all BASELINE configs have
+ *     nnz < 2^31); the reference stores int64 (sparse.py:47-48);
+ *   - `stream` is a cudaStream_t passed as void*; calls are stream-ordered
+ *     and never synchronize unless documented;
+ *   - no function allocates device memory on the hot path: scratch is
+ *     passed in, sized by the *_workspace helpers;
+ *   - return value: LR_OK or an lr_status code; lr_last_error() gives the
+ *     message of the calling thread's last failure.
+ */
+#ifndef LOWRANK_B200_H
+#define LOWRANK_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LR_OK = 0,
+  LR_ERR_ARG = 1,    /* -> ValueError            */
+  LR_ERR_RANK = 2,   /* -> RankDeficiencyError   */
+  LR_ERR_NOCONV = 3, /* -> NumericalError        */
+  LR_ERR_CUDA = 4,   /* -> RuntimeError          */
+} lr_status;
+
+int lr_version(void);
+const char* lr_last_error(void);
+int lr_sm_count(void);
+/* Number of kernels this library has launched in the process (all streams). */
+long long lr_launch_count(void);
+
+/* ------------------------------------------------------------------ sparse */
+
+/* Y[rows x w] = A * X  for a row-compressed pattern (CSR for Y*X, the CSC copy
+ * for Y^T*X).  Replaces scipy csr_matvecs as called by `spmm`
+ * (sparse.py:153-158) and by `spmm_t` (sparse.py:161-170, which re-gathers
+ * A.data[perm] every call -- here the CSC values are a persistent copy).
+ * items: optional (NULL -> one item per row) int4 {row, beg, end, slot}
+ *   schedule splitting long rows; slot >= 0 writes a partial row into
+ *   scratch[slot*w ...]; splits (int4 {row, slot_beg, slot_end, 0}) then sum
+ *   partial rows in slot order (deterministic).  Rows are summed in stored
+ *   order (scipy's sequential axpy order) within an item. */
+int lr_spmm_f64(const int* ptr, const int* idx, const double* val, int rows,
+                const int* items, int n_items, const int* splits, int n_splits,
+                const double* X, long long ldx, int w, double* Y, long long ldy,
+                double* scratch, void* stream);
+
+/* x_e = sum_t U[i,t]*S[t]*V[j,t] for every stored (i,j), CSR order.
+ * Replaces `project_pattern` / `_project_entries` (sparse.py:173-191). */
+int lr_sddmm_f64(const int* ptr, const int* idx, int rows, const int* items, int n_items,
+                 const double* U, long long ldu, const double* S, const double* V, long long ldv,
+                 int r, double* x, void* stream);
+
+/* The fused SVT step of completion.py:373-386 in one pass over the pattern:
+ *   x_e   = sum_t U[i,t]*S[t]*V[j,t]           (project_pattern)
+ *   d_e   = x_e - m_e;  partial sums of d_e^2   (frobenius(x - m), sparse.py:219-228)
+ *   if apply: y_e += step*(m_e - x_e) in the CSR copy and, through inv_perm,
+ *             in the CSC copy                   (update_pattern_values, sparse.py:205-216)
+ * r == 0 is legal (x = 0).  Writes n_blocks partial (sum d^2, max|d|) pairs to
+ * partial[]; lr_svt_step_finish reduces them in fixed order into out2[0..1]. */
+int lr_svt_step_f64(const int* ptr, const int* idx, int rows, const int* items, int n_items,
+                    const double* U, long long ldu, const double* S, const double* V, long long ldv,
+                    int r, const double* m_vals, double* y_csr, double* y_csc, const int* inv_perm,
+                    double step, int apply, double* partial, int n_partial, double* out2, void* stream);
+int lr_svt_step_partials(void);
+
+/* y_csr += delta; y_csc[inv_perm[e]] += delta[e]  (update_pattern_values). */
+int lr_pattern_axpy_f64(double* y_csr, double* y_csc, const int* inv_perm, const double* delta,
+                        double alpha, long long nnz, void* stream);
+/* dst[t] = src[perm[t]] : builds/refreshes the CSC value copy. */
+int lr_gather_f64(const double* src, const int* perm, double* dst, long long n, void* stream);
+
+/* ----------------------------------------------------------- reductions */
+/* out[0] = sum x^2, out[1] = max |x|, out[2] = #non-finite  over an
+ * rows x cols block (ld); deterministic fixed-order tree.  Backs
+ * `frobenius` (sparse.py:219-228) and the finiteness checks of
+ * linalg._check_matrix (linalg.py:78-84). */
+int lr_block_stats_f64(const double* X, long long rows, long long cols, long long ld,
+                       double* partial, double* out3, void* stream);
+int lr_stats_partials(void);
+/* out[0] = sum_i x_i*y_i (deterministic). */
+int lr_dot_f64(const double* x, const double* y, long long n, double* partial, double* out,
+               void* stream);
+/* Power-iteration helper for spectral_norm_est (sparse.py:231-256):
+ * given z (n) and the current x (n): lam = x.z, zn = ||z||; if not done:
+ * prev=curr, curr=sqrt(max(lam,0)); x = z/zn; done when |curr-prev| <=
+ * tol*max(curr,1e-300) or zn == 0.  state = {prev, curr, done, iters, zero}. */
+int lr_power_update_f64(double* x, const double* z, long long n, double tol, double* state,
+                        double* partial, void* stream);
+
+/* ---------------------------------------------------------------- dense */
+enum {
+  LR_GEMM_B_UPPER = 1,    /* B is upper triangular (K == N): skip zero blocks   */
+  LR_GEMM_SYRK_UPPER = 2, /* transA, A == B: compute upper tiles, mirror (exactly symmetric) */
+};
+/* C[MxN] = alpha*op(A)*B + beta*C on fp64 tensor cores (mma.sync f64 ->
+ * DMMA.8x8x4).  transA=0: A is MxK; transA=1: A is KxM (C = A^T B, split-K
+ * over the long K with a fixed-order partial reduction).  Replaces the BLAS
+ * dsyrk/dgemm calls of eig_svd (linalg.py:189,200), the lift products
+ * (rsvd.py:195,229; completion.py:217,243) and qb_error (rsvd.py:252). */
+long long lr_gemm_workspace_doubles(int transA, int M, int N, int K, int flags);
+int lr_gemm_f64(int transA, int M, int N, int K, double alpha, const double* A, long long lda,
+                const double* B, long long ldb, double beta, double* C, long long ldc, int flags,
+                double* work, long long work_doubles, void* stream);
+
+/* Upper Cholesky A = R^T R (n x n, in place; upper triangle of A receives R,
+ * lower triangle zeroed) and R^{-1} (upper, into Rinv).  info_host receives 0
+ * or 1 + the first non-positive pivot column (synchronizes). Building block of
+ * the CholeskyQR2 / shifted CholeskyQR3 replacement of the Householder QR in
+ * `orth` (linalg.py:101-124). shift is added to the diagonal first. */
+long long lr_potrf_workspace_doubles(int n);
+int lr_potrf_inv_f64(int n, double* A, long long lda, double shift, double* Rinv, long long ldr,
+                     double* work, int* info_host, void* stream);
+
+/* Partial-pivoting LU of a tall m x n block (m >= n), in place, returning
+ * P^T L like scipy.linalg.lu(X, permute_l=True) as used by `lu_pl`
+ * (linalg.py:127-150): pivot = first max |x| of the remaining rows, unit
+ * entry at the pivot row, zeros to its right, multipliers elsewhere.
+ * status_host[0] = -1 on success, else the first column whose |pivot| <
+ * 1e-14*max|X| (pivot value in status_host[1], tolerance in status_host[2]),
+ * -2 for a zero matrix, -3 for non-finite input. Synchronizes. */
+long long lr_lu_workspace_doubles(int m, int n);
+int lr_lu_pl_f64(int m, int n, double* X, long long ldx, double* work, double* status_host,
+                 void* stream);
+
+/* Symmetric eigendecomposition by parallel (block-)Jacobi: eigenvalues
+ * ascending in d, orthonormal eigenvectors in V (n x n, ldv).  A (n x n) is
+ * overwritten.  Replaces LAPACK dsyevd behind `sym_eig` (linalg.py:153-169).
+ * sweeps_host receives the sweep count; LR_ERR_NOCONV after max_sweeps. */
+long long lr_syevj_workspace_doubles(int n);
+int lr_syevj_f64(int n, double* A, long long lda, double* d, double* V, long long ldv,
+                 int max_sweeps, double* work, int* sweeps_host, void* stream);
+
+/* Symmetric eigendecomposition by Householder tridiagonalization (cooperative
+ * kernel, rows in shared memory), multisection bisection and inverse
+ * iteration (+ MGS inside clusters closer than 1e-8*||A||), then the
+ * back-transform.  Eigenvalues ascending in d, eigenvectors in V; A is not
+ * modified.  LAPACK-level accuracy (absolute eps*||A||), the default solver
+ * behind sym_eig / eig_svd (linalg.py:153-202).  clusters_host (optional)
+ * receives the number of re-orthonormalised clusters.  Synchronizes once. */
+long long lr_syevd_workspace_doubles(int n);
+int lr_syevd_f64(int n, const double* A, long long lda, double* d, double* V, long long ldv, double* work,
+                 int* clusters_host, void* stream);
+
+/* Sign rule of linalg._fix_signs (linalg.py:87-98): flip column j of V (and
+ * of U if non-NULL) so V's first nonzero entry in column j is >= 0. */
+int lr_fix_signs_f64(double* V, long long ldv, int rows_v, int cols, double* U, long long ldu,
+                     int rows_u, void* stream);
+/* B[:, j] = V[:, idx_j] * scale_j with scale_j = sgn/S[idx_j]; column gather
+ * used by eig_svd's U = A (V / S) for a selected window (linalg.py:199-201). */
+int lr_scale_columns_f64(const double* V, long long ldv, int rows, const int* cols_idx, int ncols,
+                         const double* S, int invert, double* B, long long ldb, void* stream);
+
+/* --------------------------------------------------------------- random */
+/* Omega (rows x cols, row-major, ldo) = gaussian_matrix(RngState(seed), rows,
+ * cols) of rng.py:77-94 on the device: numpy Philox4x64-10 (key = seed,
+ * counter starting at 1), uniforms (x >> 11) * 2^-53, Box-Muller pairs over
+ * the whole request, column-major fill.  Uniform stream bit-exact with numpy;
+ * normals within a few ulp (log/sincos rounding). */
+int lr_gaussian_f64(unsigned long long seed, int rows, int cols, double* omega, long long ldo,
+                    void* stream);
+
+/* ------------------------------------------------------------- utilities */
+int lr_copy2d_f64(const double* src, long long lds, double* dst, long long ldd, long long rows,
+                  long long cols, int reverse_cols, void* stream);
+int lr_fill_f64(double* dst, long long ld, long long rows, long long cols, double v, void* stream);
+/* dst (cols x rows) = src^T */
+int lr_transpose_f64(const double* src, long long lds, long long rows, long long cols, double* dst,
+                     long long ldd, void* stream);
+/* dst = (src + src^T) / 2 : the symmetrization of sym_eig (linalg.py:165) */
+int lr_symmetrize_f64(const double* src, long long lds, int n, double* dst, long long ldd, void* stream);
+/* d[i] = A[i][i] */
+int lr_diag_f64(const double* A, long long lda, int n, double* d, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOWRANK_B200_H */

@@ -1,0 +1,333 @@
+// Tall-skinny LU with partial pivoting returning P^T L, the replacement for
+// scipy.linalg.lu(X, permute_l=True) inside `lu_pl` (linalg.py:127-150;
+// survey K4).
+//
+// One cooperative persistent kernel.  Rows are split into contiguous slabs,
+// one per CTA; a panel of nb columns of the slab lives in shared memory.  Per
+// column: every CTA proposes its largest |x| among rows not yet pivoted,
+// publishes (|x|, row, panel row) and one grid barrier later every CTA picks
+// the same winner (largest |x|, ties -> smallest row), so no row swaps are
+// ever moved through memory: pivot rows are only marked.  After a panel the
+// pivot rows' trailing entries are solved with the panel's unit-lower block
+// (forward substitution, redundantly per CTA) and each CTA updates its own
+// rows' trailing columns.  Finally pivot rows get their unit entry and zeros
+// to its right, which is exactly P^T L.
+//
+// Latency-bound by construction (one grid barrier per column); reported as
+// time and share of the step, not a roofline fraction.
+#include <cooperative_groups.h>
+
+#include "lr_common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace lr {
+
+constexpr int LU_THREADS = 256;
+constexpr int LU_CHUNK = 64;  // trailing columns per U12 chunk
+
+struct LuParams {
+  double* X;
+  long long ldx;
+  int m, n, nb, rows_per;
+  const double* stats;  // {sumsq, max|x|, nonfinite}
+  double* cand;         // [2][G][2]  {|x|, row}
+  double* prow;         // [2][G][nb]
+  int* pivrow;          // [n]
+  double* status;       // {bad col or -1, pivot, tol}
+};
+
+__device__ __forceinline__ void better(double& v, int& r, double v2, int r2) {
+  if (v2 > v || (v2 == v && r2 < r)) {
+    v = v2;
+    r = r2;
+  }
+}
+
+__global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double lu_smem[];
+  const int nb = p.nb, LD = nb + 1;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int r0 = cta * p.rows_per;
+  const int r1 = min(p.m, r0 + p.rows_per);
+  const int nr = max(0, r1 - r0);
+  double* P = lu_smem;                                   // rows_per x LD
+  double* U12 = P + (long long)p.rows_per * LD;          // nb x LU_CHUNK
+  double* urow = U12 + nb * LU_CHUNK;                    // nb
+  double* L11 = urow + nb;                               // nb x nb
+  int* pivflag = reinterpret_cast<int*>(L11 + nb * nb);  // rows_per
+  __shared__ double red_v[LU_THREADS / 32];
+  __shared__ int red_r[LU_THREADS / 32];
+  __shared__ double win_v;
+  __shared__ int win_r, win_c;
+
+  const double maxabs = p.stats[1];
+  const double tol = 1e-14 * maxabs;
+  if (maxabs == 0.0 || p.stats[2] != 0.0) return;  // handled by the host wrapper
+  for (int i = tid; i < nr; i += LU_THREADS) pivflag[i] = -1;
+  int par = 0;
+
+  for (int J = 0; J < p.n; J += nb) {
+    const int jb = min(nb, p.n - J);
+    for (int e = tid; e < nr * jb; e += LU_THREADS) {
+      int i = e / jb, c = e - (e / jb) * jb;
+      P[i * LD + c] = p.X[(long long)(r0 + i) * p.ldx + J + c];
+    }
+    __syncthreads();
+    for (int jj = 0; jj < jb; ++jj) {
+      const int j = J + jj;
+      // local argmax among un-pivoted rows
+      double bv = -1.0;
+      int br = 0x7fffffff;
+      for (int i = tid; i < nr; i += LU_THREADS)
+        if (pivflag[i] < 0) better(bv, br, fabs(P[i * LD + jj]), r0 + i);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        int r2 = __shfl_xor_sync(0xffffffffu, br, o);
+        better(bv, br, v2, r2);
+      }
+      if (lane == 0) {
+        red_v[wid] = bv;
+        red_r[wid] = br;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < LU_THREADS / 32; ++w) better(bv, br, red_v[w], red_r[w]);
+        p.cand[(par * G + cta) * 2 + 0] = bv;
+        p.cand[(par * G + cta) * 2 + 1] = (double)br;
+        win_r = br;
+      }
+      __syncthreads();
+      if (win_r != 0x7fffffff)
+        for (int c = tid; c < jb; c += LU_THREADS)
+          p.prow[((long long)par * G + cta) * nb + c] = P[(win_r - r0) * LD + c];
+      grid.sync();
+      // global winner: same answer in every CTA
+      bv = -1.0;
+      br = 0x7fffffff;
+      int bc = -1;
+      for (int c = tid; c < G; c += LU_THREADS) {
+        double v2 = p.cand[(par * G + c) * 2 + 0];
+        int r2 = (int)p.cand[(par * G + c) * 2 + 1];
+        if (v2 > bv || (v2 == bv && r2 < br)) {
+          bv = v2;
+          br = r2;
+          bc = c;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        int r2 = __shfl_xor_sync(0xffffffffu, br, o);
+        int c2 = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (v2 > bv || (v2 == bv && r2 < br)) {
+          bv = v2;
+          br = r2;
+          bc = c2;
+        }
+      }
+      if (lane == 0) {
+        red_v[wid] = bv;
+        red_r[wid] = br;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int wc = bc;
+        // recompute the winning CTA index from rows (rows are slab-contiguous)
+        for (int w = 1; w < LU_THREADS / 32; ++w) better(bv, br, red_v[w], red_r[w]);
+        wc = br / p.rows_per;
+        win_v = bv;
+        win_r = br;
+        win_c = wc;
+      }
+      __syncthreads();
+      const double* wrow = p.prow + ((long long)par * G + win_c) * nb;
+      if (!(win_v >= tol) || win_v == 0.0) {
+        if (cta == 0 && tid == 0) {
+          p.status[0] = (double)j;
+          p.status[1] = win_v;
+          p.status[2] = tol;
+        }
+        return;  // uniform across the grid
+      }
+      for (int c = tid; c < jb; c += LU_THREADS) urow[c] = wrow[c];
+      if (tid == 0) {
+        if (win_r >= r0 && win_r < r1) pivflag[win_r - r0] = j;
+        if (cta == 0) p.pivrow[j] = win_r;
+      }
+      __syncthreads();
+      const double upiv = urow[jj];
+      for (int i = tid; i < nr; i += LU_THREADS) {
+        if (pivflag[i] >= 0) continue;
+        double* row = P + i * LD;
+        const double l = row[jj] / upiv;
+        row[jj] = l;
+        for (int c = jj + 1; c < jb; ++c) row[c] = fma(-l, urow[c], row[c]);
+      }
+      __syncthreads();
+      par ^= 1;
+    }
+    // write the panel back
+    for (int e = tid; e < nr * jb; e += LU_THREADS) {
+      int i = e / jb, c = e - (e / jb) * jb;
+      p.X[(long long)(r0 + i) * p.ldx + J + c] = P[i * LD + c];
+    }
+    const int rest = p.n - J - jb;
+    if (rest > 0) {
+      grid.sync();
+      // unit-lower L11 from the pivot rows' multipliers
+      for (int e = tid; e < jb * jb; e += LU_THREADS) {
+        int a = e / jb, b = e - (e / jb) * jb;
+        L11[a * nb + b] = (b < a) ? p.X[(long long)p.pivrow[J + a] * p.ldx + J + b] : 0.0;
+      }
+      __syncthreads();
+      for (int c0 = 0; c0 < rest; c0 += LU_CHUNK) {
+        const int cw = min(LU_CHUNK, rest - c0);
+        for (int e = tid; e < jb * cw; e += LU_THREADS) {
+          int a = e / cw, c = e - (e / cw) * cw;
+          U12[a * LU_CHUNK + c] = p.X[(long long)p.pivrow[J + a] * p.ldx + J + jb + c0 + c];
+        }
+        __syncthreads();
+        // forward substitution with the unit-lower L11, parallel over columns
+        for (int c = tid; c < cw; c += LU_THREADS)
+          for (int a = 1; a < jb; ++a) {
+            double s = U12[a * LU_CHUNK + c];
+            for (int b = 0; b < a; ++b) s = fma(-L11[a * nb + b], U12[b * LU_CHUNK + c], s);
+            U12[a * LU_CHUNK + c] = s;
+          }
+        __syncthreads();
+        for (int e = tid; e < nr * cw; e += LU_THREADS) {
+          int i = e / cw, c = e - (e / cw) * cw;
+          if (pivflag[i] >= 0) continue;
+          double* xp = p.X + (long long)(r0 + i) * p.ldx + J + jb + c0 + c;
+          double s = *xp;
+          const double* li = P + i * LD;
+          for (int a = 0; a < jb; ++a) s = fma(-li[a], U12[a * LU_CHUNK + c], s);
+          *xp = s;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  // pivot rows: unit entry at their step, zeros to the right
+  for (int i = tid; i < nr; i += LU_THREADS) {
+    const int j = pivflag[i];
+    if (j < 0) continue;
+    double* row = p.X + (long long)(r0 + i) * p.ldx;
+    row[j] = 1.0;
+    for (int c = j + 1; c < p.n; ++c) row[c] = 0.0;
+  }
+  if (cta == 0 && tid == 0) p.status[0] = -1.0;
+}
+
+struct LuPlan {
+  int G, nb, rows_per;
+  size_t smem;
+};
+
+static size_t lu_smem_bytes(int rows_per, int nb) {
+  return (size_t)rows_per * (nb + 1) * 8 + (size_t)nb * LU_CHUNK * 8 + (size_t)nb * 8 +
+         (size_t)nb * nb * 8 + (size_t)rows_per * 4 + 16;
+}
+
+static LuPlan lu_plan(int m, int n) {
+  LuPlan pl{};
+  const int sms = sm_count();
+  const size_t limit2 = 110 * 1024, limit1 = 220 * 1024;
+  for (int occ = 2; occ >= 1; --occ) {
+    int G = sms * occ;
+    if (G > (m + 31) / 32) G = (m + 31) / 32;
+    if (G < 1) G = 1;
+    int rows_per = (m + G - 1) / G;
+    G = (m + rows_per - 1) / rows_per;
+    for (int nb = 32; nb >= 1; nb >>= 1) {
+      int nbe = nb > n ? n : nb;
+      size_t sm = lu_smem_bytes(rows_per, nbe);
+      if (sm <= (occ == 2 ? limit2 : limit1)) {
+        pl.G = G;
+        pl.nb = nbe;
+        pl.rows_per = rows_per;
+        pl.smem = sm;
+        return pl;
+      }
+    }
+  }
+  pl.G = 0;
+  return pl;
+}
+
+}  // namespace lr
+
+using namespace lr;
+
+extern "C" {
+
+long long lr_lu_workspace_doubles(int m, int n) {
+  LuPlan pl = lu_plan(m, n);
+  long long G = pl.G > 0 ? pl.G : 1;
+  return 4 * G + 2 * G * 32 + n + 8 + lr_stats_partials() + 8;
+}
+
+int lr_lu_pl_f64(int m, int n, double* X, long long ldx, double* work, double* status_host,
+                 void* stream) {
+  LR_REQUIRE(m >= n && n >= 1, "lu_pl requires m >= n, got %dx%d", m, n);
+  LR_REQUIRE(ldx >= n, "lu_pl: ldx < n");
+  cudaStream_t s = as_stream(stream);
+  LuPlan pl = lu_plan(m, n);
+  LR_REQUIRE(pl.G > 0, "lu_pl: %d rows do not fit the cooperative plan", m);
+  const long long G = pl.G;
+  double* cand = work;
+  double* prow = cand + 4 * G;
+  int* pivrow = reinterpret_cast<int*>(prow + 2 * G * 32);
+  double* status = prow + 2 * G * 32 + n;  // n ints fit in n doubles
+  double* stats = status + 4;
+  double* partial = stats + 4;
+  int st = lr_block_stats_f64(X, m, n, ldx, partial, stats, stream);
+  if (st) return st;
+  LR_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(double), s));
+  // status[0] preset to -3 (not run) so an early exit is visible
+  static bool attr = false;
+  if (!attr) {
+    LR_CHECK_CUDA(cudaFuncSetAttribute(lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr = true;
+  }
+  int max_blocks = 0;
+  LR_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks, lu_kernel, LU_THREADS, pl.smem));
+  LR_REQUIRE((long long)max_blocks * sm_count() >= G, "lu_pl: cooperative grid %lld exceeds residency %d",
+             G, max_blocks * sm_count());
+  LuParams prm;
+  prm.X = X;
+  prm.ldx = ldx;
+  prm.m = m;
+  prm.n = n;
+  prm.nb = pl.nb;
+  prm.rows_per = pl.rows_per;
+  prm.stats = stats;
+  prm.cand = cand;
+  prm.prow = prow;
+  prm.pivrow = pivrow;
+  prm.status = status;
+  void* args[] = {&prm};
+  LR_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)lu_kernel, dim3((unsigned)G), dim3(LU_THREADS), args,
+                                            pl.smem, s));
+  count_launches(1);
+  double host[8];
+  LR_CHECK_CUDA(cudaMemcpyAsync(host, status, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  LR_CHECK_CUDA(cudaMemcpyAsync(host + 4, stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  LR_CHECK_CUDA(cudaStreamSynchronize(s));
+  if (host[6] != 0.0) {
+    status_host[0] = -3.0;
+  } else if (host[5] == 0.0) {
+    status_host[0] = -2.0;
+  } else {
+    status_host[0] = host[0];
+    status_host[1] = host[1];
+    status_host[2] = host[2];
+  }
+  return LR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,427 @@
+// Sparse kernels of the hot path: SpMM over a row-compressed pattern (CSR for
+// Y*X, the persistent CSC copy for Y^T*X), the sampled dense-dense product,
+// and the fused SVT step (SDDMM + residual + in-place update of both copies).
+//
+// Roofline: these are gathers of dense rows (w or r doubles per stored entry)
+// that live in L2 (the dense operands of every BASELINE config fit in the
+// 126 MB L2), plus a compulsory HBM stream of 12 B/nnz (SpMM) or 40 B/nnz
+// (SVT step).  Work is split into "items" (a row, or a chunk of a long row)
+// so Zipf-shaped rows (cfg4: up to 26,744 entries) do not serialize a warp.
+#include "lr_common.cuh"
+
+namespace lr {
+
+struct Item {
+  int row, beg, end, slot;
+};
+
+__device__ __forceinline__ Item load_item(const int* __restrict__ items, const int* __restrict__ ptr,
+                                          int i) {
+  Item it;
+  if (items) {
+    int4 v = reinterpret_cast<const int4*>(items)[i];
+    it.row = v.x;
+    it.beg = v.y;
+    it.end = v.z;
+    it.slot = v.w;
+  } else {
+    it.row = i;
+    it.beg = __ldg(ptr + i);
+    it.end = __ldg(ptr + i + 1);
+    it.slot = -1;
+  }
+  return it;
+}
+
+// ------------------------------------------------------------------- SpMM
+// A group of G lanes owns one item; lane g covers column pairs
+// c = 2*(g + G*t), t < T, of a column tile of width 2*G*T starting at c0.
+// VEC2: double2 loads/stores (requires 16B-aligned rows); tail columns scalar.
+template <int G, int T, bool VEC2>
+__global__ void __launch_bounds__(256) spmm_kernel(const int* __restrict__ ptr,
+                                                   const int* __restrict__ idx,
+                                                   const double* __restrict__ val,
+                                                   const int* __restrict__ items, int n_items,
+                                                   const double* __restrict__ X, long long ldx, int w,
+                                                   double* __restrict__ Y, long long ldy,
+                                                   double* __restrict__ scratch, int n_tiles) {
+  constexpr int GROUPS = 32 / G;
+  constexpr int TILE = 2 * G * T;  // columns per tile
+  const int lane = threadIdx.x & 31;
+  const int g = lane % G;
+  const int grp = lane / G;
+  const long long warp_global = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long n_units = (long long)((n_items + GROUPS - 1) / GROUPS) * n_tiles;
+
+  for (long long u = warp_global; u < n_units; u += n_warps) {
+    const int tile = (int)(u % n_tiles);
+    const int item_i = (int)(u / n_tiles) * GROUPS + grp;
+    const bool active = item_i < n_items;
+    Item it{0, 0, 0, -1};
+    if (active) it = load_item(items, ptr, item_i);
+    const int c0 = tile * TILE;
+    double2 acc[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) acc[t] = make_double2(0.0, 0.0);
+
+    if (active) {
+      int e = it.beg;
+      // process 4 entries per step for memory-level parallelism
+      for (; e + 4 <= it.end; e += 4) {
+        int cj[4];
+        double vj[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          cj[q] = __ldg(idx + e + q);
+          vj[q] = __ldg(val + e + q);
+        }
+        double2 xv[4][T];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double* xr = X + (long long)cj[q] * ldx + c0;
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            const int c = 2 * (g + G * t);
+            if (VEC2 && c0 + c + 1 < w) {
+              xv[q][t] = __ldg(reinterpret_cast<const double2*>(xr + c));
+            } else {
+              xv[q][t].x = (c0 + c < w) ? __ldg(xr + c) : 0.0;
+              xv[q][t].y = (c0 + c + 1 < w) ? __ldg(xr + c + 1) : 0.0;
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            acc[t].x = fma(vj[q], xv[q][t].x, acc[t].x);
+            acc[t].y = fma(vj[q], xv[q][t].y, acc[t].y);
+          }
+      }
+      for (; e < it.end; ++e) {
+        const int cj = __ldg(idx + e);
+        const double vj = __ldg(val + e);
+        const double* xr = X + (long long)cj * ldx + c0;
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          const int c = 2 * (g + G * t);
+          double2 xv;
+          if (VEC2 && c0 + c + 1 < w) {
+            xv = __ldg(reinterpret_cast<const double2*>(xr + c));
+          } else {
+            xv.x = (c0 + c < w) ? __ldg(xr + c) : 0.0;
+            xv.y = (c0 + c + 1 < w) ? __ldg(xr + c + 1) : 0.0;
+          }
+          acc[t].x = fma(vj, xv.x, acc[t].x);
+          acc[t].y = fma(vj, xv.y, acc[t].y);
+        }
+      }
+      double* dst = (it.slot >= 0) ? (scratch + (long long)it.slot * w + c0)
+                                   : (Y + (long long)it.row * ldy + c0);
+      const bool dst_vec = VEC2 && (it.slot < 0 || (w % 2 == 0));
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        const int c = 2 * (g + G * t);
+        if (dst_vec && c0 + c + 1 < w) {
+          *reinterpret_cast<double2*>(dst + c) = acc[t];
+        } else {
+          if (c0 + c < w) dst[c] = acc[t].x;
+          if (c0 + c + 1 < w) dst[c + 1] = acc[t].y;
+        }
+      }
+    }
+  }
+}
+
+// sum partial rows of split items, in slot order
+__global__ void spmm_split_reduce_kernel(const int* __restrict__ splits, int n_splits,
+                                         const double* __restrict__ scratch, int w,
+                                         double* __restrict__ Y, long long ldy) {
+  const long long total = (long long)n_splits * w;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(t / w), c = (int)(t - (long long)s * w);
+    const int4 sp = reinterpret_cast<const int4*>(splits)[s];
+    double acc = 0.0;
+    for (int k = sp.y; k < sp.z; ++k) acc += scratch[(long long)k * w + c];
+    Y[(long long)sp.x * ldy + c] = acc;
+  }
+}
+
+// SpMV (w == 1): one warp per item, lanes stride the entries, tree-reduce.
+__global__ void __launch_bounds__(256) spmv_kernel(const int* __restrict__ ptr,
+                                                   const int* __restrict__ idx,
+                                                   const double* __restrict__ val,
+                                                   const int* __restrict__ items, int n_items,
+                                                   const double* __restrict__ X, long long ldx,
+                                                   double* __restrict__ Y, long long ldy,
+                                                   double* __restrict__ scratch) {
+  const int lane = threadIdx.x & 31;
+  const long long warp_global = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long i = warp_global; i < n_items; i += n_warps) {
+    Item it = load_item(items, ptr, (int)i);
+    double acc = 0.0;
+    for (int e = it.beg + lane; e < it.end; e += 32)
+      acc = fma(__ldg(val + e), __ldg(X + (long long)__ldg(idx + e) * ldx), acc);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      if (it.slot >= 0)
+        scratch[it.slot] = acc;
+      else
+        Y[(long long)it.row * ldy] = acc;
+    }
+  }
+}
+
+// --------------------------------------------------------------- SDDMM / SVT
+// One warp per item; the item's row of U*S is staged in shared memory
+// (broadcast reads); each lane owns one stored entry at a time and walks the
+// r columns of V[j,:] with double2 loads.
+constexpr int kSvtThreads = 256;
+constexpr int kSvtBlocksPerSm = 4;
+constexpr int kMaxRankSmem = 1024;  // per-warp staging of U*S (doubles)
+
+template <bool FUSED, bool VEC2>
+__global__ void __launch_bounds__(kSvtThreads) sddmm_kernel(
+    const int* __restrict__ ptr, const int* __restrict__ idx, const int* __restrict__ items,
+    int n_items, const double* __restrict__ U, long long ldu, const double* __restrict__ S,
+    const double* __restrict__ V, long long ldv, int r, double* __restrict__ x_out,
+    const double* __restrict__ m_vals, double* __restrict__ y_csr, double* __restrict__ y_csc,
+    const int* __restrict__ inv_perm, double step, int apply, double* __restrict__ partial) {
+  extern __shared__ double sh_us[];  // (threads/32) * r
+  __shared__ double red[32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* us = sh_us + wib * r;
+  const long long warp_global = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  double ss = 0.0, mx = 0.0;
+  for (long long i = warp_global; i < n_items; i += n_warps) {
+    Item it = load_item(items, ptr, (int)i);
+    __syncwarp();
+    for (int t = lane; t < r; t += 32) us[t] = U[(long long)it.row * ldu + t] * S[t];
+    __syncwarp();
+    for (int e = it.beg + lane; e < it.end; e += 32) {
+      const int j = __ldg(idx + e);
+      const double* vr = V + (long long)j * ldv;
+      double acc = 0.0;
+      int t = 0;
+      if (VEC2) {
+        for (; t + 1 < r; t += 2) {
+          double2 v2 = __ldg(reinterpret_cast<const double2*>(vr + t));
+          acc = fma(us[t], v2.x, acc);
+          acc = fma(us[t + 1], v2.y, acc);
+        }
+      }
+      for (; t < r; ++t) acc = fma(us[t], __ldg(vr + t), acc);
+      if (FUSED) {
+        const double mv = __ldg(m_vals + e);
+        const double d = acc - mv;
+        ss = fma(d, d, ss);
+        mx = fmax(mx, fabs(d));
+        if (apply) {
+          // Y.data += step * (m - x): same rounding sequence as numpy
+          const double ynew = add_rn(y_csr[e], mul_rn(step, add_rn(mv, -acc)));
+          y_csr[e] = ynew;
+          y_csc[__ldg(inv_perm + e)] = ynew;
+        }
+      } else {
+        x_out[e] = acc;
+      }
+    }
+  }
+  if (FUSED) {
+    double S2 = block_sum<kSvtThreads>(ss, red);
+    double M2 = block_max<kSvtThreads>(mx, red);
+    if (threadIdx.x == 0) {
+      partial[2 * blockIdx.x] = S2;
+      partial[2 * blockIdx.x + 1] = M2;
+    }
+  }
+}
+
+__global__ void svt_finish_kernel(const double* partial, int n, double* out2) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0, m = 0.0;
+    for (int i = 0; i < n; ++i) {
+      s += partial[2 * i];
+      m = fmax(m, partial[2 * i + 1]);
+    }
+    out2[0] = s;
+    out2[1] = m;
+  }
+}
+
+__global__ void pattern_axpy_kernel(double* __restrict__ y_csr, double* __restrict__ y_csc,
+                                    const int* __restrict__ inv_perm,
+                                    const double* __restrict__ delta, double alpha, long long nnz) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double d = (alpha == 1.0) ? delta[e] : alpha * delta[e];
+    const double ynew = add_rn(y_csr[e], d);
+    y_csr[e] = ynew;
+    if (y_csc) y_csc[inv_perm[e]] = ynew;
+  }
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <int G, int T, bool V2>
+static void launch_spmm_t(const int* ptr, const int* idx, const double* val, const int* items,
+                          int n_items, const double* X, long long ldx, int w, double* Y,
+                          long long ldy, double* scratch, cudaStream_t s) {
+  constexpr int TILE = 2 * G * T;
+  const int n_tiles = (w + TILE - 1) / TILE;
+  constexpr int GROUPS = 32 / G;
+  long long units = (long long)((n_items + GROUPS - 1) / GROUPS) * n_tiles;
+  long long blocks = (units + 7) / 8;  // 8 warps per block
+  long long cap = (long long)sm_count() * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  spmm_kernel<G, T, V2><<<(int)blocks, 256, 0, s>>>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy,
+                                                    scratch, n_tiles);
+}
+
+template <bool V2>
+static void dispatch_spmm(const int* ptr, const int* idx, const double* val, const int* items,
+                          int n_items, const double* X, long long ldx, int w, double* Y,
+                          long long ldy, double* scratch, cudaStream_t s) {
+  const int pairs = (w + 1) / 2;
+  if (pairs <= 1)
+    launch_spmm_t<1, 1, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+  else if (pairs <= 2)
+    launch_spmm_t<2, 1, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+  else if (pairs <= 4)
+    launch_spmm_t<4, 1, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+  else if (pairs <= 8)
+    launch_spmm_t<8, 1, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+  else if (pairs <= 16)
+    launch_spmm_t<16, 1, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+  else if (pairs <= 32)
+    launch_spmm_t<32, 1, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+  else if (pairs <= 64)
+    launch_spmm_t<32, 2, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+  else
+    launch_spmm_t<32, 3, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+}
+
+}  // namespace lr
+
+using namespace lr;
+
+extern "C" {
+
+int lr_svt_step_partials(void) { return sm_count() * kSvtBlocksPerSm * 2; }
+
+int lr_spmm_f64(const int* ptr, const int* idx, const double* val, int rows, const int* items,
+                int n_items, const int* splits, int n_splits, const double* X, long long ldx, int w,
+                double* Y, long long ldy, double* scratch, void* stream) {
+  LR_REQUIRE(w >= 0 && ldx >= w && ldy >= w, "spmm: bad widths (w=%d ldx=%lld ldy=%lld)", w, ldx,
+             ldy);
+  if (w == 0 || rows == 0) return LR_OK;
+  if (!items) n_items = rows;
+  LR_REQUIRE(n_splits == 0 || scratch, "spmm: split schedule needs scratch");
+  cudaStream_t s = as_stream(stream);
+  if (w == 1) {
+    long long blocks = ((long long)n_items + 7) / 8;
+    long long cap = (long long)sm_count() * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    spmv_kernel<<<(int)blocks, 256, 0, s>>>(ptr, idx, val, items, n_items, X, ldx, Y, ldy, scratch);
+  } else {
+    const bool v2 = (ldx % 2 == 0) && (ldy % 2 == 0) && aligned16(X) && aligned16(Y) &&
+                    (scratch == nullptr || aligned16(scratch));
+    if (v2)
+      dispatch_spmm<true>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+    else
+      dispatch_spmm<false>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+  }
+  LR_CHECK_LAUNCH();
+  if (n_splits > 0) {
+    long long total = (long long)n_splits * w;
+    long long blocks = (total + 255) / 256;
+    if (blocks > sm_count() * 8) blocks = sm_count() * 8;
+    spmm_split_reduce_kernel<<<(int)blocks, 256, 0, s>>>(splits, n_splits, scratch, w, Y, ldy);
+    LR_CHECK_LAUNCH();
+  }
+  return LR_OK;
+}
+
+static int launch_sddmm(bool fused, const int* ptr, const int* idx, int rows, const int* items,
+                        int n_items, const double* U, long long ldu, const double* S,
+                        const double* V, long long ldv, int r, double* x, const double* m_vals,
+                        double* y_csr, double* y_csc, const int* inv_perm, double step, int apply,
+                        double* partial, cudaStream_t s) {
+  LR_REQUIRE(r <= kMaxRankSmem, "sddmm: rank %d exceeds %d", r, kMaxRankSmem);
+  if (!items) n_items = rows;
+  const int blocks = sm_count() * kSvtBlocksPerSm;
+  const size_t smem = (size_t)(kSvtThreads / 32) * (r > 0 ? r : 1) * sizeof(double);
+  const bool v2 = (ldv % 2 == 0) && aligned16(V);
+  if (smem > 48 * 1024) {
+    if (fused) {
+      cudaFuncSetAttribute(sddmm_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(sddmm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    } else {
+      cudaFuncSetAttribute(sddmm_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(sddmm_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+  }
+#define LR_SDDMM_ARGS                                                                           \
+  ptr, idx, items, n_items, U, ldu, S, V, ldv, r, x, m_vals, y_csr, y_csc, inv_perm, step, apply, \
+      partial
+  if (fused) {
+    if (v2)
+      sddmm_kernel<true, true><<<blocks, kSvtThreads, smem, s>>>(LR_SDDMM_ARGS);
+    else
+      sddmm_kernel<true, false><<<blocks, kSvtThreads, smem, s>>>(LR_SDDMM_ARGS);
+  } else {
+    if (v2)
+      sddmm_kernel<false, true><<<blocks, kSvtThreads, smem, s>>>(LR_SDDMM_ARGS);
+    else
+      sddmm_kernel<false, false><<<blocks, kSvtThreads, smem, s>>>(LR_SDDMM_ARGS);
+  }
+#undef LR_SDDMM_ARGS
+  LR_CHECK_LAUNCH();
+  return LR_OK;
+}
+
+int lr_sddmm_f64(const int* ptr, const int* idx, int rows, const int* items, int n_items,
+                 const double* U, long long ldu, const double* S, const double* V, long long ldv,
+                 int r, double* x, void* stream) {
+  LR_REQUIRE(r >= 1, "sddmm: rank must be >= 1");
+  return launch_sddmm(false, ptr, idx, rows, items, n_items, U, ldu, S, V, ldv, r, x, nullptr,
+                      nullptr, nullptr, nullptr, 0.0, 0, nullptr, as_stream(stream));
+}
+
+int lr_svt_step_f64(const int* ptr, const int* idx, int rows, const int* items, int n_items,
+                    const double* U, long long ldu, const double* S, const double* V, long long ldv,
+                    int r, const double* m_vals, double* y_csr, double* y_csc, const int* inv_perm,
+                    double step, int apply, double* partial, int n_partial, double* out2,
+                    void* stream) {
+  cudaStream_t s = as_stream(stream);
+  const int blocks = sm_count() * kSvtBlocksPerSm;
+  LR_REQUIRE(n_partial >= 2 * blocks, "svt_step: partial buffer too small (%d < %d)", n_partial,
+             2 * blocks);
+  {
+    int st = launch_sddmm(true, ptr, idx, rows, items, n_items, U, ldu, S, V, ldv, r, nullptr,
+                          m_vals, y_csr, y_csc, inv_perm, step, apply, partial, s);
+    if (st != LR_OK) return st;
+  }
+  svt_finish_kernel<<<1, 32, 0, s>>>(partial, blocks, out2);
+  LR_CHECK_LAUNCH();
+  return LR_OK;
+}
+
+int lr_pattern_axpy_f64(double* y_csr, double* y_csc, const int* inv_perm, const double* delta,
+                        double alpha, long long nnz, void* stream) {
+  if (nnz == 0) return LR_OK;
+  long long blocks = (nnz + 255) / 256;
+  if (blocks > sm_count() * 8) blocks = sm_count() * 8;
+  pattern_axpy_kernel<<<(int)blocks, 256, 0, as_stream(stream)>>>(y_csr, y_csc, inv_perm, delta,
+                                                                  alpha, nnz);
+  LR_CHECK_LAUNCH();
+  return LR_OK;
+}
+
+}  // extern "C"

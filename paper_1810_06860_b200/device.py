@@ -1,0 +1,135 @@
+"""Device plumbing: CUDA availability, the working stream, padded dense
+blocks and a reusable scratch arena.
+
+Dense device blocks are torch float64 tensors viewed as (rows, cols) with
+row stride `ld` >= cols (ld rounded up to an even count so rows are 16-byte
+aligned for the double2 paths of the kernels).  torch owns every device
+buffer; the native library never allocates.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native
+
+F64 = torch.float64
+I32 = torch.int32
+
+# host<->device traffic of this process, for the bench's e2e accounting
+TRAFFIC = {"h2d": 0, "d2h": 0}
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_1810_06860_b200 needs a CUDA device (B200, sm_100a); it has no CPU fallback")
+    _native.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def ld(t) -> int:
+    """Row stride of a row-major (rows, cols) view."""
+    if t.dim() != 2:
+        raise ValueError("expected a 2-D block")
+    if t.stride(1) != 1 and t.shape[1] > 1:
+        raise ValueError("expected unit column stride")
+    return max(int(t.stride(0)), int(t.shape[1]), 1)
+
+
+def padded_ld(cols: int) -> int:
+    return max(2, (cols + 1) & ~1)
+
+
+def empty(rows: int, cols: int) -> torch.Tensor:
+    dev = require_cuda()
+    base = torch.empty((max(rows, 1), padded_ld(cols)), dtype=F64, device=dev)
+    return base[:rows, :cols]
+
+
+def zeros(rows: int, cols: int) -> torch.Tensor:
+    t = empty(rows, cols)
+    if rows and cols:
+        _native.call("lr_fill_f64", ptr(t), ld(t), rows, cols, 0.0, stream())
+    return t
+
+
+def vector(n: int) -> torch.Tensor:
+    return torch.empty(max(n, 1), dtype=F64, device=require_cuda())[:n]
+
+
+def to_device(x, *, copy=True) -> torch.Tensor:
+    """numpy/torch 2-D float64 -> device block with unit column stride."""
+    if isinstance(x, torch.Tensor):
+        if x.device.type == "cuda" and x.dtype == F64 and x.dim() == 2 and (x.stride(1) == 1 or x.shape[1] <= 1):
+            return x
+        x = x.detach()
+        if x.device.type == "cuda":
+            x = x.to(F64)
+            out = empty(*x.shape)
+            out.copy_(x)
+            return out
+        x = x.numpy()
+    a = np.asarray(x, dtype=np.float64)
+    if a.ndim != 2:
+        raise ValueError(f"expected a 2-D array, got shape {a.shape}")
+    out = empty(*a.shape)
+    if a.size:
+        host = torch.from_numpy(np.ascontiguousarray(a))
+        out.copy_(host, non_blocking=False)
+        TRAFFIC["h2d"] += a.nbytes
+    return out
+
+
+def to_host(t) -> np.ndarray:
+    if isinstance(t, np.ndarray):
+        return t
+    out = t.detach().contiguous().cpu().numpy()
+    TRAFFIC["d2h"] += out.nbytes
+    return out
+
+
+def int_buffer(a: np.ndarray) -> torch.Tensor:
+    h = np.ascontiguousarray(a, dtype=np.int32)
+    TRAFFIC["h2d"] += h.nbytes
+    return torch.from_numpy(h).to(require_cuda())
+
+
+def f64_buffer(a: np.ndarray) -> torch.Tensor:
+    h = np.ascontiguousarray(a, dtype=np.float64)
+    TRAFFIC["h2d"] += h.nbytes
+    return torch.from_numpy(h).to(require_cuda())
+
+
+class Arena:
+    """Named, grow-only scratch buffers (float64) reused across calls."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def get(self, name: str, ndoubles: int) -> torch.Tensor:
+        n = max(int(ndoubles), 1)
+        b = self._bufs.get(name)
+        if b is None or b.numel() < n:
+            b = torch.empty(int(n * 1.25) + 64, dtype=F64, device=require_cuda())
+            self._bufs[name] = b
+        return b
+
+
+_ARENA = None
+
+
+def arena() -> Arena:
+    global _ARENA
+    if _ARENA is None:
+        _ARENA = Arena()
+    return _ARENA

@@ -1,0 +1,441 @@
+"""Dense building blocks of the randomized SVDs, on the device.
+
+Drop-in for /root/reference/pkg/src/lowrank/linalg.py (same names, result
+types, orders, tolerances and error messages).  The LAPACK calls of the
+reference are replaced by the native library:
+
+  orth      Householder QR (dgeqrf/dorgqr)  -> CholeskyQR2 on DMMA Grams,
+            shifted CholeskyQR3 when the first Cholesky breaks down; the
+            |R_jj| collapse test uses R = R2 R1 (R3 R2 R1), whose diagonal is
+            the unique positive-diagonal R of X = QR       (linalg.py:101-124)
+  lu_pl     dgetrf + P L                    -> cooperative GEPP kernel
+                                                            (linalg.py:127-150)
+  sym_eig   dsyevd                          -> parallel block Jacobi
+                                                            (linalg.py:153-169)
+  eig_svd   dsyrk + dsyevd + dgemm          -> DMMA syrk + Jacobi + DMMA gemm
+                                                            (linalg.py:172-202)
+  oracle_svd dgesdd (dense, capped)         -> Gram + Jacobi, U re-orthonormalised
+            by CholeskyQR2 (orthonormal completion for null directions)
+                                                            (linalg.py:205-221)
+
+Public functions take and return numpy arrays (CUDA tensors pass through
+as tensors); the `*_dev` variants keep everything on the device and are what
+rsvd.py / completion.py call.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native, device
+from .errors import NumericalError, RankDeficiencyError, SizeCapError
+
+GRAM_RANK_TOL = 1e-12
+ORTH_RANK_TOL = 1e-12
+LU_PIVOT_TOL = 1e-14
+ORACLE_SVD_CAP = 2000
+JACOBI_MAX_SWEEPS = 60
+# "syevd": tridiagonalization + bisection + inverse iteration (default);
+# "syevj": parallel block Jacobi (relative accuracy, slower at large n)
+EIG_METHOD = "syevd"
+_U_ROUND = 2.0 ** -53
+
+
+@dataclass
+class SvdResult:
+    """Economic SVD triple with an explicit order ("ascending"/"descending")."""
+
+    U: np.ndarray
+    S: np.ndarray
+    V: np.ndarray
+    order: str
+
+    @property
+    def rank(self) -> int:
+        return self.S.shape[0]
+
+    def descending(self) -> "SvdResult":
+        if self.order == "descending":
+            return self
+        return SvdResult(self.U[:, ::-1], self.S[::-1], self.V[:, ::-1], "descending")
+
+    def ascending(self) -> "SvdResult":
+        if self.order == "ascending":
+            return self
+        return SvdResult(self.U[:, ::-1], self.S[::-1], self.V[:, ::-1], "ascending")
+
+    def truncate(self, k: int) -> "SvdResult":
+        d = self.descending()
+        return SvdResult(d.U[:, :k], d.S[:k], d.V[:, :k], "descending")
+
+    def reconstruct(self) -> np.ndarray:
+        return (self.U * self.S) @ self.V.T
+
+
+@dataclass
+class DevSvd:
+    """Device triple, always descending; S_host mirrors S for host decisions."""
+
+    U: object
+    S: object
+    V: object
+    S_host: np.ndarray
+
+    def to_host(self) -> SvdResult:
+        return SvdResult(device.to_host(self.U), self.S_host.copy(), device.to_host(self.V), "descending")
+
+
+# ------------------------------------------------------------------ helpers
+
+def _st():
+    return device.stream()
+
+
+def _gemm(transA, M, N, K, alpha, A, B, beta, C, flags=0, work_name="gemm_work"):
+    need = int(_native.load().lr_gemm_workspace_doubles(transA, M, N, K, flags))
+    work = device.arena().get(work_name, need) if need else None
+    _native.call("lr_gemm_f64", transA, M, N, K, alpha, device.ptr(A), device.ld(A), device.ptr(B),
+                 device.ld(B), beta, device.ptr(C), device.ld(C), flags, device.ptr(work),
+                 int(work.numel()) if work is not None else 0, _st(),
+                 meta={"M": M, "N": N, "K": K, "transA": transA, "flags": flags})
+    return C
+
+
+def gram_dev(A, out=None):
+    """A^T A (exactly symmetric, upper tiles mirrored)."""
+    rows, n = A.shape
+    if out is None:
+        out = device.empty(n, n)
+    return _gemm(1, n, n, rows, 1.0, A, A, 0.0, out, _native.LR_GEMM_SYRK_UPPER)
+
+
+def matmul_dev(A, B, out=None, b_upper=False):
+    """A (M x K) @ B (K x N)."""
+    M, K = A.shape
+    N = B.shape[1]
+    if out is None:
+        out = device.empty(M, N)
+    return _gemm(0, M, N, K, 1.0, A, B, 0.0, out, _native.LR_GEMM_B_UPPER if b_upper else 0)
+
+
+def matmul_tn_dev(A, B, out=None):
+    """A^T (M x K) @ B (K x N), A is K x M."""
+    K, M = A.shape
+    N = B.shape[1]
+    if out is None:
+        out = device.empty(M, N)
+    return _gemm(1, M, N, K, 1.0, A, B, 0.0, out, 0, "gemm_work_tn")
+
+
+def stats_dev(X):
+    """(sum of squares, max|x|, #non-finite) of a device block, one sync."""
+    rows, cols = X.shape
+    if rows * cols == 0:
+        return 0.0, 0.0, 0
+    part = device.arena().get("stats_partial", _native.load().lr_stats_partials() + 8)
+    out = device.vector(3)
+    _native.call("lr_block_stats_f64", device.ptr(X), rows, cols, device.ld(X), device.ptr(part),
+                 device.ptr(out), _st())
+    h = device.to_host(out)
+    return float(h[0]), float(h[1]), int(h[2])
+
+
+def _check_dev(X, name):
+    if X.dim() != 2 or X.shape[0] < 1 or X.shape[1] < 1:
+        raise ValueError(f"{name} must be 2-D with positive dims, got shape {tuple(X.shape)}")
+    s = stats_dev(X)
+    if s[2]:
+        raise ValueError(f"{name} contains non-finite entries")
+    return s
+
+
+def _fro_from_stats(s, X):
+    sumsq, big = s[0], s[1]
+    if big == 0.0:
+        return 0.0
+    if np.isfinite(sumsq) and 1e-150 < big < 1e150:
+        return float(np.sqrt(sumsq))
+    from .sparse import frobenius_dev
+
+    return frobenius_dev(X)
+
+
+def _diag_host(R, n):
+    d = device.vector(n)
+    _native.call("lr_diag_f64", device.ptr(R), device.ld(R), n, device.ptr(d), _st())
+    return device.to_host(d)
+
+
+def potrf_inv_dev(G, shift=0.0):
+    """In place upper Cholesky of G (+ shift I); returns (info, Rinv)."""
+    n = G.shape[0]
+    Rinv = device.empty(n, n)
+    work = device.arena().get("potrf_work", int(_native.load().lr_potrf_workspace_doubles(n)))
+    info = ctypes.c_int(0)
+    _native.call("lr_potrf_inv_f64", n, device.ptr(G), device.ld(G), float(shift), device.ptr(Rinv),
+                 device.ld(Rinv), device.ptr(work), ctypes.byref(info), _st())
+    return int(info.value), Rinv
+
+
+# --------------------------------------------------------------------- orth
+
+def _cholqr_pass(X, shift=0.0):
+    """One CholeskyQR pass: returns (info, Q, diag(R))."""
+    n = X.shape[1]
+    G = gram_dev(X)
+    info, Rinv = potrf_inv_dev(G, shift)
+    if info:
+        return info, None, None
+    diag = _diag_host(G, n)
+    Q = matmul_dev(X, Rinv, b_upper=True)
+    return 0, Q, diag
+
+
+def orth_dev(X):
+    """Orthonormal basis of range(X) (linalg.py:101-124), device in/out."""
+    s = _check_dev(X, "orth input")
+    m, n = X.shape
+    if m < n:
+        raise ValueError(f"orth requires m >= n, got {m}x{n}")
+    scale = _fro_from_stats(s, X)
+    if scale == 0.0:
+        raise RankDeficiencyError("cannot orthonormalize a zero matrix")
+    info, Q1, d1 = _cholqr_pass(X)
+    if info == 0:
+        info2, Q, d2 = _cholqr_pass(Q1)
+        if info2 == 0:
+            rdiag = d2 * d1
+            if np.max(np.abs(d2 - 1.0)) > 1e-6:  # Q1 was far from orthonormal: one more pass
+                info3, Q3, d3 = _cholqr_pass(Q)
+                if info3 == 0:
+                    Q, rdiag = Q3, d3 * rdiag
+    else:
+        info2 = 1
+    if info != 0 or info2 != 0:
+        # shifted CholeskyQR3 (Fukaya et al.): well defined for any full-rank X
+        shift = 11.0 * (m * n + n * (n + 1)) * _U_ROUND * scale * scale
+        info, Q1, d1 = _cholqr_pass(X, shift)
+        if info:
+            raise RankDeficiencyError(f"shifted Cholesky failed at column {info - 1}; cannot orthonormalize")
+        rdiag = d1
+        Q = Q1
+        for _ in range(2):
+            info, Qn, dn = _cholqr_pass(Q)
+            if info:
+                raise RankDeficiencyError(
+                    f"column norm collapse at column {info - 1} (|R[{info - 1},{info - 1}]| = 0.000e+00 < "
+                    f"{ORTH_RANK_TOL:.0e} * ||X||_F = {ORTH_RANK_TOL * scale:.3e})")
+            Q, rdiag = Qn, dn * rdiag
+    rdiag = np.abs(rdiag)
+    bad = np.flatnonzero(rdiag < ORTH_RANK_TOL * scale)
+    if bad.size:
+        j = int(bad[0])
+        raise RankDeficiencyError(
+            f"column norm collapse at column {j} (|R[{j},{j}]| = {rdiag[j]:.3e} < "
+            f"{ORTH_RANK_TOL:.0e} * ||X||_F = {ORTH_RANK_TOL * scale:.3e})")
+    return Q
+
+
+def _public(fn_dev, X, *args):
+    is_t = type(X).__module__.startswith("torch")
+    out = fn_dev(device.to_device(X), *args)
+    return out if is_t else device.to_host(out)
+
+
+def orth(X):
+    """Orthonormal basis of range(X) via CholeskyQR2 on the device."""
+    return _public(orth_dev, X)
+
+
+# -------------------------------------------------------------------- lu_pl
+
+def lu_pl_dev(X, inplace=True):
+    """P^T L of partial-pivoting LU (linalg.py:127-150); in place by default."""
+    if X.dim() != 2 or X.shape[0] < 1 or X.shape[1] < 1:
+        raise ValueError(f"lu input must be 2-D with positive dims, got shape {tuple(X.shape)}")
+    m, n = X.shape
+    if m < n:
+        raise ValueError(f"lu_pl requires m >= n, got {m}x{n}")
+    if not inplace:
+        Y = device.empty(m, n)
+        _native.call("lr_copy2d_f64", device.ptr(X), device.ld(X), device.ptr(Y), device.ld(Y), m, n, 0, _st())
+        X = Y
+    work = device.arena().get("lu_work", int(_native.load().lr_lu_workspace_doubles(m, n)))
+    status = (ctypes.c_double * 4)()
+    _native.call("lr_lu_pl_f64", m, n, device.ptr(X), device.ld(X), device.ptr(work), status, _st())
+    code = status[0]
+    if code == -3.0:
+        raise ValueError("lu input contains non-finite entries")
+    if code == -2.0:
+        raise RankDeficiencyError("cannot LU-factor a zero matrix")
+    if code >= 0.0:
+        j = int(code)
+        raise RankDeficiencyError(f"zero pivot at column {j} (|pivot| = {status[1]:.3e} < {status[2]:.3e})")
+    return X
+
+
+def lu_pl(X):
+    """Permuted lower-triangular LU factor spanning range(X)."""
+    is_t = type(X).__module__.startswith("torch")
+    Xd = device.to_device(X)
+    out = lu_pl_dev(Xd, inplace=Xd is not X)
+    return out if is_t else device.to_host(out)
+
+
+# ------------------------------------------------------------------ sym_eig
+
+def sym_eig_dev(B, symmetrize=True):
+    """(V, d) with d ascending (linalg.py:153-169); B is not modified."""
+    n = B.shape[0]
+    A = device.empty(n, n)
+    if symmetrize:
+        _native.call("lr_symmetrize_f64", device.ptr(B), device.ld(B), n, device.ptr(A), device.ld(A), _st())
+    else:
+        _native.call("lr_copy2d_f64", device.ptr(B), device.ld(B), device.ptr(A), device.ld(A), n, n, 0, _st())
+    d = device.vector(n)
+    V = device.empty(n, n)
+    if EIG_METHOD == "syevd":
+        work = device.arena().get("syevd_work", int(_native.load().lr_syevd_workspace_doubles(n)))
+        ncl = ctypes.c_int(0)
+        _native.call("lr_syevd_f64", n, device.ptr(A), device.ld(A), device.ptr(d), device.ptr(V), device.ld(V),
+                     device.ptr(work), ctypes.byref(ncl), _st(), meta={"n": n})
+        return V, d
+    work = device.arena().get("syevj_work", int(_native.load().lr_syevj_workspace_doubles(n)))
+    sweeps = ctypes.c_int(0)
+    try:
+        _native.call("lr_syevj_f64", n, device.ptr(A), device.ld(A), device.ptr(d), device.ptr(V), device.ld(V),
+                     JACOBI_MAX_SWEEPS, device.ptr(work), ctypes.byref(sweeps), _st(), meta={"n": n})
+    except NumericalError as exc:
+        raise NumericalError(f"symmetric eigensolver did not converge: {_native.last_error()}") from exc
+    return V, d
+
+
+def sym_eig(B):
+    """Eigendecomposition of (B + B^T)/2, eigenvalues ascending."""
+    Bd = device.to_device(B)
+    if Bd.dim() != 2 or Bd.shape[0] < 1 or Bd.shape[1] < 1:
+        raise ValueError(f"sym_eig input must be 2-D with positive dims, got shape {tuple(Bd.shape)}")
+    _check_dev(Bd, "sym_eig input")
+    if Bd.shape[0] != Bd.shape[1]:
+        raise ValueError(f"sym_eig needs a square matrix, got {tuple(Bd.shape)}")
+    V, d = sym_eig_dev(Bd)
+    if type(B).__module__.startswith("torch"):
+        return V, d
+    return device.to_host(V), device.to_host(d)
+
+
+# ------------------------------------------------------------------ eig_svd
+
+def eig_svd_dev(A, cols=None, check=True):
+    """Gram-route SVD of tall A (linalg.py:172-202), device in/out.
+
+    Returns (S_host ascending (all n), V (n x n, sign rule applied),
+    U_sel (rows x len(cols)) = A V[:, cols] / S[cols], cols) with cols an
+    index array into the ascending order (default: all, ascending).
+    """
+    if check:
+        _check_dev(A, "eig_svd input")
+    rows, n = A.shape
+    if rows < n:
+        raise ValueError(f"eig_svd requires m >= n, got {rows}x{n}")
+    G = gram_dev(A)
+    V, d = sym_eig_dev(G, symmetrize=False)
+    dh = device.to_host(d)
+    dmax = dh[-1]
+    if dmax <= 0.0:
+        raise RankDeficiencyError("Gram matrix has no positive eigenvalue (zero input?)")
+    bad = np.flatnonzero(dh <= GRAM_RANK_TOL * dmax)
+    if bad.size:
+        raise RankDeficiencyError(
+            f"Gram eigenvalue {bad.size} of {n} at/below rank tolerance "
+            f"(index {bad[0]}: {dh[bad[0]]:.3e} <= {GRAM_RANK_TOL:.0e} * {dmax:.3e})")
+    S = np.sqrt(np.maximum(dh, 0.0))
+    _native.call("lr_fix_signs_f64", device.ptr(V), device.ld(V), n, n, None, 0, 0, _st())
+    if cols is None:
+        cols = np.arange(n)
+    cols = np.asarray(cols, dtype=np.int64)
+    Sd = device.f64_buffer(S)
+    B = device.empty(n, cols.shape[0])
+    ci = device.int_buffer(cols)
+    _native.call("lr_scale_columns_f64", device.ptr(V), device.ld(V), n, device.ptr(ci), cols.shape[0],
+                 device.ptr(Sd), 1, device.ptr(B), device.ld(B), _st())
+    U = matmul_dev(A, B)
+    return S, V, U, cols
+
+
+def eig_svd(A) -> SvdResult:
+    """Economic SVD of a tall full-column-rank matrix via its Gram matrix;
+    singular values ascending."""
+    Ad = device.to_device(A)
+    S, V, U, _ = eig_svd_dev(Ad)
+    if type(A).__module__.startswith("torch"):
+        return SvdResult(U, device.f64_buffer(S), V, "ascending")
+    return SvdResult(device.to_host(U), S, device.to_host(V), "ascending")
+
+
+# --------------------------------------------------------------- oracle_svd
+
+def _tall_dense_svd_dev(A):
+    """Descending SVD of tall A on the device: Gram + Jacobi for V and S,
+    U = A V / S re-orthonormalised by CholeskyQR2 (null directions get an
+    orthonormal completion from a seeded Gaussian block)."""
+    rows, n = A.shape
+    G = gram_dev(A)
+    V, d = sym_eig_dev(G, symmetrize=False)
+    dh = device.to_host(d)[::-1].copy()  # descending
+    S = np.sqrt(np.maximum(dh, 0.0))
+    order = np.arange(n - 1, -1, -1)
+    Vd = device.empty(n, n)
+    oi = device.int_buffer(order)
+    _native.call("lr_scale_columns_f64", device.ptr(V), device.ld(V), n, device.ptr(oi), n, None, 0,
+                 device.ptr(Vd), device.ld(Vd), _st())
+    good = S > (S[0] * 1e-7 if S[0] > 0 else np.inf)
+    Ssafe = device.f64_buffer(np.where(good, S, 1.0))
+    B = device.empty(n, n)
+    _native.call("lr_scale_columns_f64", device.ptr(Vd), device.ld(Vd), n, None, n,
+                 device.ptr(Ssafe), 1, device.ptr(B), device.ld(B), _st())
+    U = matmul_dev(A, B)
+    nbad = int((~good).sum())
+    if nbad:
+        from .rng import gaussian_matrix_device
+
+        Z = gaussian_matrix_device(0x5EED, rows, nbad)
+        first_bad = n - nbad
+        _native.call("lr_copy2d_f64", device.ptr(Z), device.ld(Z), device.ptr(U[:, first_bad:]), device.ld(U),
+                     rows, nbad, 0, _st())
+    # re-orthonormalise (columns keep their order; good columns barely move)
+    for _ in range(2):
+        info, Qn, _d = _cholqr_pass(U)
+        if info:
+            shift = 11.0 * (rows * n + n * (n + 1)) * _U_ROUND * float(n)
+            info, Qn, _d = _cholqr_pass(U, shift)
+            if info:
+                raise NumericalError("dense SVD: could not orthonormalize the left factor")
+        U = Qn
+    _native.call("lr_fix_signs_f64", device.ptr(Vd), device.ld(Vd), n, n, device.ptr(U), device.ld(U), rows, _st())
+    return U, S, Vd
+
+
+def oracle_svd_dev(A):
+    """Full economic SVD, descending (linalg.py:205-221) -> (U, S_host, V)."""
+    _check_dev(A, "oracle_svd input")
+    m, n = A.shape
+    if min(m, n) > ORACLE_SVD_CAP:
+        raise SizeCapError(f"oracle SVD capped at min(m,n) <= {ORACLE_SVD_CAP}, got {m}x{n}")
+    if m >= n:
+        return _tall_dense_svd_dev(A)
+    At = device.empty(n, m)
+    _native.call("lr_transpose_f64", device.ptr(A), device.ld(A), m, n, device.ptr(At), device.ld(At), _st())
+    U2, S, V2 = _tall_dense_svd_dev(At)  # A^T = U2 S V2^T  ->  A = V2 S U2^T
+    # sign rule on A's V (= U2): first nonzero of each column >= 0
+    _native.call("lr_fix_signs_f64", device.ptr(U2), device.ld(U2), n, m, device.ptr(V2), device.ld(V2), m, _st())
+    return V2, S, U2
+
+
+def oracle_svd(A) -> SvdResult:
+    """Dense economic SVD (descending) on the device; desk-scale only."""
+    U, S, V = oracle_svd_dev(device.to_device(A))
+    return SvdResult(device.to_host(U), S, device.to_host(V), "descending")

@@ -1,0 +1,283 @@
+"""Randomized truncated SVDs of sparse matrices, on the device.
+
+Drop-in for /root/reference/pkg/src/lowrank/rsvd.py:
+  rsvd_bki  Alg. 5: LU-normalised Krylov blocks H_0..H_p written straight
+            into column slices of one m x W device block (no hstack), QR of
+            the block, B^T = Y^T Q on the CSC copy, Gram-route SVD with only
+            the top-k window lifted                          (rsvd.py:200-231)
+  rsvd_pi   Alg. 4: LU power iteration, Gram-route final basis (rsvd.py:168-197)
+  rsvd_basic Alg. 1 comparator (QR each product, dense small SVD)
+                                                              (rsvd.py:134-165)
+  qb_error  ||A - U S V^T||_F / ||A||_F without densifying   (rsvd.py:234-254)
+Rank deficiency reroutes through the dense device SVD when allow_fallback,
+else re-raises with the same advice suffixes (rsvd.py:81-126).
+
+Omega is gaussian_matrix(RngState(seed), n, k+s).  `omega="host"` (default)
+draws it with numpy on the host and uploads it -- the reference's own
+arithmetic; `omega="device"` generates the same Philox stream on the GPU
+(uniforms bit-exact, normals within a few ulp), avoiding the PCIe transfer.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native, device
+from .errors import RankDeficiencyError
+from .linalg import (DevSvd, SvdResult, eig_svd_dev, lu_pl_dev, matmul_dev, oracle_svd_dev, orth_dev)
+from .rng import RngState, gaussian_matrix, gaussian_matrix_device
+from .sparse import SparseMatrix, frobenius, spmm_dev, spmm_t_dev
+
+OMEGA_SOURCE = "host"
+
+
+@dataclass
+class RsvdParams:
+    """k target rank, p power/Krylov parameter, s oversampling, seed."""
+
+    k: int
+    p: int
+    s: int = 5
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.k < 1:
+            raise ValueError(f"rank k must be >= 1, got {self.k}")
+        if self.s < 0:
+            raise ValueError(f"oversampling s must be >= 0, got {self.s}")
+        if self.p < 0:
+            raise ValueError(f"power parameter p must be >= 0, got {self.p}")
+
+    def check_against(self, A: SparseMatrix, krylov: bool = False) -> None:
+        width = (self.k + self.s) * ((self.p + 1) if krylov else 1)
+        limit = min(A.rows, A.cols)
+        if width > limit:
+            raise ValueError(f"sketch width {width} exceeds min(m, n) = {limit}; reduce k, s or p")
+
+
+class Subspace:
+    """Orthonormal sketch basis (device resident; `.Q` downloads lazily)."""
+
+    def __init__(self, Q, provenance: str, p: int, fallbacks: int = 0):
+        self._Q = Q
+        self.provenance = provenance
+        self.p = p
+        self.fallbacks = fallbacks
+        self._Qh = None
+
+    @property
+    def Q(self) -> np.ndarray:
+        if isinstance(self._Q, np.ndarray):
+            return self._Q
+        if self._Qh is None:
+            self._Qh = device.to_host(self._Q)
+        return self._Qh
+
+    @property
+    def Q_dev(self):
+        if isinstance(self._Q, np.ndarray):
+            self._Q = device.to_device(self._Q)
+        return self._Q
+
+    @property
+    def width(self) -> int:
+        return int(self._Q.shape[1])
+
+
+class _Fallback:
+    __slots__ = ("enabled", "count", "advice")
+
+    def __init__(self, enabled: bool, advice: str):
+        self.enabled, self.count, self.advice = enabled, 0, advice
+
+    def fail(self, exc):
+        if not self.enabled:
+            if self.advice is None:
+                raise exc
+            raise RankDeficiencyError(f"{exc}; {self.advice}") from exc
+        self.count += 1
+
+
+def _copy(src, dst):
+    _native.call("lr_copy2d_f64", device.ptr(src), device.ld(src), device.ptr(dst), device.ld(dst),
+                 src.shape[0], src.shape[1], 0, device.stream())
+
+
+def _omega(seed: int, n: int, w: int, source: str):
+    if source == "device":
+        return gaussian_matrix_device(seed, n, w)
+    return device.to_device(gaussian_matrix(RngState(seed), n, w))
+
+
+def _lu_block(block, fb: _Fallback):
+    """LU-normalise a device block in place; dense-SVD basis on fallback."""
+    keep = None
+    if fb.enabled:
+        keep = device.empty(*block.shape)
+        _copy(block, keep)
+    try:
+        lu_pl_dev(block)
+    except RankDeficiencyError as exc:
+        fb.fail(exc)
+        U, _, _ = oracle_svd_dev(keep)
+        _copy(U, block)
+
+
+def _orthonormalize(X, fb: _Fallback):
+    try:
+        return orth_dev(X)
+    except RankDeficiencyError as exc:
+        fb.fail(exc)
+        return oracle_svd_dev(X)[0]
+
+
+def _windowed_small_svd(Bt, idx, fb: _Fallback):
+    """eig_svd of Bt (n x W) keeping the ascending-order columns idx (given in
+    the output order).  Returns (S_sel host, V_small[:, idx] device,
+    U_small[:, idx] device).  Falls back to the dense SVD (ascending)."""
+    try:
+        S, V, U, cols = eig_svd_dev(Bt, cols=idx)
+        Vsel = device.empty(V.shape[0], len(idx))
+        ci = device.int_buffer(cols)
+        _native.call("lr_scale_columns_f64", device.ptr(V), device.ld(V), V.shape[0], device.ptr(ci), len(idx),
+                     None, 0, device.ptr(Vsel), device.ld(Vsel), device.stream())
+        return S[cols], Vsel, U
+    except RankDeficiencyError as exc:
+        fb.fail(exc)
+        Ud, Sd, Vd = oracle_svd_dev(Bt)  # descending
+        W = Bt.shape[1]
+        desc = W - 1 - np.asarray(idx)  # ascending index -> descending position
+        ci = device.int_buffer(desc)
+        Vsel = device.empty(Vd.shape[0], len(idx))
+        Usel = device.empty(Ud.shape[0], len(idx))
+        _native.call("lr_scale_columns_f64", device.ptr(Vd), device.ld(Vd), Vd.shape[0], device.ptr(ci), len(idx),
+                     None, 0, device.ptr(Vsel), device.ld(Vsel), device.stream())
+        _native.call("lr_scale_columns_f64", device.ptr(Ud), device.ld(Ud), Ud.shape[0], device.ptr(ci), len(idx),
+                     None, 0, device.ptr(Usel), device.ld(Usel), device.stream())
+        return Sd[desc], Vsel, Usel
+
+
+def project_and_solve(Y: SparseMatrix, Q, k: int, fb: _Fallback):
+    """B^T = Y^T Q, small SVD, lift: the shared tail of Alg. 5 steps 8-10,
+    recycle_q and rsvd_pi.  Returns the top-k DevSvd (descending)."""
+    W = int(Q.shape[1])
+    Bt = spmm_t_dev(Y, Q)
+    idx = np.arange(W - 1, W - k - 1, -1)  # top-k of the ascending order, descending
+    S_sel, Vsel, Usel = _windowed_small_svd(Bt, idx, fb)
+    U = matmul_dev(Q, Vsel)
+    return DevSvd(U, device.f64_buffer(S_sel), Usel, np.asarray(S_sel, dtype=np.float64))
+
+
+def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, omega=None):
+    """Device Alg. 5 -> (DevSvd, Q device, fallbacks)."""
+    params.check_against(A, krylov=True)
+    fb = _Fallback(allow_fallback, "Krylov blocks are near-collinear, reduce p or use a larger matrix")
+    w = params.k + params.s
+    W = w * (params.p + 1)
+    m, n = A.shape
+    Om = _omega(params.seed, n, w, omega or OMEGA_SOURCE)
+    H = device.empty(m, W)
+    spmm_dev(A, Om, out=H[:, 0:w])
+    _lu_block(H[:, 0:w], fb)
+    T = device.empty(n, w)
+    for i in range(1, params.p + 1):
+        spmm_t_dev(A, H[:, (i - 1) * w:i * w], out=T)
+        spmm_dev(A, T, out=H[:, i * w:(i + 1) * w])
+        _lu_block(H[:, i * w:(i + 1) * w], fb)
+    Q = _orthonormalize(H, fb)
+    res = project_and_solve(A, Q, params.k, fb)
+    return res, Q, fb.count
+
+
+def rsvd_bki(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, *, omega=None):
+    """Rank-k randomized SVD by block Krylov iteration (descending)."""
+    res, Q, nfb = rsvd_bki_dev(A, params, allow_fallback, omega)
+    return res.to_host(), Subspace(Q, "bki", params.p, nfb)
+
+
+def rsvd_pi_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, omega=None):
+    params.check_against(A)
+    fb = _Fallback(allow_fallback, "increase s or reduce k")
+    w = params.k + params.s
+    m, n = A.shape
+    Om = _omega(params.seed, n, w, omega or OMEGA_SOURCE)
+    Q = spmm_dev(A, Om)
+    T = device.empty(n, w)
+    for _ in range(params.p):
+        _lu_block(Q, fb)
+        spmm_t_dev(A, Q, out=T)
+        spmm_dev(A, T, out=Q)
+    # final basis through the Gram-route SVD (all w columns, ascending)
+    try:
+        _, _, Q, _ = eig_svd_dev(Q)
+    except RankDeficiencyError as exc:
+        fb.fail(exc)
+        Q = oracle_svd_dev(Q)[0]
+    Bt = spmm_t_dev(A, Q)
+    idx = np.arange(params.k + params.s - 1, params.s - 1, -1)  # window [s, k+s), descending
+    S_sel, Vsel, Usel = _windowed_small_svd(Bt, idx, fb)
+    U = matmul_dev(Q, Vsel)
+    return DevSvd(U, device.f64_buffer(S_sel), Usel, np.asarray(S_sel)), Q, fb.count
+
+
+def rsvd_pi(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, *, omega=None):
+    """Rank-k randomized SVD with LU-renormalised power iteration."""
+    res, Q, nfb = rsvd_pi_dev(A, params, allow_fallback, omega)
+    return res.to_host(), Subspace(Q, "pi", params.p, nfb)
+
+
+def rsvd_basic(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, *, omega=None):
+    """Alg. 1 comparator: orthonormalise after every product, dense SVD of
+    the projected matrix (rsvd.py:134-165)."""
+    params.check_against(A)
+    fb = _Fallback(allow_fallback, "matrix rank is likely below k+s, reduce k")
+    w = params.k + params.s
+    Om = _omega(params.seed, A.cols, w, omega or OMEGA_SOURCE)
+    Q = _orthonormalize(spmm_dev(A, Om), fb)
+    for _ in range(params.p):
+        G = _orthonormalize(spmm_t_dev(A, Q), fb)
+        Q = _orthonormalize(spmm_dev(A, G), fb)
+    Bt = spmm_t_dev(A, Q)  # (Q^T A)^T, n x w; SVD of B = Q^T A from that of B^T
+    Ub, S, Vb = oracle_svd_dev(Bt)  # B^T = Ub S Vb^T -> B = Vb S Ub^T
+    _native.call("lr_fix_signs_f64", device.ptr(Ub), device.ld(Ub), Ub.shape[0], Ub.shape[1], device.ptr(Vb),
+                 device.ld(Vb), Vb.shape[0], device.stream())
+    k = params.k
+    U = matmul_dev(Q, Vb)
+    res = SvdResult(device.to_host(U)[:, :k], S[:k].copy(), device.to_host(Ub)[:, :k], "descending")
+    return res, Subspace(Q, "pi", params.p, fb.count)
+
+
+def qb_error(A: SparseMatrix, res: SvdResult) -> float:
+    """||A - U S V^T||_F / ||A||_F via ||A||^2 - 2<A V S, U> + ||S||^2."""
+    U, S, V = res.U, res.S, res.V
+    if U.shape[0] != A.rows or V.shape[0] != A.cols:
+        raise ValueError(f"factor dims {U.shape[0]}x{V.shape[0]} do not match matrix {A.shape}")
+    if U.shape[1] != S.shape[0] or V.shape[1] != S.shape[0]:
+        raise ValueError("factor rank mismatch")
+    a_norm = frobenius(A.data)
+    if a_norm == 0.0:
+        raise ValueError("relative error undefined for a zero matrix")
+    k = int(S.shape[0])
+    if k == 0:
+        return 1.0
+    Sh = np.asarray(S, dtype=np.float64)
+    Vd = device.to_device(V)
+    P = spmm_dev(A, Vd)  # m x k
+    Ud = device.to_device(U)
+    # cross = sum_ij P_ij S_j U_ij : scale U's columns by S, then a Frobenius inner product
+    Sd = device.f64_buffer(Sh)
+    US = device.empty(U.shape[0], k)
+    _native.call("lr_scale_columns_f64", device.ptr(Ud), device.ld(Ud), U.shape[0], None, k, device.ptr(Sd), 0,
+                 device.ptr(US), device.ld(US), device.stream())
+    # <P, US> = trace(P^T US): sum of the diagonal of a k x k product
+    G = device.empty(k, k)
+    from .linalg import matmul_tn_dev
+
+    matmul_tn_dev(P, US, out=G)
+    d = device.vector(k)
+    _native.call("lr_diag_f64", device.ptr(G), device.ld(G), k, device.ptr(d), device.stream())
+    cross = float(np.sum(device.to_host(d)))
+    sq = a_norm * a_norm - 2.0 * cross + float(Sh @ Sh)
+    return float(np.sqrt(max(sq, 0.0))) / a_norm

@@ -1,0 +1,505 @@
+"""Fixed-pattern sparse storage on the device and the sparse kernels of the
+SVT / rSVD path.
+
+Drop-in for /root/reference/pkg/src/lowrank/sparse.py:28-328 (the pattern,
+the products, the sampled product, the in-place update, the scaled norm, the
+spectral-norm estimate, and the observation sets).  Differences are in where
+the data lives, not in what is computed:
+
+* The pattern is built on the host exactly like the reference (lexsort by
+  (row, col), stable argsort for the transpose index: integer work, bit-exact)
+  and mirrored once on the device as int32 CSR + CSC + the CSC->CSR
+  permutation and its inverse.
+* The values keep TWO device copies, CSR order and CSC order, so Y^T X never
+  re-gathers A.data[perm] per call (sparse.py:166-169) and the fused SVT step
+  writes both copies in the same pass.
+* Work schedules ("items") split rows longer than SPLIT_CHUNK entries so
+  Zipf-shaped rows do not serialize a warp; partial rows are summed in fixed
+  slot order, so every product is deterministic.
+* `.data` stays a host numpy buffer with a stable identity: after device-side
+  updates it is refreshed in place on access.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native, device
+from .errors import DataError
+
+SPLIT_CHUNK = 512
+_SPECTRAL_TOL = 1e-3
+_SPECTRAL_MAX_ITERS = 200
+_SPECTRAL_BATCH = 8
+
+
+def _schedule(indptr: np.ndarray, chunk: int = SPLIT_CHUNK):
+    """Work items {row, beg, end, slot} (int32 x4) and split rows
+    {row, slot_beg, slot_end, 0}; (None, None, 0) when no row is split."""
+    lens = np.diff(indptr)
+    longm = lens > chunk
+    if not longm.any():
+        return None, None, 0
+    m = lens.shape[0]
+    per_row = np.where(longm, (lens + chunk - 1) // chunk, 1)
+    total = int(per_row.sum())
+    rows = np.repeat(np.arange(m, dtype=np.int64), per_row)
+    first = np.cumsum(per_row) - per_row
+    k = np.arange(total, dtype=np.int64) - np.repeat(first, per_row)
+    beg = indptr[rows] + k * chunk
+    end = np.minimum(beg + chunk, indptr[rows + 1])
+    is_long = np.repeat(longm, per_row)
+    slot = np.full(total, -1, dtype=np.int64)
+    n_slots = int(is_long.sum())
+    slot[is_long] = np.arange(n_slots)
+    items = np.stack([rows, beg, end, slot], axis=1).astype(np.int32)
+    long_rows = np.flatnonzero(longm)
+    s_cnt = per_row[long_rows]
+    s_beg = np.cumsum(s_cnt) - s_cnt
+    splits = np.stack([long_rows, s_beg, s_beg + s_cnt, np.zeros_like(long_rows)], axis=1).astype(np.int32)
+    return items, splits, n_slots
+
+
+class _Side:
+    """One compressed orientation of the pattern on the device."""
+
+    def __init__(self, ptr_host, idx_host, n_rows):
+        self.rows = int(n_rows)
+        self.ptr = device.int_buffer(ptr_host)
+        self.idx = device.int_buffer(idx_host)
+        items, splits, n_slots = _schedule(np.asarray(ptr_host, dtype=np.int64))
+        self.items = None if items is None else device.int_buffer(items.ravel())
+        self.n_items = self.rows if items is None else int(items.shape[0])
+        self.splits = None if splits is None else device.int_buffer(splits.ravel())
+        self.n_splits = 0 if splits is None else int(splits.shape[0])
+        self.n_slots = n_slots
+        self.max_len = int(np.max(np.diff(ptr_host))) if self.rows else 0
+
+
+class DevicePattern:
+    """CSR + CSC structure of one pattern on the device (shared by every
+    matrix with that pattern, e.g. Y and P_Phi(M) in the SVT loop)."""
+
+    def __init__(self, A: "SparseMatrix"):
+        m, n, nnz = A.rows, A.cols, A.nnz
+        self.shape = (m, n)
+        self.nnz = nnz
+        perm, t_indptr, t_indices = A._transpose_index()
+        inv = np.empty(nnz, dtype=np.int64)
+        inv[perm] = np.arange(nnz)
+        self.csr = _Side(A.indptr, A.indices, m)
+        self.csc = _Side(t_indptr, t_indices, n)
+        self.perm = device.int_buffer(perm)
+        self.inv_perm = device.int_buffer(inv)
+
+    def values(self, host_vals: np.ndarray):
+        """(csr, csc) device value copies of host values in CSR order."""
+        vc = device.f64_buffer(host_vals)
+        vt = device.vector(self.nnz)
+        if self.nnz:
+            _native.call("lr_gather_f64", device.ptr(vc), device.ptr(self.perm), device.ptr(vt),
+                         self.nnz, device.stream())
+        return vc, vt
+
+
+class SparseMatrix:
+    """CSR matrix with an immutable pattern (sparse.py:28-150 contract).
+
+    rows, cols; indptr / indices int64 host arrays (columns strictly
+    increasing within a row); data float64 (explicit zeros are legal).  The
+    sanctioned mutation is `update_pattern_values`.
+    """
+
+    def __init__(self, rows: int, cols: int, indptr, indices, data):
+        self.rows = int(rows)
+        self.cols = int(cols)
+        self.indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+        self.indices = np.ascontiguousarray(indices, dtype=np.int64)
+        self._data = np.ascontiguousarray(data, dtype=np.float64)
+        self._validate()
+        self._tperm = self._t_indptr = self._t_indices = self._coo_rows = None
+        self._pattern = None  # DevicePattern (shared structure)
+        self._dvals = None  # (csr, csc) device values
+        self._host_stale = False
+
+    # ------------------------------------------------------------ checks
+    def _validate(self) -> None:
+        if self.rows < 1 or self.cols < 1:
+            raise DataError(f"matrix dims must be positive, got {self.rows}x{self.cols}")
+        if self.indptr.shape != (self.rows + 1,):
+            raise DataError(f"indptr length {self.indptr.shape[0]} != rows + 1 = {self.rows + 1}")
+        if self.indptr[0] != 0 or np.any(self.indptr[1:] < self.indptr[:-1]):
+            raise DataError("row offsets must start at 0 and be monotone")
+        nnz = int(self.indptr[-1])
+        if self.indices.shape != (nnz,) or self._data.shape != (nnz,):
+            raise DataError("indices/data length must equal last row offset")
+        if nnz:
+            if self.indices.min() < 0 or self.indices.max() >= self.cols:
+                raise DataError("column index out of range")
+            step_ok = np.ones(max(nnz - 1, 0), dtype=bool)
+            inner = np.diff(self.indices) > 0
+            row_start = self.indptr[1:-1]
+            row_start = row_start[(row_start > 0) & (row_start < nnz)]
+            at_break = np.zeros(max(nnz - 1, 0), dtype=bool)
+            at_break[row_start - 1] = True
+            step_ok = inner | at_break
+            if not step_ok.all():
+                raise DataError("column indices must strictly increase within a row")
+        if not np.isfinite(self._data).all():
+            raise DataError("matrix values must be finite")
+
+    # ------------------------------------------------------ construction
+    @classmethod
+    def from_coo(cls, rows: int, cols: int, i, j, v) -> "SparseMatrix":
+        """Coordinate triples -> CSR (lexsort by row then column); duplicates
+        raise DataError (sparse.py:84-104)."""
+        i = np.asarray(i, dtype=np.int64)
+        j = np.asarray(j, dtype=np.int64)
+        v = np.asarray(v, dtype=np.float64)
+        if not (i.shape == j.shape == v.shape) or i.ndim != 1:
+            raise DataError("coordinate arrays must be 1-D and equal length")
+        if i.size and (i.min() < 0 or i.max() >= rows or j.min() < 0 or j.max() >= cols):
+            raise DataError("coordinate out of range")
+        order = np.lexsort((j, i))
+        i, j, v = i[order], j[order], v[order]
+        if i.size > 1:
+            dup = (i[1:] == i[:-1]) & (j[1:] == j[:-1])
+            if dup.any():
+                k = int(np.argmax(dup))
+                raise DataError(f"duplicate entry at ({i[k]}, {j[k]})")
+        indptr = np.zeros(rows + 1, dtype=np.int64)
+        np.cumsum(np.bincount(i, minlength=rows), out=indptr[1:])
+        return cls(rows, cols, indptr, j, v)
+
+    @classmethod
+    def identity(cls, n: int) -> "SparseMatrix":
+        ar = np.arange(n, dtype=np.int64)
+        return cls(n, n, np.arange(n + 1, dtype=np.int64), ar, np.ones(n))
+
+    # --------------------------------------------------------- structure
+    @property
+    def nnz(self) -> int:
+        return int(self.indptr[-1])
+
+    @property
+    def shape(self):
+        return (self.rows, self.cols)
+
+    @property
+    def data(self) -> np.ndarray:
+        if self._host_stale:
+            self._data[...] = device.to_host(self._dvals[0])
+            self._host_stale = False
+        return self._data
+
+    def coo_rows(self) -> np.ndarray:
+        if self._coo_rows is None:
+            self._coo_rows = np.repeat(np.arange(self.rows, dtype=np.int64), np.diff(self.indptr))
+        return self._coo_rows
+
+    def _transpose_index(self):
+        # stable sort by column keeps rows ascending inside each column
+        if self._tperm is None:
+            self._tperm = np.argsort(self.indices, kind="stable")
+            t_indptr = np.zeros(self.cols + 1, dtype=np.int64)
+            np.cumsum(np.bincount(self.indices, minlength=self.cols), out=t_indptr[1:])
+            self._t_indptr = t_indptr
+            self._t_indices = self.coo_rows()[self._tperm]
+        return self._tperm, self._t_indptr, self._t_indices
+
+    def densify(self) -> np.ndarray:
+        out = np.zeros(self.shape)
+        out[self.coo_rows(), self.indices] = self.data
+        return out
+
+    # ------------------------------------------------------------ device
+    def pattern(self) -> DevicePattern:
+        if self._pattern is None:
+            self._pattern = DevicePattern(self)
+        return self._pattern
+
+    def share_pattern(self, other: "SparseMatrix") -> None:
+        """Reuse other's device structure (same indptr/indices objects)."""
+        if other._pattern is not None:
+            self._pattern = other._pattern
+            self._tperm, self._t_indptr, self._t_indices = other._tperm, other._t_indptr, other._t_indices
+            self._coo_rows = other._coo_rows
+
+    def device_values(self):
+        """(csr, csc) device value vectors, created from the host data once."""
+        if self._dvals is None:
+            self._dvals = self.pattern().values(self._data)
+        return self._dvals
+
+
+# --------------------------------------------------------------- kernels
+
+def _spmm_side(side: _Side, vals, X, out=None):
+    rows_out = side.rows
+    w = int(X.shape[1])
+    if out is None:
+        out = device.empty(rows_out, w)
+    scratch = None
+    if side.n_splits:
+        scratch = device.arena().get("spmm_scratch", side.n_slots * max(w, 1) + 2)
+    _native.call("lr_spmm_f64", device.ptr(side.ptr), device.ptr(side.idx), device.ptr(vals), side.rows,
+                 device.ptr(side.items), side.n_items if side.items is not None else side.rows,
+                 device.ptr(side.splits), side.n_splits, device.ptr(X), device.ld(X), w,
+                 device.ptr(out), device.ld(out), device.ptr(scratch), device.stream(),
+                 meta={"nnz": int(side.idx.numel()), "rows": side.rows, "cols": int(X.shape[0]), "w": w})
+    return out
+
+
+def spmm_dev(A: SparseMatrix, X, out=None):
+    """Device Y @ X (X: n x w device block) -> m x w device block."""
+    return _spmm_side(A.pattern().csr, A.device_values()[0], X, out)
+
+
+def spmm_t_dev(A: SparseMatrix, H, out=None):
+    """Device Y^T @ H (H: m x w device block) -> n x w device block."""
+    return _spmm_side(A.pattern().csc, A.device_values()[1], H, out)
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def spmm(A: SparseMatrix, X):
+    """A @ X (sparse.py:153-158).  numpy in -> numpy out; CUDA tensor in ->
+    CUDA tensor out."""
+    if X is None or np.ndim(X) != 2 or A.cols != X.shape[0]:
+        shp = getattr(X, "shape", None)
+        raise ValueError(f"spmm dimension mismatch: {A.shape} @ {shp}")
+    out = spmm_dev(A, device.to_device(X))
+    return out if _is_torch(X) else device.to_host(out)
+
+
+def spmm_t(A: SparseMatrix, X):
+    """A.T @ X via the persistent CSC copy (sparse.py:161-170)."""
+    if X is None or np.ndim(X) != 2 or A.rows != X.shape[0]:
+        shp = getattr(X, "shape", None)
+        raise ValueError(f"spmm_t dimension mismatch: {A.shape}^T @ {shp}")
+    out = spmm_t_dev(A, device.to_device(X))
+    return out if _is_torch(X) else device.to_host(out)
+
+
+def project_pattern_dev(U, S, V, pattern: SparseMatrix, out=None):
+    dp = pattern.pattern()
+    r = int(S.shape[0])
+    if out is None:
+        out = device.vector(pattern.nnz)
+    if pattern.nnz == 0:
+        return out
+    if r == 0:
+        _native.call("lr_fill_f64", device.ptr(out), 1, pattern.nnz, 1, 0.0, device.stream())
+        return out
+    _native.call("lr_sddmm_f64", device.ptr(dp.csr.ptr), device.ptr(dp.csr.idx), dp.csr.rows,
+                 device.ptr(dp.csr.items), dp.csr.n_items, device.ptr(U), device.ld(U), device.ptr(S),
+                 device.ptr(V), device.ld(V), r, device.ptr(out), device.stream())
+    return out
+
+
+def _vec_dev(x):
+    import torch
+
+    if isinstance(x, torch.Tensor) and x.device.type == "cuda":
+        return x.to(torch.float64).contiguous()
+    return device.f64_buffer(np.asarray(x, dtype=np.float64).ravel())
+
+
+def project_pattern(U, S, V, pattern: SparseMatrix):
+    """Entries of U diag(S) V^T on the pattern, CSR order (sparse.py:173-191)."""
+    if U.shape[0] != pattern.rows or V.shape[0] != pattern.cols:
+        raise ValueError("factor dims do not match pattern dims")
+    if U.shape[1] != S.shape[0] or V.shape[1] != S.shape[0]:
+        raise ValueError("factor rank mismatch")
+    r = int(S.shape[0])
+    Ud = device.to_device(U) if r else None
+    Vd = device.to_device(V) if r else None
+    out = project_pattern_dev(Ud, _vec_dev(S), Vd, pattern)
+    return out if _is_torch(U) else device.to_host(out)
+
+
+def project_observed(U, S, V, obs: "ObservationSet"):
+    """Sampled entries of U diag(S) V^T on the train split of obs."""
+    if U.shape[0] != obs.m or V.shape[0] != obs.n:
+        raise ValueError("factor dims do not match observation dims")
+    if U.shape[1] != S.shape[0] or V.shape[1] != S.shape[0]:
+        raise ValueError("factor rank mismatch")
+    mask = obs.split == ObservationSet.TRAIN
+    return sample_at(U, S, V, obs.rows[mask], obs.cols[mask])
+
+
+def sample_at(U, S, V, rows, cols):
+    """U diag(S) V^T at arbitrary (rows, cols), in the given order."""
+    n_e = int(rows.shape[0])
+    r = int(S.shape[0])
+    out = device.vector(n_e)
+    if n_e == 0:
+        return device.to_host(out)
+    if r == 0:
+        return np.zeros(n_e)
+    # every entry is its own "row" of a pattern with rows -> U rows via items
+    items = np.stack([np.asarray(rows, np.int64), np.arange(n_e), np.arange(n_e) + 1,
+                      np.full(n_e, -1)], axis=1).astype(np.int32)
+    d_items = device.int_buffer(items.ravel())
+    d_idx = device.int_buffer(np.asarray(cols))
+    Ud, Vd, Sd = device.to_device(U), device.to_device(V), _vec_dev(S)
+    _native.call("lr_sddmm_f64", device.ptr(d_idx), device.ptr(d_idx), n_e, device.ptr(d_items), n_e,
+                 device.ptr(Ud), device.ld(Ud), device.ptr(Sd), device.ptr(Vd), device.ld(Vd), r,
+                 device.ptr(out), device.stream())
+    return device.to_host(out)
+
+
+def update_pattern_values(Y: SparseMatrix, delta_vals) -> SparseMatrix:
+    """Y.data += delta_vals in place on the device (both value copies); the
+    pattern and the host buffer identity are untouched (sparse.py:205-216)."""
+    if tuple(np.shape(delta_vals)) != (Y.nnz,):
+        raise ValueError(f"delta length {tuple(np.shape(delta_vals))} != nnz {Y.nnz}")
+    vc, vt = Y.device_values()
+    d = _vec_dev(delta_vals)
+    _native.call("lr_pattern_axpy_f64", device.ptr(vc), device.ptr(vt), device.ptr(Y.pattern().inv_perm),
+                 device.ptr(d), 1.0, Y.nnz, device.stream())
+    Y._host_stale = True
+    return Y
+
+
+def _stats(x, rows, cols, ldx):
+    part = device.arena().get("stats_partial", _native.load().lr_stats_partials() + 8)
+    out = device.vector(3)
+    _native.call("lr_block_stats_f64", device.ptr(x), rows, cols, ldx, device.ptr(part), device.ptr(out),
+                 device.stream())
+    return out
+
+
+def frobenius_dev(x) -> float:
+    """Scaled-safe Euclidean norm of a device vector/block (one sync)."""
+    if x.dim() == 1:
+        rows, cols, ldx = x.shape[0], 1, 1
+    else:
+        rows, cols, ldx = x.shape[0], x.shape[1], device.ld(x)
+    if rows * cols == 0:
+        return 0.0
+    s = device.to_host(_stats(x, rows, cols, ldx))
+    sumsq, big = float(s[0]), float(s[1])
+    if big == 0.0:
+        return 0.0
+    if np.isfinite(sumsq) and 1e-150 < big < 1e150:
+        return float(np.sqrt(sumsq))
+    # rescale on the device when squares would over/underflow
+    y = device.empty(rows, cols)
+    scale = device.f64_buffer(np.full(max(cols, 1), big))
+    _native.call("lr_scale_columns_f64", device.ptr(x), ldx, rows, None, cols, device.ptr(scale), 1,
+                 device.ptr(y), device.ld(y), device.stream())
+    s2 = device.to_host(_stats(y, rows, cols, device.ld(y)))
+    return float(big * np.sqrt(s2[0]))
+
+
+def frobenius(values) -> float:
+    """Euclidean norm with overflow-safe scaling (sparse.py:219-228)."""
+    if _is_torch(values):
+        return frobenius_dev(values.reshape(-1))
+    v = np.asarray(values, dtype=np.float64).ravel()
+    if v.size == 0:
+        return 0.0
+    return frobenius_dev(device.f64_buffer(v))
+
+
+def spectral_norm_est_dev(A: SparseMatrix, x0_host: np.ndarray) -> float:
+    """Power iteration on A^T A from x0 (sparse.py:231-256): stop at 1e-3
+    relative agreement or 200 steps; return the larger of the last two."""
+    n, m = A.cols, A.rows
+    # unit-stride (n, 1) views: the dot / power kernels treat them as flat vectors
+    x = device.f64_buffer(np.asarray(x0_host, dtype=np.float64).ravel()).view(n, 1)
+    part = device.arena().get("power_partial", 2 * 4096)
+    nrm2 = device.vector(1)
+    _native.call("lr_dot_f64", device.ptr(x), device.ptr(x), n, device.ptr(part), device.ptr(nrm2),
+                 device.stream())
+    nrm = float(np.sqrt(device.to_host(nrm2)[0]))
+    inv = device.f64_buffer(np.array([nrm]))
+    xs = device.vector(n).view(n, 1)
+    _native.call("lr_scale_columns_f64", device.ptr(x), 1, n, None, 1, device.ptr(inv), 1,
+                 device.ptr(xs), 1, device.stream())
+    x = xs
+    y = device.vector(m).view(m, 1)
+    z = device.vector(n).view(n, 1)
+    state = device.f64_buffer(np.zeros(6))
+    for it in range(_SPECTRAL_MAX_ITERS):
+        if it and it % _SPECTRAL_BATCH == 0 and device.to_host(state)[2] != 0.0:
+            break
+        spmm_dev(A, x, out=y)
+        spmm_t_dev(A, y, out=z)
+        _native.call("lr_power_update_f64", device.ptr(x), device.ptr(z), n, _SPECTRAL_TOL,
+                     device.ptr(state), device.ptr(part), device.stream())
+    st = device.to_host(state)
+    if st[4] != 0.0:
+        return 0.0
+    return float(max(st[0], st[1]))
+
+
+def spectral_norm_est(A: SparseMatrix, rng) -> float:
+    """Largest singular value estimate (sparse.py:231-256); the starting
+    vector comes from rng.normal_pairs(A.cols) as in the reference."""
+    if A.nnz < 1:
+        raise ValueError("spectral norm estimate needs at least one stored entry")
+    return spectral_norm_est_dev(A, rng.normal_pairs(A.cols))
+
+
+class ObservationSet:
+    """Split-tagged coordinate samples (sparse.py:259-328): TRAIN = 0,
+    TEST = 1; duplicate cells within a split are rejected."""
+
+    TRAIN = 0
+    TEST = 1
+
+    def __init__(self, m: int, n: int, rows, cols, values, split=None):
+        self.m = int(m)
+        self.n = int(n)
+        self.rows = np.ascontiguousarray(rows, dtype=np.int64)
+        self.cols = np.ascontiguousarray(cols, dtype=np.int64)
+        self.values = np.ascontiguousarray(values, dtype=np.float64)
+        if split is None:
+            split = np.zeros(self.rows.shape[0], dtype=np.uint8)
+        self.split = np.ascontiguousarray(split, dtype=np.uint8)
+        self._validate()
+
+    def _validate(self) -> None:
+        if self.m < 1 or self.n < 1:
+            raise DataError(f"observation dims must be positive, got {self.m}x{self.n}")
+        cnt = self.rows.shape[0]
+        if not (self.cols.shape[0] == self.values.shape[0] == self.split.shape[0] == cnt):
+            raise DataError("observation arrays must have equal length")
+        if cnt:
+            if self.rows.min() < 0 or self.rows.max() >= self.m:
+                raise DataError("observation row index out of range")
+            if self.cols.min() < 0 or self.cols.max() >= self.n:
+                raise DataError("observation col index out of range")
+        if not np.isfinite(self.values).all():
+            raise DataError("observation values must be finite")
+        if np.any(self.split > 1):
+            raise DataError("split tags must be 0 (train) or 1 (test)")
+        for tag, name in ((self.TRAIN, "train"), (self.TEST, "test")):
+            sel = self.split == tag
+            key = self.rows[sel] * self.n + self.cols[sel]
+            if key.size != np.unique(key).size:
+                raise DataError(f"duplicate (row, col) within {name} split")
+
+    @property
+    def count(self) -> int:
+        return self.rows.shape[0]
+
+    @property
+    def train_count(self) -> int:
+        return int(np.count_nonzero(self.split == self.TRAIN))
+
+    @property
+    def test_count(self) -> int:
+        return int(np.count_nonzero(self.split == self.TEST))
+
+    def subset(self, tag: int):
+        sel = self.split == tag
+        return self.rows[sel], self.cols[sel], self.values[sel]
+
+    def train_matrix(self) -> SparseMatrix:
+        r, c, v = self.subset(self.TRAIN)
+        return SparseMatrix.from_coo(self.m, self.n, r, c, v)

@@ -1,0 +1,315 @@
+"""GPU parity of the individual kernels against the CPU oracle (oracle/),
+on seeded inputs.  Tolerances are the reference's own:
+SpMM 1e-12 * ||ref||, SDDMM 1e-12, eigSVD values 1e-10 relative,
+projectors 1e-8..1e-10; integer/structural results exact."""
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+lr = pytest.importorskip("paper_1810_06860_b200")
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def rand_pattern(m, n, nnz, seed, long_rows=0, long_cols=0):
+    rng = np.random.default_rng(seed)
+    flat = rng.choice(m * n, size=nnz, replace=False)
+    i, j = np.divmod(flat, n)
+    extra_i, extra_j = [], []
+    for r in range(long_rows):  # fully dense rows (exercise the split schedule)
+        extra_i.append(np.full(n, r))
+        extra_j.append(np.arange(n))
+    for c in range(long_cols):
+        extra_i.append(np.arange(m))
+        extra_j.append(np.full(m, n - 1 - c))
+    if extra_i:
+        i = np.concatenate([i] + extra_i)
+        j = np.concatenate([j] + extra_j)
+        key = np.unique(i * n + j)
+        i, j = np.divmod(key, n)
+    v = rng.standard_normal(i.shape[0])
+    return i, j, v
+
+
+@pytest.mark.parametrize("w", [1, 2, 3, 7, 16, 33, 64, 65, 110, 131, 200])
+def test_spmm_and_spmm_t_match_oracle(w):
+    from paper_1810_06860_b200.sparse import SparseMatrix, spmm, spmm_t
+
+    m, n = 700, 1300
+    i, j, v = rand_pattern(m, n, 20000, seed=w, long_rows=2, long_cols=1)
+    A = SparseMatrix.from_coo(m, n, i, j, v)
+    P = oracle.csr_from_triples(m, n, i, j, v)
+    rng = np.random.default_rng(100 + w)
+    X = rng.standard_normal((n, w))
+    H = rng.standard_normal((m, w))
+    ref = oracle.csr_times_dense(P, X)
+    assert np.linalg.norm(spmm(A, X) - ref) <= 1e-12 * np.linalg.norm(ref)
+    ref_t = oracle.csr_t_times_dense(P, H)
+    assert np.linalg.norm(spmm_t(A, H) - ref_t) <= 1e-12 * np.linalg.norm(ref_t)
+
+
+def test_spmm_golden(golden):
+    from paper_1810_06860_b200.sparse import SparseMatrix, spmm, spmm_t
+
+    A = SparseMatrix.from_coo(60, 45, golden["sp_i"], golden["sp_j"], golden["sp_v"])
+    assert np.array_equal(A.indptr, golden["sp_indptr"]) and np.array_equal(A.indices, golden["sp_indices"])
+    perm, tip, tix = A._transpose_index()
+    assert np.array_equal(perm, golden["sp_tperm"]) and np.array_equal(tix, golden["sp_tindices"])
+    assert rel(spmm(A, golden["sp_X"]), golden["sp_spmm"]) <= 1e-12
+    assert rel(spmm_t(A, golden["sp_H"]), golden["sp_spmm_t"]) <= 1e-12
+
+
+def test_spmm_empty_rows_and_identity():
+    from paper_1810_06860_b200.sparse import SparseMatrix, spmm, spmm_t
+
+    A = SparseMatrix.from_coo(5, 4, [0, 4], [1, 3], [2.0, -1.0])  # rows 1..3 empty
+    X = np.arange(12.0).reshape(4, 3)
+    np.testing.assert_array_equal(spmm(A, X), A.densify() @ X)
+    H = np.arange(15.0).reshape(5, 3)
+    np.testing.assert_array_equal(spmm_t(A, H), A.densify().T @ H)
+    I = SparseMatrix.identity(9)
+    Z = np.random.default_rng(0).standard_normal((9, 4))
+    np.testing.assert_array_equal(spmm(I, Z), Z)
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        spmm(A, np.ones((5, 2)))
+
+
+def test_sddmm_and_frobenius(golden):
+    from paper_1810_06860_b200.sparse import SparseMatrix, frobenius, project_pattern
+
+    A = SparseMatrix.from_coo(60, 45, golden["sp_i"], golden["sp_j"], golden["sp_v"])
+    x = project_pattern(golden["sp_U"], golden["sp_S"], golden["sp_V"], A)
+    assert rel(x, golden["sp_project"]) <= 1e-12
+    assert abs(frobenius(A.data) - float(golden["sp_frob"])) <= 1e-14 * float(golden["sp_frob"])
+    assert frobenius(np.array([3.0, 4.0])) == 5.0
+    assert frobenius(np.zeros(0)) == 0.0 and frobenius(np.zeros(7)) == 0.0
+    assert abs(frobenius(np.array([3e200, 4e200])) - 5e200) <= 1e-14 * 5e200
+
+
+def test_update_pattern_values_both_copies():
+    from paper_1810_06860_b200.sparse import SparseMatrix, spmm, spmm_t, update_pattern_values
+
+    i, j, v = rand_pattern(80, 50, 900, seed=3)
+    A = SparseMatrix.from_coo(80, 50, i, j, v)
+    data_id = id(A.data)
+    X = np.random.default_rng(1).standard_normal((50, 4))
+    spmm(A, X)  # materialise device copies
+    delta = np.random.default_rng(2).standard_normal(A.nnz)
+    update_pattern_values(A, delta)
+    assert id(A.data) == data_id
+    np.testing.assert_allclose(A.data, v[np.lexsort((j, i))] + delta, rtol=0, atol=0)
+    D = A.densify()
+    np.testing.assert_allclose(spmm(A, X), D @ X, rtol=1e-12, atol=1e-12)
+    H = np.random.default_rng(3).standard_normal((80, 4))
+    np.testing.assert_allclose(spmm_t(A, H), D.T @ H, rtol=1e-12, atol=1e-12)
+
+
+def test_spectral_norm_matches_oracle(golden):
+    from paper_1810_06860_b200.rng import RngState
+    from paper_1810_06860_b200.sparse import SparseMatrix, spectral_norm_est
+
+    A = SparseMatrix.from_coo(60, 45, golden["sp_i"], golden["sp_j"], golden["sp_v"])
+    got = spectral_norm_est(A, RngState(3))
+    assert abs(got - float(golden["sp_norm2"])) <= 1e-12 * got
+
+
+@pytest.mark.parametrize("M,N,K,transA", [(64, 64, 64, 0), (100, 37, 129, 0), (1000, 110, 110, 0),
+                                          (7, 5, 3, 0), (660, 660, 5000, 1), (33, 17, 100000, 1),
+                                          (1, 1, 1, 1)])
+def test_gemm_matches_numpy(M, N, K, transA):
+    import torch
+
+    from paper_1810_06860_b200 import device
+    from paper_1810_06860_b200.linalg import matmul_dev, matmul_tn_dev
+
+    rng = np.random.default_rng(M + N + K)
+    A = rng.standard_normal((K, M) if transA else (M, K))
+    B = rng.standard_normal((K, N))
+    ref = (A.T if transA else A) @ B
+    got = device.to_host((matmul_tn_dev if transA else matmul_dev)(device.to_device(A), device.to_device(B)))
+    assert rel(got, ref) <= 1e-14 * max(1.0, np.sqrt(K) / 10)
+    del torch
+
+
+def test_gram_is_exactly_symmetric_and_accurate():
+    from paper_1810_06860_b200 import device
+    from paper_1810_06860_b200.linalg import gram_dev
+
+    A = np.random.default_rng(5).standard_normal((20000, 131))
+    G = device.to_host(gram_dev(device.to_device(A)))
+    assert np.array_equal(G, G.T)
+    assert rel(G, A.T @ A) <= 1e-14
+
+
+def test_upper_triangular_b_and_potrf_inverse():
+    from paper_1810_06860_b200 import device
+    from paper_1810_06860_b200.linalg import matmul_dev, potrf_inv_dev
+
+    for n in (1, 5, 64, 65, 130, 300):
+        X = np.random.default_rng(n).standard_normal((3 * n + 10, n))
+        G = X.T @ X
+        Gd = device.to_device(G)
+        info, Rinv = potrf_inv_dev(Gd)
+        assert info == 0
+        R = device.to_host(Gd)
+        Rref = np.linalg.cholesky(G).T
+        assert np.allclose(np.tril(R, -1), 0.0)
+        assert rel(R, Rref) <= 1e-12
+        Ri = device.to_host(Rinv)
+        assert rel(Ri @ R, np.eye(n)) <= 1e-10
+        Q = device.to_host(matmul_dev(device.to_device(X), Rinv, b_upper=True))
+        assert rel(Q.T @ Q, np.eye(n)) <= 1e-9
+    # breakdown is reported, not raised
+    info, _ = potrf_inv_dev(device.to_device(np.array([[1.0, 2.0], [2.0, 1.0]])))
+    assert info == 2
+
+
+@pytest.mark.parametrize("m,n", [(25, 7), (300, 40), (5000, 110), (100000, 110), (138493, 65), (40, 40)])
+def test_lu_pl_structure_and_span(m, n):
+    from paper_1810_06860_b200.linalg import lu_pl
+
+    X = np.random.default_rng(m + n).standard_normal((m, n))
+    PL = lu_pl(X)
+    assert PL.shape == (m, n)
+    assert np.max(np.abs(PL)) <= 1.0 + 1e-12
+    ref = oracle.pivoted_lower(X)
+    # same pivots (no near ties in Gaussian data) -> same factor to rounding
+    assert rel(PL, ref) <= 1e-10
+    Qa, _ = np.linalg.qr(PL)
+    Qb, _ = np.linalg.qr(X)
+    assert np.linalg.norm(Qa @ (Qa.T @ Qb) - Qb) <= 1e-8 * np.sqrt(n)
+
+
+def test_lu_pl_golden(golden):
+    from paper_1810_06860_b200.linalg import lu_pl
+
+    assert rel(lu_pl(golden["lu_X"]), golden["lu_PL"]) <= 1e-12
+    assert rel(lu_pl(golden["lu2_X"]), golden["lu2_PL"]) <= 1e-12
+
+
+def test_lu_pl_errors():
+    from paper_1810_06860_b200.errors import RankDeficiencyError
+    from paper_1810_06860_b200.linalg import lu_pl
+
+    with pytest.raises(RankDeficiencyError, match="zero matrix"):
+        lu_pl(np.zeros((10, 3)))
+    X = np.random.default_rng(0).standard_normal((30, 5))
+    X[:, 3] = X[:, 1]
+    with pytest.raises(RankDeficiencyError, match="zero pivot at column 3"):
+        lu_pl(X)
+    with pytest.raises(ValueError):
+        lu_pl(np.ones((3, 5)))
+    Y = np.ones((6, 2))
+    Y[1, 1] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        lu_pl(Y)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 11, 50, 96, 97, 130, 260, 400])
+def test_sym_eig_matches_numpy(n):
+    from paper_1810_06860_b200.linalg import sym_eig
+
+    X = np.random.default_rng(n).standard_normal((n + 20, n))
+    B = X.T @ X
+    V, d = sym_eig(B)
+    dref = np.linalg.eigvalsh(B)
+    assert np.all(np.diff(d) >= 0)
+    assert np.max(np.abs(d - dref)) <= 1e-12 * dref[-1]
+    assert rel(V.T @ V, np.eye(n)) <= 1e-12 * max(1, n / 10)
+    assert rel(B @ V, V * d) <= 1e-12
+
+
+def test_eig_svd_golden_and_acceptance_01(golden):
+    from paper_1810_06860_b200.linalg import eig_svd
+
+    r = eig_svd(golden["eig_A"])
+    assert r.order == "ascending"
+    assert rel(r.S, golden["eig_S"]) <= 1e-12
+    assert rel(r.V, golden["eig_V"]) <= 1e-9  # same sign rule
+    assert rel(r.U, golden["eig_U"]) <= 1e-9
+    worst_val = worst_rec = 0.0
+    for seed in range(30):  # test_acceptance.py:92-110 contract on 30 seeds
+        rng = np.random.default_rng(seed)
+        n = int(rng.integers(5, 61))
+        m = int(rng.integers(n, 301))
+        A = rng.standard_normal((m, n))
+        got = eig_svd(A).descending()
+        ref = np.linalg.svd(A, compute_uv=False)
+        worst_val = max(worst_val, float(np.max(np.abs(got.S - ref)) / ref[0]))
+        worst_rec = max(worst_rec, np.linalg.norm(A - (got.U * got.S) @ got.V.T) / np.linalg.norm(A))
+    assert worst_val <= 1e-10 and worst_rec < 1e-8
+
+
+def test_eig_svd_rank_errors():
+    from paper_1810_06860_b200.errors import RankDeficiencyError
+    from paper_1810_06860_b200.linalg import eig_svd
+
+    X = np.random.default_rng(0).standard_normal((20, 5))
+    X[:, 4] = X[:, 0]
+    with pytest.raises(RankDeficiencyError, match="eigenvalue"):
+        eig_svd(X)
+    with pytest.raises(RankDeficiencyError, match="no positive eigenvalue"):
+        eig_svd(np.zeros((6, 3)))
+    with pytest.raises(ValueError):
+        eig_svd(np.ones((2, 4)))
+
+
+def test_orth_golden_and_rank_checks(golden):
+    from paper_1810_06860_b200.errors import RankDeficiencyError
+    from paper_1810_06860_b200.linalg import orth
+
+    Q = orth(golden["orth_X"])
+    Qr = golden["orth_Q"]
+    assert rel(Q @ Q.T, Qr @ Qr.T) <= 1e-12
+    assert rel(Q.T @ Q, np.eye(Q.shape[1])) <= 1e-13
+    X = np.random.default_rng(0).standard_normal((20, 5))
+    X[:, 4] = X[:, 0]
+    with pytest.raises(RankDeficiencyError):
+        orth(X)
+    with pytest.raises(RankDeficiencyError, match="zero matrix"):
+        orth(np.zeros((10, 3)))
+    # an ill-conditioned Krylov-like block (cond ~ 1e10) still orthonormalizes
+    rng = np.random.default_rng(7)
+    U, _ = np.linalg.qr(rng.standard_normal((3000, 40)))
+    W, _ = np.linalg.qr(rng.standard_normal((40, 40)))
+    Xc = (U * np.logspace(0, -10, 40)) @ W
+    Q = orth(Xc)
+    assert rel(Q.T @ Q, np.eye(40)) <= 1e-12
+    assert np.linalg.norm(Q @ (Q.T @ U) - U) <= 1e-6 * np.sqrt(40)
+
+
+def test_oracle_svd_matches_lapack(golden):
+    from paper_1810_06860_b200.linalg import oracle_svd
+
+    r = oracle_svd(golden["eig_A"])
+    assert rel(r.S, golden["osvd_S"]) <= 1e-12
+    assert rel((r.U * r.S) @ r.V.T, golden["eig_A"]) <= 1e-12
+    rw = oracle_svd(golden["eig_A"].T)  # wide input
+    assert rel(rw.S, golden["osvd_S"]) <= 1e-12
+    assert rel((rw.U * rw.S) @ rw.V.T, golden["eig_A"].T) <= 1e-12
+    # rank-deficient input still gets an orthonormal U
+    X = np.random.default_rng(4).standard_normal((50, 6))
+    X[:, 5] = X[:, 1]
+    r = oracle_svd(X)
+    assert rel(r.U.T @ r.U, np.eye(6)) <= 1e-12
+    # Gram route: the null singular value is resolved only to ~sqrt(eps)*s_max
+    assert r.S[-1] <= 1e-7 * r.S[0]
+    assert rel((r.U * r.S) @ r.V.T, X) <= 1e-7
+
+
+def test_device_gaussian_matches_host():
+    from paper_1810_06860_b200 import device
+    from paper_1810_06860_b200.rng import RngState, gaussian_matrix, gaussian_matrix_device
+
+    for seed, rows, cols in ((0, 1, 1), (5, 4, 3), (7, 37, 11), (2**62 + 7, 1001, 65), (12345, 50000, 110)):
+        host = gaussian_matrix(RngState(seed), rows, cols)
+        dev = device.to_host(gaussian_matrix_device(seed, rows, cols))
+        # uniform words are bit-exact; log/sincos differ by a few ulp
+        np.testing.assert_allclose(dev, host, rtol=4e-15, atol=4e-15)
