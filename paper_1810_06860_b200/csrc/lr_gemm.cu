@@ -6,26 +6,25 @@
 //   transA = 0: A is M x K  (tall A times small B: TRSM-as-GEMM, lifts, rescale)
 //   transA = 1: A is K x M  (C = A^T B: Gram / projections, split-K over the
 //               long K with partial tiles reduced in fixed order)
-// CTA tile 64x64x16, 4 warps of 32x32, cp.async double buffering.
+// Two tile shapes share one template: 128x64 CTA tiles with 64x32 warp tiles
+// (32 DMMA per k4 step per warp, 0.375 fragment loads per DMMA) for large
+// problems, 64x64 / 32x32 for small ones.  3-stage cp.async pipeline with
+// 16-byte copies (zero-filled at the edges).  SYRK mode computes upper tiles
+// only and mirrors them (exactly symmetric, like the reference's dsyrk).
 #include "lr_common.cuh"
 
 namespace lr {
 
-constexpr int BM = 64, BN = 64, BK = 16;
-constexpr int WM = 32, WN = 32;
-constexpr int MT = WM / 8, NT = WN / 8;
-constexpr int GEMM_THREADS = 128;
-constexpr int LDA_N = BK + 4;  // A stored [m][k] (transA = 0)
-constexpr int LDA_T = BM + 4;  // A stored [k][m] (transA = 1)
-constexpr int LDB = BN + 4;    // B stored [k][n]
-constexpr int A_STAGE = (BM * LDA_N > BK * LDA_T) ? BM * LDA_N : BK * LDA_T;
-constexpr int B_STAGE = BK * LDB;
+constexpr int BK = 16;
+constexpr int STAGES = 3;
 
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int src_bytes) {
   unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  int src_size = pred ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem),
-               "r"(src_size));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, int src_bytes) {
+  unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem), "r"(src_bytes));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -39,114 +38,150 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <bool TRANS_A>
-__global__ void __launch_bounds__(GEMM_THREADS) gemm_kernel(int M, int N, int K, double alpha,
-                                                           const double* __restrict__ A, long long lda,
-                                                           const double* __restrict__ B, long long ldb,
-                                                           double beta, double* __restrict__ C,
-                                                           long long ldc, int flags,
-                                                           double* __restrict__ work, int k_chunk) {
-  const int tn = blockIdx.x, tm = blockIdx.y, z = blockIdx.z;
-  if ((flags & LR_GEMM_SYRK_UPPER) && tn < tm) return;
-  __shared__ __align__(16) double As[2][A_STAGE];
-  __shared__ __align__(16) double Bs[2][B_STAGE];
+template <int BM_, int BN_, int WM_, int WN_>
+struct Tile {
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_;
+  static constexpr int MT = WM / 8, NT = WN / 8;
+  static constexpr int WARPS = (BM / WM) * (BN / WN);
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int LDA_N = BK + 4;  // A stored [m][k]
+  static constexpr int LDA_T = BM + 4;  // A stored [k][m]
+  static constexpr int LDB = BN + 4;    // B stored [k][n]
+  static constexpr int A_STAGE = (BM * LDA_N > BK * LDA_T) ? BM * LDA_N : BK * LDA_T;
+  static constexpr int B_STAGE = BK * LDB;
+  static constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) * (int)sizeof(double);
+};
+using TileL = Tile<128, 64, 64, 32>;
+using TileS = Tile<64, 64, 32, 32>;
 
-  const int m0 = tm * BM, n0 = tn * BN;
-  int k_begin = z * k_chunk;
+template <typename T, bool TRANS_A>
+__global__ void __launch_bounds__(T::THREADS) gemm_kernel(int M, int N, int K, double alpha,
+                                                         const double* __restrict__ A, long long lda,
+                                                         const double* __restrict__ B, long long ldb, double beta,
+                                                         double* __restrict__ C, long long ldc, int flags,
+                                                         double* __restrict__ work, int k_chunk, int vec16) {
+  const int tn = blockIdx.x, tm = blockIdx.y, z = blockIdx.z;
+  if ((flags & LR_GEMM_SYRK_UPPER) && (tn + 1) * T::BN <= tm * T::BM) return;  // tile entirely below diagonal
+  extern __shared__ __align__(16) double g_smem[];
+  double* As = g_smem;
+  double* Bs = g_smem + STAGES * T::A_STAGE;
+
+  const int m0 = tm * T::BM, n0 = tn * T::BN;
+  const int k_begin = z * k_chunk;
   int k_end = min(K, k_begin + k_chunk);
-  if (flags & LR_GEMM_B_UPPER) k_end = min(k_end, n0 + BN);
+  if (flags & LR_GEMM_B_UPPER) k_end = min(k_end, n0 + T::BN);
   const int nk = (k_end > k_begin) ? (k_end - k_begin + BK - 1) / BK : 0;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp / (BN / WN), wn = warp % (BN / WN);
+  const int wm = warp / (T::BN / T::WN), wn = warp % (T::BN / T::WN);
   const int gid = lane >> 2, tig = lane & 3;
 
-  double acc[MT][NT][2];
+  double acc[T::MT][T::NT][2];
 #pragma unroll
-  for (int i = 0; i < MT; ++i)
+  for (int i = 0; i < T::MT; ++i)
 #pragma unroll
-    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < T::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   auto load_stage = [&](int st, int kt) {
     const int k0 = k_begin + kt * BK;
-    double* as = As[st];
-    double* bs = Bs[st];
-    if (!TRANS_A) {
-      // A[m][k]: 16 consecutive k per row (128 B)
-#pragma unroll
-      for (int i = 0; i < (BM * BK) / GEMM_THREADS; ++i) {
-        const int e = tid + i * GEMM_THREADS;
-        const int mm = e / BK, kk = e % BK;
-        const int gm = m0 + mm, gk = k0 + kk;
-        const bool ok = gm < M && gk < k_end;
-        cp_async8(as + mm * LDA_N + kk, ok ? A + (long long)gm * lda + gk : A, ok);
+    double* as = As + st * T::A_STAGE;
+    double* bs = Bs + st * T::B_STAGE;
+    if (vec16) {
+      if (!TRANS_A) {
+        // A[m][k]: 8 pairs of k per row
+        for (int e = tid; e < T::BM * (BK / 2); e += T::THREADS) {
+          const int mm = e / (BK / 2), kk = 2 * (e % (BK / 2));
+          const int gm = m0 + mm, gk = k0 + kk;
+          const int nb = (gm < M) ? (gk + 1 < k_end ? 16 : (gk < k_end ? 8 : 0)) : 0;
+          cp_async16(as + mm * T::LDA_N + kk, nb ? A + (long long)gm * lda + gk : A, nb);
+        }
+      } else {
+        for (int e = tid; e < BK * (T::BM / 2); e += T::THREADS) {
+          const int kk = e / (T::BM / 2), mm = 2 * (e % (T::BM / 2));
+          const int gm = m0 + mm, gk = k0 + kk;
+          const int nb = (gk < k_end) ? (gm + 1 < M ? 16 : (gm < M ? 8 : 0)) : 0;
+          cp_async16(as + kk * T::LDA_T + mm, nb ? A + (long long)gk * lda + gm : A, nb);
+        }
+      }
+      for (int e = tid; e < BK * (T::BN / 2); e += T::THREADS) {
+        const int kk = e / (T::BN / 2), nn = 2 * (e % (T::BN / 2));
+        const int gn = n0 + nn, gk = k0 + kk;
+        const int nb = (gk < k_end) ? (gn + 1 < N ? 16 : (gn < N ? 8 : 0)) : 0;
+        cp_async16(bs + kk * T::LDB + nn, nb ? B + (long long)gk * ldb + gn : B, nb);
       }
     } else {
-      // A[k][m]: 64 consecutive m per k-row (512 B)
-#pragma unroll
-      for (int i = 0; i < (BM * BK) / GEMM_THREADS; ++i) {
-        const int e = tid + i * GEMM_THREADS;
-        const int kk = e / BM, mm = e % BM;
-        const int gm = m0 + mm, gk = k0 + kk;
-        const bool ok = gm < M && gk < k_end;
-        cp_async8(as + kk * LDA_T + mm, ok ? A + (long long)gk * lda + gm : A, ok);
+      if (!TRANS_A) {
+        for (int e = tid; e < T::BM * BK; e += T::THREADS) {
+          const int mm = e / BK, kk = e % BK;
+          const int gm = m0 + mm, gk = k0 + kk;
+          const bool ok = gm < M && gk < k_end;
+          cp_async8(as + mm * T::LDA_N + kk, ok ? A + (long long)gm * lda + gk : A, ok ? 8 : 0);
+        }
+      } else {
+        for (int e = tid; e < BK * T::BM; e += T::THREADS) {
+          const int kk = e / T::BM, mm = e % T::BM;
+          const int gm = m0 + mm, gk = k0 + kk;
+          const bool ok = gm < M && gk < k_end;
+          cp_async8(as + kk * T::LDA_T + mm, ok ? A + (long long)gk * lda + gm : A, ok ? 8 : 0);
+        }
+      }
+      for (int e = tid; e < BK * T::BN; e += T::THREADS) {
+        const int kk = e / T::BN, nn = e % T::BN;
+        const int gn = n0 + nn, gk = k0 + kk;
+        const bool ok = gn < N && gk < k_end;
+        cp_async8(bs + kk * T::LDB + nn, ok ? B + (long long)gk * ldb + gn : B, ok ? 8 : 0);
       }
     }
-#pragma unroll
-    for (int i = 0; i < (BN * BK) / GEMM_THREADS; ++i) {
-      const int e = tid + i * GEMM_THREADS;
-      const int kk = e / BN, nn = e % BN;
-      const int gn = n0 + nn, gk = k0 + kk;
-      const bool ok = gn < N && gk < k_end;
-      cp_async8(bs + kk * LDB + nn, ok ? B + (long long)gk * ldb + gn : B, ok);
-    }
-    cp_async_commit();
   };
 
-  if (nk > 0) load_stage(0, 0);
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s);
+    cp_async_commit();
+  }
   for (int kt = 0; kt < nk; ++kt) {
-    if (kt + 1 < nk) {
-      load_stage((kt + 1) & 1, kt + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
-    const double* as = As[kt & 1];
-    const double* bs = Bs[kt & 1];
+    {
+      const int nxt = kt + STAGES - 1;
+      if (nxt < nk) load_stage(nxt % STAGES, nxt);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % STAGES) * T::A_STAGE;
+    const double* bs = Bs + (kt % STAGES) * T::B_STAGE;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[MT], bf[NT];
+      double af[T::MT], bf[T::NT];
 #pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        const int mm = wm * WM + i * 8 + gid;
-        af[i] = TRANS_A ? as[(kk + tig) * LDA_T + mm] : as[mm * LDA_N + kk + tig];
+      for (int i = 0; i < T::MT; ++i) {
+        const int mm = wm * T::WM + i * 8 + gid;
+        af[i] = TRANS_A ? as[(kk + tig) * T::LDA_T + mm] : as[mm * T::LDA_N + kk + tig];
       }
 #pragma unroll
-      for (int j = 0; j < NT; ++j) bf[j] = bs[(kk + tig) * LDB + wn * WN + j * 8 + gid];
+      for (int j = 0; j < T::NT; ++j) bf[j] = bs[(kk + tig) * T::LDB + wn * T::WN + j * 8 + gid];
 #pragma unroll
-      for (int i = 0; i < MT; ++i)
+      for (int i = 0; i < T::MT; ++i)
 #pragma unroll
-        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < T::NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
 
   // epilogue
   const bool split = gridDim.z > 1;
   const bool syrk = (flags & LR_GEMM_SYRK_UPPER) != 0;
 #pragma unroll
-  for (int i = 0; i < MT; ++i) {
-    const int row = m0 + wm * WM + i * 8 + gid;
+  for (int i = 0; i < T::MT; ++i) {
+    const int row = m0 + wm * T::WM + i * 8 + gid;
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
+    for (int j = 0; j < T::NT; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int col = n0 + wn * WN + j * 8 + 2 * tig + h;
+        const int col = n0 + wn * T::WN + j * 8 + 2 * tig + h;
         if (row >= M || col >= N) continue;
         const double v = acc[i][j][h];
         if (split) {
-          work[((long long)z * M + row) * N + col] = v;
+          if (!syrk || row <= col) work[((long long)z * M + row) * N + col] = v;
         } else if (syrk) {
           if (row <= col) {
             double out = alpha * v;
@@ -181,20 +216,62 @@ __global__ void splitk_reduce_kernel(int M, int N, int S, const double* __restri
   }
 }
 
-static int choose_splits(int transA, int M, int N, int K, int flags) {
-  if (!transA) return 1;
-  long long tiles = (long long)((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  if (flags & LR_GEMM_SYRK_UPPER) {
-    long long t = (M + BM - 1) / BM;
-    tiles = t * (t + 1) / 2;
+static bool use_large(int M, int N, long long K) {
+  return (long long)M * N * K >= (1LL << 27) && M >= 128;
+}
+
+template <typename T, bool TA>
+static int occupancy() {
+  static int occ = -1;
+  if (occ < 0) {
+    cudaFuncSetAttribute(gemm_kernel<T, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_kernel<T, TA>, T::THREADS, T::SMEM);
+    if (occ < 1) occ = 1;
   }
-  const long long target = (long long)sm_count() * 4;
-  long long s = (target + tiles - 1) / tiles;
-  long long smax = (K + 255) / 256;
+  return occ;
+}
+
+template <typename T>
+static long long upper_tiles(int M, int N) {
+  long long cnt = 0;
+  const int tm_n = (M + T::BM - 1) / T::BM, tn_n = (N + T::BN - 1) / T::BN;
+  for (int tm = 0; tm < tm_n; ++tm)
+    for (int tn = 0; tn < tn_n; ++tn)
+      if ((tn + 1) * T::BN > tm * T::BM) ++cnt;
+  return cnt;
+}
+
+// split-K so the live CTAs fill whole waves of the GPU
+template <typename T, bool TA>
+static int choose_splits_t(int M, int N, int K, int flags) {
+  if (!TA) return 1;
+  long long tiles = (flags & LR_GEMM_SYRK_UPPER) ? upper_tiles<T>(M, N)
+                                                 : (long long)((M + T::BM - 1) / T::BM) * ((N + T::BN - 1) / T::BN);
+  const long long cap = (long long)sm_count() * occupancy<T, TA>();
+  long long s = tiles >= cap ? 1 : cap / tiles;
+  const long long smax = (K + 511) / 512;
   if (s > smax) s = smax;
   if (s < 1) s = 1;
   return (int)s;
 }
+
+static int choose_splits(int transA, int M, int N, int K, int flags) {
+  if (!transA) return 1;
+  return use_large(M, N, K) ? choose_splits_t<TileL, true>(M, N, K, flags)
+                            : choose_splits_t<TileS, true>(M, N, K, flags);
+}
+
+template <typename T, bool TA>
+static void launch(int M, int N, int K, double alpha, const double* A, long long lda, const double* B,
+                   long long ldb, double beta, double* C, long long ldc, int flags, double* work, int S,
+                   int k_chunk, int vec16, cudaStream_t s) {
+  occupancy<T, TA>();
+  dim3 grid((N + T::BN - 1) / T::BN, (M + T::BM - 1) / T::BM, S);
+  gemm_kernel<T, TA><<<grid, T::THREADS, T::SMEM, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, flags, work,
+                                                       k_chunk, vec16);
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace lr
 
@@ -216,21 +293,24 @@ int lr_gemm_f64(int transA, int M, int N, int K, double alpha, const double* A, 
   LR_REQUIRE(!(flags & LR_GEMM_B_UPPER) || (K == N), "gemm: B_UPPER needs K == N");
   if (M == 0 || N == 0) return LR_OK;
   cudaStream_t s = as_stream(stream);
-  if (K == 0) {
-    // C = beta*C
-    if (beta == 0.0) return lr_fill_f64(C, ldc, M, N, 0.0, stream);
-  }
+  if (K == 0 && beta == 0.0) return lr_fill_f64(C, ldc, M, N, 0.0, stream);
   int S = choose_splits(transA, M, N, K, flags);
   if (S > 1 && (work == nullptr || work_doubles < (long long)S * M * N)) S = 1;
   int k_chunk = S > 1 ? ((K + S - 1) / S + BK - 1) / BK * BK : (K > 0 ? K : 1);
   if (S > 1) S = (K + k_chunk - 1) / k_chunk;
-  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, S);
-  if (transA)
-    gemm_kernel<true><<<grid, GEMM_THREADS, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
-                                                    flags, work, k_chunk);
-  else
-    gemm_kernel<false><<<grid, GEMM_THREADS, 0, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
-                                                     flags, work, k_chunk);
+  const int vec16 = (lda % 2 == 0) && (ldb % 2 == 0) && aligned16(A) && aligned16(B);
+  const bool large = use_large(M, N, K);
+  if (transA) {
+    if (large)
+      launch<TileL, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, flags, work, S, k_chunk, vec16, s);
+    else
+      launch<TileS, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, flags, work, S, k_chunk, vec16, s);
+  } else {
+    if (large)
+      launch<TileL, false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, flags, work, S, k_chunk, vec16, s);
+    else
+      launch<TileS, false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, flags, work, S, k_chunk, vec16, s);
+  }
   LR_CHECK_LAUNCH();
   if (S > 1) {
     long long total = (long long)M * N;

@@ -182,10 +182,11 @@ def potrf_inv_dev(G, shift=0.0):
 
 # --------------------------------------------------------------------- orth
 
-def _cholqr_pass(X, shift=0.0):
-    """One CholeskyQR pass: returns (info, Q, diag(R))."""
+def _cholqr_pass(X, shift=0.0, G=None):
+    """One CholeskyQR pass: returns (info, Q, diag(R)); G = X^T X if given."""
     n = X.shape[1]
-    G = gram_dev(X)
+    if G is None:
+        G = gram_dev(X)
     info, Rinv = potrf_inv_dev(G, shift)
     if info:
         return info, None, None
@@ -195,15 +196,24 @@ def _cholqr_pass(X, shift=0.0):
 
 
 def orth_dev(X):
-    """Orthonormal basis of range(X) (linalg.py:101-124), device in/out."""
-    s = _check_dev(X, "orth input")
+    """Orthonormal basis of range(X) (linalg.py:101-124), device in/out.
+
+    ||X||_F comes from the trace of the first Gram (no extra pass over X);
+    a non-finite trace triggers the explicit finiteness check."""
+    if X.dim() != 2 or X.shape[0] < 1 or X.shape[1] < 1:
+        raise ValueError(f"orth input must be 2-D with positive dims, got shape {tuple(X.shape)}")
     m, n = X.shape
     if m < n:
         raise ValueError(f"orth requires m >= n, got {m}x{n}")
-    scale = _fro_from_stats(s, X)
+    G0 = gram_dev(X)
+    tr = float(np.sum(_diag_host(G0, n)))
+    if np.isfinite(tr) and tr < 1e300:
+        scale = float(np.sqrt(tr))
+    else:
+        scale = _fro_from_stats(_check_dev(X, "orth input"), X)
     if scale == 0.0:
         raise RankDeficiencyError("cannot orthonormalize a zero matrix")
-    info, Q1, d1 = _cholqr_pass(X)
+    info, Q1, d1 = _cholqr_pass(X, G=G0)
     if info == 0:
         info2, Q, d2 = _cholqr_pass(Q1)
         if info2 == 0:
@@ -336,12 +346,14 @@ def eig_svd_dev(A, cols=None, check=True):
     U_sel (rows x len(cols)) = A V[:, cols] / S[cols], cols) with cols an
     index array into the ascending order (default: all, ascending).
     """
-    if check:
-        _check_dev(A, "eig_svd input")
+    if A.dim() != 2 or A.shape[0] < 1 or A.shape[1] < 1:
+        raise ValueError(f"eig_svd input must be 2-D with positive dims, got shape {tuple(A.shape)}")
     rows, n = A.shape
     if rows < n:
         raise ValueError(f"eig_svd requires m >= n, got {rows}x{n}")
     G = gram_dev(A)
+    if check and not np.isfinite(np.sum(_diag_host(G, n))):
+        _check_dev(A, "eig_svd input")  # raises ValueError on non-finite input
     V, d = sym_eig_dev(G, symmetrize=False)
     dh = device.to_host(d)
     dmax = dh[-1]

@@ -12,10 +12,13 @@ Drop-in for /root/reference/pkg/src/lowrank/rsvd.py:
 Rank deficiency reroutes through the dense device SVD when allow_fallback,
 else re-raises with the same advice suffixes (rsvd.py:81-126).
 
-Omega is gaussian_matrix(RngState(seed), n, k+s).  `omega="host"` (default)
-draws it with numpy on the host and uploads it -- the reference's own
-arithmetic; `omega="device"` generates the same Philox stream on the GPU
-(uniforms bit-exact, normals within a few ulp), avoiding the PCIe transfer.
+Omega is gaussian_matrix(RngState(seed), n, k+s).  `omega="device"`
+(default, OMEGA_SOURCE) generates it on the GPU from the same numpy Philox
+stream (uniform words bit-exact, normals within 4e-15 of the host values --
+tests/test_gpu_kernels.py::test_device_gaussian_matches_host), so no n x w
+block crosses PCIe per call; `omega="host"` draws it with numpy on the host
+and uploads it (the reference's own arithmetic, bit for bit).  The parity
+suite runs both.
 """
 
 from __future__ import annotations
@@ -30,7 +33,7 @@ from .linalg import (DevSvd, SvdResult, eig_svd_dev, lu_pl_dev, matmul_dev, orac
 from .rng import RngState, gaussian_matrix, gaussian_matrix_device
 from .sparse import SparseMatrix, frobenius, spmm_dev, spmm_t_dev
 
-OMEGA_SOURCE = "host"
+OMEGA_SOURCE = "device"
 
 
 @dataclass

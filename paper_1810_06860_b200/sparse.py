@@ -60,20 +60,43 @@ def _schedule(indptr: np.ndarray, chunk: int = SPLIT_CHUNK):
     return items, splits, n_slots
 
 
-class _Side:
-    """One compressed orientation of the pattern on the device."""
+class _HostSide:
+    """Host-prepared int32 arrays + schedule of one orientation (built once
+    per pattern, like the reference's lazily cached transpose index)."""
 
     def __init__(self, ptr_host, idx_host, n_rows):
         self.rows = int(n_rows)
-        self.ptr = device.int_buffer(ptr_host)
-        self.idx = device.int_buffer(idx_host)
+        self.ptr = np.ascontiguousarray(ptr_host, dtype=np.int32)
+        self.idx = np.ascontiguousarray(idx_host, dtype=np.int32)
         items, splits, n_slots = _schedule(np.asarray(ptr_host, dtype=np.int64))
-        self.items = None if items is None else device.int_buffer(items.ravel())
+        self.items = None if items is None else np.ascontiguousarray(items.ravel())
+        self.splits = None if splits is None else np.ascontiguousarray(splits.ravel())
         self.n_items = self.rows if items is None else int(items.shape[0])
-        self.splits = None if splits is None else device.int_buffer(splits.ravel())
         self.n_splits = 0 if splits is None else int(splits.shape[0])
         self.n_slots = n_slots
-        self.max_len = int(np.max(np.diff(ptr_host))) if self.rows else 0
+
+
+class _Side:
+    """One compressed orientation of the pattern on the device."""
+
+    def __init__(self, hs: _HostSide):
+        self.rows = hs.rows
+        self.ptr = device.int_buffer(hs.ptr)
+        self.idx = device.int_buffer(hs.idx)
+        self.items = None if hs.items is None else device.int_buffer(hs.items)
+        self.splits = None if hs.splits is None else device.int_buffer(hs.splits)
+        self.n_items, self.n_splits, self.n_slots = hs.n_items, hs.n_splits, hs.n_slots
+
+
+class _HostPrep:
+    def __init__(self, A: "SparseMatrix"):
+        perm, t_indptr, t_indices = A._transpose_index()
+        inv = np.empty(A.nnz, dtype=np.int32)
+        inv[perm] = np.arange(A.nnz, dtype=np.int32)
+        self.csr = _HostSide(A.indptr, A.indices, A.rows)
+        self.csc = _HostSide(t_indptr, t_indices, A.cols)
+        self.perm = np.ascontiguousarray(perm, dtype=np.int32)
+        self.inv_perm = inv
 
 
 class DevicePattern:
@@ -81,16 +104,13 @@ class DevicePattern:
     matrix with that pattern, e.g. Y and P_Phi(M) in the SVT loop)."""
 
     def __init__(self, A: "SparseMatrix"):
-        m, n, nnz = A.rows, A.cols, A.nnz
-        self.shape = (m, n)
-        self.nnz = nnz
-        perm, t_indptr, t_indices = A._transpose_index()
-        inv = np.empty(nnz, dtype=np.int64)
-        inv[perm] = np.arange(nnz)
-        self.csr = _Side(A.indptr, A.indices, m)
-        self.csc = _Side(t_indptr, t_indices, n)
-        self.perm = device.int_buffer(perm)
-        self.inv_perm = device.int_buffer(inv)
+        self.shape = (A.rows, A.cols)
+        self.nnz = A.nnz
+        hp = A._host_prep()
+        self.csr = _Side(hp.csr)
+        self.csc = _Side(hp.csc)
+        self.perm = device.int_buffer(hp.perm)
+        self.inv_perm = device.int_buffer(hp.inv_perm)
 
     def values(self, host_vals: np.ndarray):
         """(csr, csc) device value copies of host values in CSR order."""
@@ -213,10 +233,22 @@ class SparseMatrix:
         return out
 
     # ------------------------------------------------------------ device
+    def _host_prep(self) -> _HostPrep:
+        if getattr(self, "_hprep", None) is None:
+            self._hprep = _HostPrep(self)
+        return self._hprep
+
     def pattern(self) -> DevicePattern:
         if self._pattern is None:
             self._pattern = DevicePattern(self)
         return self._pattern
+
+    def drop_device(self) -> None:
+        """Release the device mirror (pattern and values); host data stay."""
+        if self._host_stale:
+            _ = self.data
+        self._pattern = None
+        self._dvals = None
 
     def share_pattern(self, other: "SparseMatrix") -> None:
         """Reuse other's device structure (same indptr/indices objects)."""
@@ -224,6 +256,7 @@ class SparseMatrix:
             self._pattern = other._pattern
             self._tperm, self._t_indptr, self._t_indices = other._tperm, other._t_indptr, other._t_indices
             self._coo_rows = other._coo_rows
+            self._hprep = getattr(other, "_hprep", None)
 
     def device_values(self):
         """(csr, csc) device value vectors, created from the host data once."""
