@@ -22,58 +22,91 @@ __global__ void add_diag_kernel(double* A, long long lda, int n, double shift) {
 __global__ void __launch_bounds__(CH_THREADS) chol_diag_kernel(double* A, long long lda, int J, int jb,
                                                              double* Dinv, int* info) {
   if (*info != 0) return;
+  // 16 x 16 threads, each owns a 4 x 4 tile (rows 4ty.., cols 4tx..) of the
+  // 64 x 64 block; indices >= jb are padded with the identity (decoupled).
   extern __shared__ double ch_smem[];
   double(*a)[CH_NB + 1] = reinterpret_cast<double(*)[CH_NB + 1]>(ch_smem);
   double(*x)[CH_NB + 1] = reinterpret_cast<double(*)[CH_NB + 1]>(ch_smem + CH_NB * (CH_NB + 1));
-  __shared__ int fail;
-  const int tid = threadIdx.x;
-  if (tid == 0) fail = 0;
-  for (int e = tid; e < jb * jb; e += CH_THREADS) {
-    int i = e / jb, c = e % jb;
-    a[i][c] = (c >= i) ? A[(long long)(J + i) * lda + J + c] : 0.0;
-  }
+  __shared__ double rowbuf[CH_NB];
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int i0 = 4 * ty, c0 = 4 * tx;
+#pragma unroll
+  for (int di = 0; di < 4; ++di)
+#pragma unroll
+    for (int dc = 0; dc < 4; ++dc) {
+      const int i = i0 + di, c = c0 + dc;
+      double v;
+      if (i < jb && c < jb)
+        v = (c >= i) ? A[(long long)(J + i) * lda + J + c] : 0.0;
+      else
+        v = (i == c) ? 1.0 : 0.0;
+      a[i][c] = v;
+      x[i][c] = (i == c) ? 1.0 : 0.0;
+    }
   __syncthreads();
-  for (int j = 0; j < jb; ++j) {
-    if (tid == 0) {
-      double d = a[j][j];
-      if (!(d > 0.0)) {
-        fail = J + j + 1;
-      } else {
-        a[j][j] = sqrt(d);
+  for (int j = 0; j < CH_NB; ++j) {
+    const double d = a[j][j];
+    if (!(d > 0.0)) {  // uniform: every thread read the same value
+      if (tid == 0) *info = J + j + 1;
+      return;
+    }
+    const double r = sqrt(d);
+    if (ty == (j >> 2)) {  // owners of row j: finalize it (nobody else touches row j now)
+#pragma unroll
+      for (int dc = 0; dc < 4; ++dc) {
+        const int c = c0 + dc;
+        if (c >= j) {
+          const double v = (c == j) ? r : a[j][c] / r;
+          a[j][c] = v;
+          rowbuf[c] = v;
+        }
       }
     }
     __syncthreads();
-    if (fail) break;
-    const double r = a[j][j];
-    for (int c = j + 1 + tid; c < jb; c += CH_THREADS) a[j][c] /= r;
+#pragma unroll
+    for (int di = 0; di < 4; ++di)
+#pragma unroll
+      for (int dc = 0; dc < 4; ++dc) {
+        const int i = i0 + di, c = c0 + dc;
+        if (i > j && c >= i) a[i][c] = fma(-rowbuf[i], rowbuf[c], a[i][c]);
+      }
     __syncthreads();
-    const int rest = jb - j - 1;
-    for (int e = tid; e < rest * rest; e += CH_THREADS) {
-      int i = j + 1 + e / rest, c = j + 1 + e % rest;
-      if (c >= i) a[i][c] -= a[j][i] * a[j][c];
+  }
+  // R^{-1} by right-looking back substitution: X = I; for i = n-1..0:
+  // X[i,:] /= R_ii; X[r,:] -= R_ri X[i,:] (r < i)
+  for (int i = CH_NB - 1; i >= 0; --i) {
+    const double rii = a[i][i];
+    if (ty == (i >> 2)) {
+#pragma unroll
+      for (int dc = 0; dc < 4; ++dc) {
+        const int c = c0 + dc;
+        if (c >= i) {
+          const double v = x[i][c] / rii;
+          x[i][c] = v;
+          rowbuf[c] = v;
+        }
+      }
     }
     __syncthreads();
-  }
-  if (fail) {
-    if (tid == 0) *info = fail;
-    return;
-  }
-  // inverse of upper R (jb x jb): rows bottom-up, parallel over columns
-  for (int e = tid; e < jb * jb; e += CH_THREADS) x[e / jb][e % jb] = 0.0;
-  __syncthreads();
-  for (int i = jb - 1; i >= 0; --i) {
-    for (int c = i + tid; c < jb; c += CH_THREADS) {
-      double s = (c == i) ? 1.0 : 0.0;
-      for (int k = i + 1; k <= c; ++k) s -= a[i][k] * x[k][c];
-      x[i][c] = s / a[i][i];
-    }
+#pragma unroll
+    for (int di = 0; di < 4; ++di)
+#pragma unroll
+      for (int dc = 0; dc < 4; ++dc) {
+        const int rr = i0 + di, c = c0 + dc;
+        if (rr < i && c >= i) x[rr][c] = fma(-a[rr][i], rowbuf[c], x[rr][c]);
+      }
     __syncthreads();
   }
-  for (int e = tid; e < jb * jb; e += CH_THREADS) {
-    int i = e / jb, c = e % jb;
-    A[(long long)(J + i) * lda + J + c] = a[i][c];
-    Dinv[i * CH_NB + c] = x[i][c];
-  }
+#pragma unroll
+  for (int di = 0; di < 4; ++di)
+#pragma unroll
+    for (int dc = 0; dc < 4; ++dc) {
+      const int i = i0 + di, c = c0 + dc;
+      if (i < jb && c < jb) {
+        A[(long long)(J + i) * lda + J + c] = a[i][c];
+        Dinv[i * CH_NB + c] = x[i][c];
+      }
+    }
 }
 
 __global__ void zero_lower_kernel(double* A, long long lda, int n) {

@@ -17,6 +17,8 @@
 // time and share of the step, not a roofline fraction.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "lr_common.cuh"
 
 namespace cg = cooperative_groups;
@@ -35,6 +37,7 @@ struct LuParams {
   double* prow;         // [2][G][nb]
   int* pivrow;          // [n]
   double* status;       // {bad col or -1, pivot, tol}
+  long long* prof;      // optional per-phase clock totals of CTA 0 (LR_LU_PROFILE)
 };
 
 __device__ __forceinline__ void better(double& v, int& r, double v2, int r2) {
@@ -62,6 +65,12 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
   __shared__ int red_r[LU_THREADS / 32];
   __shared__ double win_v;
   __shared__ int win_r, win_c;
+  __shared__ double red_v2[LU_THREADS / 32];
+  __shared__ int red_r2[LU_THREADS / 32];
+  long long* prof = (blockIdx.x == 0 && threadIdx.x == 0) ? p.prof : nullptr;
+  long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+  double cbv = -1.0;  // look-ahead candidate for the next column
+  int cbr = 0x7fffffff;
 
   const double maxabs = p.stats[1];
   const double tol = 1e-14 * maxabs;
@@ -79,10 +88,16 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
     for (int jj = 0; jj < jb; ++jj) {
       const int j = J + jj;
       // local argmax among un-pivoted rows
+      if (prof) t0 = clock64();
       double bv = -1.0;
       int br = 0x7fffffff;
-      for (int i = tid; i < nr; i += LU_THREADS)
-        if (pivflag[i] < 0) better(bv, br, fabs(P[i * LD + jj]), r0 + i);
+      if (jj == 0) {
+        for (int i = tid; i < nr; i += LU_THREADS)
+          if (pivflag[i] < 0) better(bv, br, fabs(P[i * LD + jj]), r0 + i);
+      } else {  // found during the previous column's update (look-ahead)
+        bv = cbv;
+        br = cbr;
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -94,57 +109,73 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
         red_r[wid] = br;
       }
       __syncthreads();
-      if (tid == 0) {
-        for (int w = 1; w < LU_THREADS / 32; ++w) better(bv, br, red_v[w], red_r[w]);
-        p.cand[(par * G + cta) * 2 + 0] = bv;
-        p.cand[(par * G + cta) * 2 + 1] = (double)br;
-        win_r = br;
-      }
-      __syncthreads();
-      if (win_r != 0x7fffffff)
-        for (int c = tid; c < jb; c += LU_THREADS)
-          p.prow[((long long)par * G + cta) * nb + c] = P[(win_r - r0) * LD + c];
-      grid.sync();
-      // global winner: same answer in every CTA
-      bv = -1.0;
-      br = 0x7fffffff;
-      int bc = -1;
-      for (int c = tid; c < G; c += LU_THREADS) {
-        double v2 = p.cand[(par * G + c) * 2 + 0];
-        int r2 = (int)p.cand[(par * G + c) * 2 + 1];
-        if (v2 > bv || (v2 == bv && r2 < br)) {
-          bv = v2;
-          br = r2;
-          bc = c;
-        }
-      }
+      if (wid == 0) {
+        // CTA candidate: warp 0 folds the per-warp winners and publishes
+        // (|x|, row) plus the candidate's panel row (one element per lane)
+        double v = (lane < LU_THREADS / 32) ? red_v[lane] : -1.0;
+        int r = (lane < LU_THREADS / 32) ? red_r[lane] : 0x7fffffff;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-        int r2 = __shfl_xor_sync(0xffffffffu, br, o);
-        int c2 = __shfl_xor_sync(0xffffffffu, bc, o);
-        if (v2 > bv || (v2 == bv && r2 < br)) {
-          bv = v2;
-          br = r2;
-          bc = c2;
+        for (int o = 4; o > 0; o >>= 1) {
+          double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+          int r2 = __shfl_xor_sync(0xffffffffu, r, o);
+          better(v, r, v2, r2);
+        }
+        v = __shfl_sync(0xffffffffu, v, 0);
+        r = __shfl_sync(0xffffffffu, r, 0);
+        if (lane == 0) {
+          p.cand[(par * G + cta) * 2 + 0] = v;
+          p.cand[(par * G + cta) * 2 + 1] = (double)r;
+        }
+        if (r != 0x7fffffff)
+          for (int c = lane; c < jb; c += 32) p.prow[((long long)par * G + cta) * nb + c] = P[(r - r0) * LD + c];
+      }
+      if (prof) t1 = clock64();
+      grid.sync();
+      if (prof) t2 = clock64();
+      {
+        // global winner, same in every CTA: all threads load candidates at
+        // once (one L2 round trip), warps reduce, warp 0 folds
+        double v = -1.0;
+        int r = 0x7fffffff;
+        for (int c = tid; c < G; c += LU_THREADS) {
+          const double2 cr = reinterpret_cast<const double2*>(p.cand)[par * G + c];
+          better(v, r, cr.x, (int)cr.y);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+          int r2 = __shfl_xor_sync(0xffffffffu, r, o);
+          better(v, r, v2, r2);
+        }
+        if (lane == 0) {
+          red_v2[wid] = v;
+          red_r2[wid] = r;
         }
       }
-      if (lane == 0) {
-        red_v[wid] = bv;
-        red_r[wid] = br;
+      __syncthreads();
+      if (wid == 0) {
+        double v = (lane < LU_THREADS / 32) ? red_v2[lane] : -1.0;
+        int r = (lane < LU_THREADS / 32) ? red_r2[lane] : 0x7fffffff;
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+          int r2 = __shfl_xor_sync(0xffffffffu, r, o);
+          better(v, r, v2, r2);
+        }
+        v = __shfl_sync(0xffffffffu, v, 0);
+        r = __shfl_sync(0xffffffffu, r, 0);
+        const int wc = r / p.rows_per;  // slabs are contiguous
+        const double* wrow = p.prow + ((long long)par * G + wc) * nb;
+        for (int c = lane; c < jb; c += 32) urow[c] = wrow[c];
+        if (lane == 0) {
+          win_v = v;
+          win_r = r;
+          win_c = wc;
+          if (r >= r0 && r < r1 && v >= tol && v != 0.0) pivflag[r - r0] = j;
+          if (cta == 0) p.pivrow[j] = r;
+        }
       }
       __syncthreads();
-      if (tid == 0) {
-        int wc = bc;
-        // recompute the winning CTA index from rows (rows are slab-contiguous)
-        for (int w = 1; w < LU_THREADS / 32; ++w) better(bv, br, red_v[w], red_r[w]);
-        wc = br / p.rows_per;
-        win_v = bv;
-        win_r = br;
-        win_c = wc;
-      }
-      __syncthreads();
-      const double* wrow = p.prow + ((long long)par * G + win_c) * nb;
       if (!(win_v >= tol) || win_v == 0.0) {
         if (cta == 0 && tid == 0) {
           p.status[0] = (double)j;
@@ -153,29 +184,37 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
         }
         return;  // uniform across the grid
       }
-      for (int c = tid; c < jb; c += LU_THREADS) urow[c] = wrow[c];
-      if (tid == 0) {
-        if (win_r >= r0 && win_r < r1) pivflag[win_r - r0] = j;
-        if (cta == 0) p.pivrow[j] = win_r;
-      }
-      __syncthreads();
+      if (prof) t3 = clock64();
       const double upiv = urow[jj];
+      cbv = -1.0;
+      cbr = 0x7fffffff;
+      const bool look = jj + 1 < jb;
       for (int i = tid; i < nr; i += LU_THREADS) {
         if (pivflag[i] >= 0) continue;
         double* row = P + i * LD;
         const double l = row[jj] / upiv;
         row[jj] = l;
         for (int c = jj + 1; c < jb; ++c) row[c] = fma(-l, urow[c], row[c]);
+        if (look) better(cbv, cbr, fabs(row[jj + 1]), r0 + i);
       }
       __syncthreads();
       par ^= 1;
+      if (prof) {
+        const long long t4 = clock64();
+        prof[0] += t1 - t0;
+        prof[1] += t2 - t1;
+        prof[2] += t3 - t2;
+        prof[3] += t4 - t3;
+      }
     }
     // write the panel back
+    const long long tp0 = prof ? clock64() : 0;
     for (int e = tid; e < nr * jb; e += LU_THREADS) {
       int i = e / jb, c = e - (e / jb) * jb;
       p.X[(long long)(r0 + i) * p.ldx + J + c] = P[i * LD + c];
     }
     const int rest = p.n - J - jb;
+    if (prof && rest <= 0) prof[4] += clock64() - tp0;
     if (rest > 0) {
       grid.sync();
       // unit-lower L11 from the pivot rows' multipliers
@@ -199,17 +238,38 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
             U12[a * LU_CHUNK + c] = s;
           }
         __syncthreads();
-        for (int e = tid; e < nr * cw; e += LU_THREADS) {
-          int i = e / cw, c = e - (e / cw) * cw;
-          if (pivflag[i] >= 0) continue;
-          double* xp = p.X + (long long)(r0 + i) * p.ldx + J + jb + c0 + c;
-          double s = *xp;
-          const double* li = P + i * LD;
-          for (int a = 0; a < jb; ++a) s = fma(-li[a], U12[a * LU_CHUNK + c], s);
-          *xp = s;
+        // X[rows, chunk] -= L[rows, panel] U12: thread = (column c, row lane);
+        // 8 rows per iteration so 8 global loads are in flight per thread
+        {
+          constexpr int RL = LU_THREADS / LU_CHUNK;  // row lanes
+          const int c = tid % LU_CHUNK, rl = tid / LU_CHUNK;
+          if (c < cw) {
+            for (int ib = rl; ib < nr; ib += RL * 8) {
+              double xv[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int i = ib + u * RL;
+                xv[u] = (i < nr && pivflag[i] < 0) ? p.X[(long long)(r0 + i) * p.ldx + J + jb + c0 + c] : 0.0;
+              }
+              for (int a = 0; a < jb; ++a) {
+                const double u12 = U12[a * LU_CHUNK + c];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                  const int i = min(ib + u * RL, nr - 1);
+                  xv[u] = fma(-P[i * LD + a], u12, xv[u]);
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int i = ib + u * RL;
+                if (i < nr && pivflag[i] < 0) p.X[(long long)(r0 + i) * p.ldx + J + jb + c0 + c] = xv[u];
+              }
+            }
+          }
         }
         __syncthreads();
       }
+      if (prof) prof[4] += clock64() - tp0;
     }
   }
   // pivot rows: unit entry at their step, zeros to the right
@@ -236,8 +296,11 @@ static size_t lu_smem_bytes(int rows_per, int nb) {
 static LuPlan lu_plan(int m, int n) {
   LuPlan pl{};
   const int sms = sm_count();
-  const size_t limit2 = 110 * 1024, limit1 = 220 * 1024;
-  for (int occ = 2; occ >= 1; --occ) {
+  // CTAs per SM (tunable: LR_LU_OCC); fewer CTAs = fewer candidates per
+  // column and a cheaper barrier, more = less per-column work per CTA
+  static const int occ_pref = getenv("LR_LU_OCC") ? atoi(getenv("LR_LU_OCC")) : 2;
+  for (int occ = occ_pref; occ >= 1; --occ) {
+    const size_t limit = (226 * 1024) / occ - 1024;
     int G = sms * occ;
     if (G > (m + 31) / 32) G = (m + 31) / 32;
     if (G < 1) G = 1;
@@ -246,7 +309,7 @@ static LuPlan lu_plan(int m, int n) {
     for (int nb = 32; nb >= 1; nb >>= 1) {
       int nbe = nb > n ? n : nb;
       size_t sm = lu_smem_bytes(rows_per, nbe);
-      if (sm <= (occ == 2 ? limit2 : limit1)) {
+      if (sm <= limit) {
         pl.G = G;
         pl.nb = nbe;
         pl.rows_per = rows_per;
@@ -268,7 +331,7 @@ extern "C" {
 long long lr_lu_workspace_doubles(int m, int n) {
   LuPlan pl = lu_plan(m, n);
   long long G = pl.G > 0 ? pl.G : 1;
-  return 4 * G + 2 * G * 32 + n + 8 + lr_stats_partials() + 8;
+  return 4 * G + 2 * G * 32 + n + 8 + lr_stats_partials() + 16;
 }
 
 int lr_lu_pl_f64(int m, int n, double* X, long long ldx, double* work, double* status_host,
@@ -310,10 +373,23 @@ int lr_lu_pl_f64(int m, int n, double* X, long long ldx, double* work, double* s
   prm.prow = prow;
   prm.pivrow = pivrow;
   prm.status = status;
+  static const bool profile = getenv("LR_LU_PROFILE") != nullptr;
+  long long* dprof = reinterpret_cast<long long*>(partial + lr_stats_partials());
+  prm.prof = profile ? dprof : nullptr;
+  if (profile) LR_CHECK_CUDA(cudaMemsetAsync(dprof, 0, 8 * sizeof(long long), s));
   void* args[] = {&prm};
   LR_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)lu_kernel, dim3((unsigned)G), dim3(LU_THREADS), args,
                                             pl.smem, s));
   count_launches(1);
+  if (profile) {
+    long long hp[8];
+    LR_CHECK_CUDA(cudaMemcpyAsync(hp, dprof, sizeof(hp), cudaMemcpyDeviceToHost, s));
+    LR_CHECK_CUDA(cudaStreamSynchronize(s));
+    fprintf(stderr,
+            "lu %dx%d G=%lld nb=%d cycles/col: local %.0f barrier %.0f winner %.0f update %.0f; panel ends total %.0f\n",
+            m, n, G, pl.nb, (double)hp[0] / n, (double)hp[1] / n, (double)hp[2] / n, (double)hp[3] / n,
+            (double)hp[4]);
+  }
   double host[8];
   LR_CHECK_CUDA(cudaMemcpyAsync(host, status, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
   LR_CHECK_CUDA(cudaMemcpyAsync(host + 4, stats, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -39,6 +39,7 @@ struct TdParams {
   double* Vr;    // n x n: row j holds reflector j at columns j+1..n-1 (v[j+1] = 1)
   double* vbuf;  // 2 x n
   double* pbuf;  // 2 x n
+  double* rows_global;  // n x (n+1) working rows when they do not fit shared memory, else null
 };
 
 __device__ __forceinline__ void td_barrier(cg::grid_group& grid) {
@@ -56,9 +57,10 @@ __global__ void __launch_bounds__(TD_THREADS) tridiag_kernel(TdParams P) {
   const int r1 = min(n, r0 + P.rows_per);
   const int nr = max(0, r1 - r0);
   const int LD = n + 1;
-  double* R = td_smem;                       // nr x LD (my rows)
-  double* v = R + (size_t)P.rows_per * LD;   // n
-  double* p = v + n;                         // n
+  // my rows: shared memory when they fit, else a global (L2-resident) slab
+  double* R = P.rows_global ? P.rows_global + (size_t)r0 * LD : td_smem;
+  double* v = P.rows_global ? td_smem : td_smem + (size_t)P.rows_per * LD;  // n
+  double* p = v + n;                                                       // n
   __shared__ double red[32];
   __shared__ double sh_tau, sh_k;
 
@@ -387,20 +389,20 @@ __global__ void __launch_bounds__(128) backtransform_kernel(const double* __rest
 struct TdPlan {
   int G, rows_per;
   size_t smem;
+  bool global_rows;
 };
 
+// one CTA per SM at most (cooperative residency); rows go to shared memory
+// when they fit, otherwise to a global slab (n >~ 1300)
 static TdPlan td_plan(int n) {
   TdPlan pl;
   const int sms = sm_count();
   int G = n <= 96 ? 1 : (n < sms ? n : sms);
   int rows_per = (n + G - 1) / G;
-  size_t smem = ((size_t)rows_per * (n + 1) + 2 * (size_t)n) * sizeof(double);
-  while (smem > 200 * 1024 && G < 2 * sms) {
-    G = G * 2 > 2 * sms ? 2 * sms : G * 2;
-    rows_per = (n + G - 1) / G;
-    smem = ((size_t)rows_per * (n + 1) + 2 * (size_t)n) * sizeof(double);
-  }
   G = (n + rows_per - 1) / rows_per;
+  size_t smem = ((size_t)rows_per * (n + 1) + 2 * (size_t)n) * sizeof(double);
+  pl.global_rows = smem > 200 * 1024;
+  if (pl.global_rows) smem = 2 * (size_t)n * sizeof(double);
   pl.G = G;
   pl.rows_per = rows_per;
   pl.smem = smem;
@@ -415,8 +417,8 @@ extern "C" {
 
 long long lr_syevd_workspace_doubles(int n) {
   const long long N = n;
-  // d, e, tau, e2, w, bounds | Vr | vbuf, pbuf | Z, U1, U2, Lm, Dg | Pv (ints) | clusters
-  return 6 * N + 8 + N * N + 4 * N + 5 * N * N + N * N / 2 + N + N + 64;
+  // d, e, tau, e2, w, bounds | Vr | vbuf, pbuf | Z, U1, U2, Lm, Dg | Pv (ints) | clusters | global rows
+  return 6 * N + 8 + N * N + 4 * N + 5 * N * N + N * N / 2 + N + N + 64 + N * (N + 1);
 }
 
 int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V, long long ldv, double* work,
@@ -468,6 +470,7 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
   P.Vr = Vr;
   P.vbuf = vbuf;
   P.pbuf = pbuf;
+  P.rows_global = pl.global_rows ? reinterpret_cast<double*>(clus) + N + 64 : nullptr;
   LR_CHECK_CUDA(cudaMemsetAsync(tau, 0, N * sizeof(double), s));
   static const bool timing = getenv("LR_SYEVD_TIMING") != nullptr;
   cudaEvent_t ev[6];
@@ -526,7 +529,8 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
   if (clusters_host) *clusters_host = ncl;
   if (timing) cudaEventRecord(ev[4], s);
   // 5. back-transform and eigenvalues out
-  const int wpb = 4;
+  const int wpb = (size_t)n * 4 * sizeof(double) <= 200 * 1024 ? 4 : 1;
+  LR_REQUIRE((size_t)n * wpb * sizeof(double) <= 200 * 1024, "syevd: n = %d too large for the back-transform", n);
   backtransform_kernel<<<(n + wpb - 1) / wpb, 32 * wpb, (size_t)wpb * n * sizeof(double), s>>>(Z, Vr, tau, n, V, ldv);
   LR_CHECK_LAUNCH();
   LR_CHECK_CUDA(cudaMemcpyAsync(d_out, w, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
