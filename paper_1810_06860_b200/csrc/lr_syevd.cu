@@ -3,20 +3,24 @@
 // `sym_eig` / `eig_svd` (linalg.py:153-202; survey K5).
 //
 //   1. tridiag   : one cooperative kernel; the n x n matrix is row-distributed
-//                  over the CTAs' shared memory.  Per column: the owner of row
-//                  j builds the reflector (dlarfg convention), one grid barrier
-//                  publishes v, every CTA forms its slice of p = tau*A*v, a
-//                  second barrier publishes p, every CTA applies the rank-2
-//                  update A -= v w^T + w v^T to its rows (w = p - tau/2 (p.v) v).
+//                  over the CTAs' shared memory.  ONE grid barrier per column:
+//                  every CTA publishes its slice of p = tau*A*v and the owner
+//                  of row j+1 publishes that row; after the barrier every CTA
+//                  forms w = p - tau/2 (p.v) v, applies A -= v w^T + w v^T to
+//                  its rows and derives the next reflector (dlarfg convention)
+//                  redundantly from the published row -- bit-identical in all
+//                  CTAs.  (single CTA, 1024 threads, for n <= 96)
 //   2. bisection : one warp per eigenvalue, 32-way multisection on Sturm counts
 //                  (eigenvalue i is the i-th smallest: the output is ascending).
-//   3. inverse iteration : one thread per eigenvalue, tridiagonal LU with
-//                  partial pivoting (coalesced [row][eigenvalue] scratch).
+//   3. inverse iteration : one thread per eigenvalue, two solves with the
+//                  dlagtf-pivoted tridiagonal LU ([row][eigenvalue] scratch).
 //   4. clusters  : eigenvalues closer than 1e-8*||T|| are re-orthonormalised
 //                  (modified Gram-Schmidt, twice) by one CTA per cluster.
-//   5. back-transform : one warp per eigenvector applies H_{n-3} ... H_0.
+//   5. back-transform : compact WY blocks of 32 reflectors (T factors built in
+//                  parallel), applied by one CTA per 8 eigenvector columns with
+//                  the block's reflectors staged in shared memory.
 // Accuracy is LAPACK's: eigenvalues to O(eps*||A||) absolute, eigenvectors to
-// O(eps*||A||/gap).  Latency-bound (2 grid barriers per column): reported as
+// O(eps*||A||/gap).  Latency-bound (one grid barrier per column): reported as
 // time and share of the step.
 #include <cooperative_groups.h>
 #include <cstdlib>
@@ -40,6 +44,7 @@ struct TdParams {
   double* vbuf;  // 2 x n
   double* pbuf;  // 2 x n
   double* rows_global;  // n x (n+1) working rows when they do not fit shared memory, else null
+  long long* prof;      // optional per-phase clocks of CTA 0 (LR_SYEVD_TIMING)
 };
 
 __device__ __forceinline__ void td_barrier(cg::grid_group& grid) {
@@ -49,7 +54,49 @@ __device__ __forceinline__ void td_barrier(cg::grid_group& grid) {
     grid.sync();
 }
 
-__global__ void __launch_bounds__(TD_THREADS) tridiag_kernel(TdParams P) {
+// Reflector of x[j+1:] (dlarfg): every CTA computes it redundantly from the
+// same data in the same order, so all CTAs hold bit-identical v and tau.
+template <int THREADS>
+__device__ __forceinline__ void td_reflector(const double* x, int j, int n, double* v, double* red, double* sh,
+                                             const TdParams& P, bool record) {
+  const int tid = threadIdx.x;
+  double ss = 0.0;
+  for (int c = j + 2 + tid; c < n; c += THREADS) ss = fma(x[c], x[c], ss);
+  ss = block_sum<THREADS>(ss, red);
+  if (tid == 0) {
+    const double alpha = x[j + 1];
+    double tau = 0.0, beta = alpha, scal = 0.0;
+    if (ss != 0.0) {
+      const double nrm = sqrt(alpha * alpha + ss);
+      beta = (alpha >= 0.0) ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    sh[0] = tau;
+    sh[1] = scal;
+    if (record) {
+      P.d[j] = x[j];
+      P.e[j] = beta;
+      P.tau[j] = tau;
+    }
+  }
+  __syncthreads();
+  const double tau = sh[0], scal = sh[1];
+  for (int c = j + 1 + tid; c < n; c += THREADS) {
+    const double vc = (c == j + 1) ? 1.0 : (tau == 0.0 ? 0.0 : x[c] * scal);
+    v[c] = vc;
+    if (record) P.Vr[(long long)j * n + c] = vc;
+  }
+  __syncthreads();
+}
+
+// One grid barrier per column: before the barrier every CTA publishes its
+// slice of p = tau*A*v and the owner of row j+1 publishes that row (state
+// after step j-1); after it every CTA forms w, updates its rows, rebuilds
+// row j+1 after step j from the published copy with the same rank-2 formula
+// and derives the next reflector redundantly.
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double td_smem[];
   const int n = P.n, tid = threadIdx.x;
@@ -60,59 +107,36 @@ __global__ void __launch_bounds__(TD_THREADS) tridiag_kernel(TdParams P) {
   // my rows: shared memory when they fit, else a global (L2-resident) slab
   double* R = P.rows_global ? P.rows_global + (size_t)r0 * LD : td_smem;
   double* v = P.rows_global ? td_smem : td_smem + (size_t)P.rows_per * LD;  // n
-  double* p = v + n;                                                       // n
+  double* w = v + n;                                                       // n
+  double* x = w + n;                                                       // n
   __shared__ double red[32];
-  __shared__ double sh_tau, sh_k;
+  __shared__ double sh[4];
+  const bool rec = blockIdx.x == 0;
 
-  for (int e = tid; e < nr * n; e += TD_THREADS) {
+  for (int e = tid; e < nr * n; e += THREADS) {
     const int i = e / n, c = e - (e / n) * n;
     R[i * LD + c] = P.A[(long long)(r0 + i) * P.lda + c];
   }
+  // row 0 to every CTA, then the first reflector
+  if (r0 == 0)
+    for (int c = tid; c < n; c += THREADS) P.vbuf[c] = P.A[c];
+  td_barrier(grid);
+  for (int c = tid; c < n; c += THREADS) x[c] = P.vbuf[c];
   __syncthreads();
+  if (n > 2) td_reflector<THREADS>(x, 0, n, v, red, sh, P, rec);
 
   for (int j = 0; j + 2 < n; ++j) {
     const int par = j & 1;
-    double* vg = P.vbuf + par * n;
     double* pg = P.pbuf + par * n;
-    const int L = n - j - 1;  // trailing indices j+1 .. n-1
-    if (j >= r0 && j < r1) {
-      // owner: Householder reflector from x = A[j][j+1:]  (dlarfg)
-      const double* row = R + (j - r0) * LD;
-      double ss = 0.0;
-      for (int c = j + 2 + tid; c < n; c += TD_THREADS) ss = fma(row[c], row[c], ss);
-      ss = block_sum<TD_THREADS>(ss, red);
-      if (tid == 0) {
-        const double alpha = row[j + 1];
-        double tau = 0.0, beta = alpha, scal = 0.0;
-        if (ss != 0.0) {
-          const double nrm = sqrt(alpha * alpha + ss);
-          beta = (alpha >= 0.0) ? -nrm : nrm;
-          tau = (beta - alpha) / beta;
-          scal = 1.0 / (alpha - beta);
-        }
-        P.d[j] = row[j];
-        P.e[j] = beta;
-        P.tau[j] = tau;
-        sh_tau = scal;  // temporarily the v scale
-        sh_k = tau;
-      }
-      __syncthreads();
-      const double scal = sh_tau;
-      const double tau = sh_k;
-      for (int c = j + 1 + tid; c < n; c += TD_THREADS) {
-        const double vc = (c == j + 1) ? 1.0 : (tau == 0.0 ? 0.0 : row[c] * scal);
-        vg[c] = vc;
-        P.Vr[(long long)j * n + c] = vc;
-      }
-    }
-    td_barrier(grid);
-    const double tau = P.tau[j];
-    for (int c = j + 1 + tid; c < n; c += TD_THREADS) v[c] = vg[c];
-    __syncthreads();
+    double* rg = P.vbuf + (1 - par) * n;  // row j+1 (vbuf[0] held row 0)
+    const double tau = sh[0];
+    long long* prof = (P.prof && blockIdx.x == 0 && tid == 0) ? P.prof : nullptr;
+    long long tp[6];
+    if (prof) tp[0] = clock64();
+    // (a) my slice of p, (b) the owner publishes row j+1
     if (tau != 0.0) {
-      // p_r = tau * sum_c A[r][c] v[c] for my rows r >= j+1 (one warp per row)
-      const int lane = tid & 31, w = tid >> 5;
-      for (int i = w; i < nr; i += TD_THREADS / 32) {
+      const int lane = tid & 31, wp = tid >> 5;
+      for (int i = wp; i < nr; i += THREADS / 32) {
         const int r = r0 + i;
         if (r <= j) continue;
         const double* row = R + i * LD;
@@ -122,39 +146,67 @@ __global__ void __launch_bounds__(TD_THREADS) tridiag_kernel(TdParams P) {
         if (lane == 0) pg[r] = tau * s;
       }
     }
+    if (j + 1 >= r0 && j + 1 < r1)
+      for (int c = j + 1 + tid; c < n; c += THREADS) rg[c] = R[(j + 1 - r0) * LD + c];
+    if (prof) tp[1] = clock64();
     td_barrier(grid);
+    if (prof) tp[2] = clock64();
+    // (c) w = p - (tau/2)(p.v) v  (every CTA, full length); row j+1 copy in
+    // the same pass so both vectors cost one L2 round trip
     if (tau != 0.0) {
-      for (int c = j + 1 + tid; c < n; c += TD_THREADS) p[c] = pg[c];
-      __syncthreads();
       double pv = 0.0;
-      for (int c = j + 1 + tid; c < n; c += TD_THREADS) pv = fma(p[c], v[c], pv);
-      pv = block_sum<TD_THREADS>(pv, red);
-      if (tid == 0) sh_k = 0.5 * tau * pv;
+      for (int c = j + 1 + tid; c < n; c += THREADS) {
+        const double pc = pg[c];
+        x[c] = rg[c];
+        w[c] = pc;
+        pv = fma(pc, v[c], pv);
+      }
+      pv = block_sum<THREADS>(pv, red);  // valid in thread 0
+      if (tid == 0) sh[2] = 0.5 * tau * pv;
       __syncthreads();
-      const double K = sh_k;
-      for (int c = j + 1 + tid; c < n; c += TD_THREADS) p[c] = p[c] - K * v[c];  // w
-      __syncthreads();
-      for (int e = tid; e < nr * L; e += TD_THREADS) {
-        const int i = e / L, c = j + 1 + (e - (e / L) * L);
-        const int r = r0 + i;
-        if (r <= j) continue;
-        // symmetric in (r, c): products are exact-commutative, sum order fixed
-        const double upd = __dadd_rn(__dmul_rn(v[r], p[c]), __dmul_rn(p[r], v[c]));
-        R[i * LD + c] -= upd;
+      const double K = sh[2];
+      for (int c = j + 1 + tid; c < n; c += THREADS) w[c] = w[c] - K * v[c];
+    } else {
+      for (int c = j + 1 + tid; c < n; c += THREADS) {
+        w[c] = 0.0;
+        x[c] = rg[c];
       }
     }
     __syncthreads();
-  }
-  // last 2x2 block
-  for (int r = r0; r < r1; ++r) {
-    if (tid != 0) break;
-    if (r == n - 2) {
-      P.d[n - 2] = R[(r - r0) * LD + n - 2];
-      P.e[n - 2] = R[(r - r0) * LD + n - 1];
+    if (prof) tp[3] = clock64();
+    // (d) rank-2 update of my rows; (e) row j+1 after step j from the copy
+    if (tau != 0.0) {
+      const int lane = tid & 31, wp = tid >> 5;
+      for (int i = max(0, j + 1 - r0) + wp; i < nr; i += THREADS / 32) {  // warp per row
+        const int r = r0 + i;
+        const double vr = v[r], wr = w[r];
+        double* row = R + i * LD;
+        for (int c = j + 1 + lane; c < n; c += 32) row[c] -= __dadd_rn(__dmul_rn(vr, w[c]), __dmul_rn(wr, v[c]));
+      }
+      for (int c = j + 1 + tid; c < n; c += THREADS)
+        x[c] -= __dadd_rn(__dmul_rn(v[j + 1], w[c]), __dmul_rn(w[j + 1], v[c]));
     }
-    if (r == n - 1) P.d[n - 1] = R[(r - r0) * LD + n - 1];
-    if (n == 1 && r == 0) P.d[0] = R[0];
+    __syncthreads();
+    if (prof) tp[4] = clock64();
+    if (j + 3 < n) {
+      td_reflector<THREADS>(x, j + 1, n, v, red, sh, P, rec);
+    } else if (rec && tid == 0) {  // j + 1 == n - 2: the last 2 x 2 block
+      P.d[n - 2] = x[n - 2];
+      P.e[n - 2] = x[n - 1];
+      sh[0] = 0.0;
+    }
+    __syncthreads();
+    if (prof) {
+      tp[5] = clock64();
+      for (int q = 0; q < 5; ++q) prof[q] += tp[q + 1] - tp[q];
+    }
   }
+  if (n == 2 && rec && tid == 0) {
+    P.d[0] = x[0];
+    P.e[0] = x[1];
+  }
+  // d[n-1] from the owner of the last row (after all updates)
+  if (tid == 0 && n - 1 >= r0 && n - 1 < r1) P.d[n - 1] = R[(n - 1 - r0) * LD + n - 1];
 }
 
 // Sturm count: number of eigenvalues of T strictly below x
@@ -279,7 +331,9 @@ __global__ void inviter_kernel(const double* __restrict__ d, const double* __res
   Dg[IX(n - 1)] = (a == 0.0) ? tiny : a;
   unsigned long long s = 0x9E3779B97F4A7C15ULL * (unsigned long long)(k + 1);
   double scale = 1.0;
-  for (int it = 0; it < 3; ++it) {
+  // two solves: the shift is accurate to ~1e-3 eps ||T|| (bisection), so the
+  // first solve already amplifies the wanted direction by ~1/(eps*||T||)
+  for (int it = 0; it < 2; ++it) {
     // forward: z <- L^{-1} P (scale * z); the start vector is generated in pass 0
     double zc;
     if (it == 0) {
@@ -362,28 +416,112 @@ __global__ void __launch_bounds__(256) cluster_mgs_kernel(double* Z, int n, cons
   }
 }
 
-// V[:, k] = H_0 H_1 ... H_{n-3} Z[:, k]; one warp per column, column staged in smem
-__global__ void __launch_bounds__(128) backtransform_kernel(const double* __restrict__ Z, const double* __restrict__ Vr,
-                                                          const double* __restrict__ tau, int n, double* __restrict__ V,
-                                                          long long ldv) {
-  extern __shared__ double bt_smem[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int k = blockIdx.x * (blockDim.x >> 5) + wib;
-  if (k >= n) return;
-  double* x = bt_smem + (size_t)wib * n;
-  for (int i = lane; i < n; i += 32) x[i] = Z[(long long)i * n + k];
-  __syncwarp();
-  for (int j = n - 3; j >= 0; --j) {
-    const double t = tau[j];
-    if (t == 0.0) continue;
-    const double* v = Vr + (long long)j * n;
-    double s = 0.0;
-    for (int i = j + 1 + lane; i < n; i += 32) s = fma(v[i], x[i], s);
-    s = warp_sum(s) * t;
-    for (int i = j + 1 + lane; i < n; i += 32) x[i] = fma(-s, v[i], x[i]);
-    __syncwarp();
+// T factor of each block of kWY reflectors (dlarft, forward, columnwise):
+// T_ii = tau_i, T[0:i, i] = -tau_i T[0:i, 0:i] (V[:, 0:i]^T v_i).  Vr rows hold
+// the reflectors with explicit zeros left of the unit entry.
+constexpr int kWY = 32;
+__global__ void __launch_bounds__(256) build_T_kernel(const double* __restrict__ Vr, const double* __restrict__ tau,
+                                                    int n, int nrefl, double* __restrict__ T) {
+  __shared__ double G[kWY][kWY + 1];
+  __shared__ double Ts[kWY][kWY + 1];
+  const int b = blockIdx.x, J = b * kWY;
+  const int bs = min(kWY, nrefl - J);
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  // G[k][i] = v_{J+k} . v_{J+i}, k < i (overlap starts at column J+i+1)
+  for (int pr = wp; pr < kWY * kWY; pr += 8) {
+    const int k = pr / kWY, i = pr % kWY;
+    if (k >= i || i >= bs) continue;
+    const double* a = Vr + (long long)(J + k) * n;
+    const double* c = Vr + (long long)(J + i) * n;
+    double sacc = 0.0;
+    for (int col = J + i + 1 + lane; col < n; col += 32) sacc = fma(a[col], c[col], sacc);
+    sacc = warp_sum(sacc);
+    if (lane == 0) G[k][i] = sacc;
   }
-  for (int i = lane; i < n; i += 32) V[(long long)i * ldv + k] = x[i];
+  for (int e = threadIdx.x; e < kWY * kWY; e += 256) Ts[e / kWY][e % kWY] = 0.0;
+  __syncthreads();
+  for (int i = 0; i < bs; ++i) {
+    const double ti = tau[J + i];
+    if (threadIdx.x < i) {
+      const int r = threadIdx.x;
+      double acc = 0.0;
+      for (int k = r; k < i; ++k) acc = fma(Ts[r][k], G[k][i], acc);
+      Ts[r][i] = -ti * acc;
+    }
+    if (threadIdx.x == 0) Ts[i][i] = ti;
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < kWY * kWY; e += 256) T[(long long)b * kWY * kWY + e] = Ts[e / kWY][e % kWY];
+}
+
+// All reflector blocks applied to a tile of kTC eigenvector columns by one
+// CTA (columns are independent: no inter-CTA dependency, one launch):
+// for b = last..0:  Y = V_b^T Z_tile, Y = T_b Y, Z_tile -= V_b Y.
+constexpr int kTC = 8;
+__global__ void __launch_bounds__(256) wy_apply_kernel(double* __restrict__ Z, int n, const double* __restrict__ Vr,
+                                                     const double* __restrict__ T, int nrefl, double* __restrict__ V,
+                                                     long long ldv, int stage_v) {
+  extern __shared__ double zs[];  // n x kTC
+  __shared__ double Y[kWY][kTC];
+  __shared__ double Y2[kWY][kTC];
+  __shared__ double Ts[kWY][kWY + 1];
+  const int tid = threadIdx.x;
+  const int c0 = blockIdx.x * kTC;
+  const int tc = min(kTC, n - c0);
+  for (int e = tid; e < n * kTC; e += 256) {
+    const int i = e / kTC, t = e % kTC;
+    zs[e] = (t < tc) ? Z[(long long)i * n + c0 + t] : 0.0;
+  }
+  const int nblk = (nrefl + kWY - 1) / kWY;
+  const int k = tid / kTC, t = tid % kTC;  // 32 x 8 threads
+  // staged: the block's reflector rows live in shared memory (ld n+1, odd)
+  double* vb = stage_v ? zs + (size_t)n * kTC : nullptr;
+  const int LDV = n + 1;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int J = b * kWY;
+    const int bsb = min(kWY, nrefl - J);
+    for (int e = tid; e < kWY * kWY; e += 256) Ts[e / kWY][e % kWY] = T[(long long)b * kWY * kWY + e];
+    if (vb) {
+      const int L = n - J - 1;
+      for (int e = tid; e < bsb * L; e += 256) {
+        const int q = e / L, c = J + 1 + (e - (e / L) * L);
+        vb[q * LDV + c] = Vr[(long long)(J + q) * n + c];
+      }
+    }
+    __syncthreads();
+    double acc = 0.0;
+    if (k < bsb) {
+      if (vb) {
+        const double* vrow = vb + k * LDV;
+#pragma unroll 4
+        for (int c = J + 1; c < n; ++c) acc = fma(vrow[c], zs[c * kTC + t], acc);
+      } else {
+        const double* vrow = Vr + (long long)(J + k) * n;
+#pragma unroll 4
+        for (int c = J + 1; c < n; ++c) acc = fma(vrow[c], zs[c * kTC + t], acc);
+      }
+    }
+    Y[k][t] = acc;
+    __syncthreads();
+    double a2 = 0.0;
+    for (int q = 0; q < bsb; ++q) a2 = fma(Ts[k][q], Y[q][t], a2);
+    Y2[k][t] = a2;
+    __syncthreads();
+    for (int c = J + 1 + tid / kTC; c < n; c += 256 / kTC) {
+      double s = zs[c * kTC + t];
+      if (vb) {
+        for (int q = 0; q < bsb; ++q) s = fma(-vb[q * LDV + c], Y2[q][t], s);
+      } else {
+        for (int q = 0; q < bsb; ++q) s = fma(-Vr[(long long)(J + q) * n + c], Y2[q][t], s);
+      }
+      zs[c * kTC + t] = s;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * kTC; e += 256) {
+    const int i = e / kTC, tt = e % kTC;
+    if (tt < tc) V[(long long)i * ldv + c0 + tt] = zs[e];
+  }
 }
 
 struct TdPlan {
@@ -397,12 +535,16 @@ struct TdPlan {
 static TdPlan td_plan(int n) {
   TdPlan pl;
   const int sms = sm_count();
-  int G = n <= 96 ? 1 : (n < sms ? n : sms);
+  // CTAs: every CTA re-reads the broadcast vectors each column, so fewer,
+  // fatter CTAs cut L2 contention (tunable: LR_TD_ROWS = rows per CTA)
+  static const int rows_pref = getenv("LR_TD_ROWS") ? atoi(getenv("LR_TD_ROWS")) : 4;
+  int G = n <= 96 ? 1 : (n + rows_pref - 1) / rows_pref;
+  if (G > sms) G = sms;
   int rows_per = (n + G - 1) / G;
   G = (n + rows_per - 1) / rows_per;
-  size_t smem = ((size_t)rows_per * (n + 1) + 2 * (size_t)n) * sizeof(double);
+  size_t smem = ((size_t)rows_per * (n + 1) + 3 * (size_t)n) * sizeof(double);
   pl.global_rows = smem > 200 * 1024;
-  if (pl.global_rows) smem = 2 * (size_t)n * sizeof(double);
+  if (pl.global_rows) smem = 3 * (size_t)n * sizeof(double);
   pl.G = G;
   pl.rows_per = rows_per;
   pl.smem = smem;
@@ -452,12 +594,15 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
   TdPlan pl = td_plan(n);
   static bool attr = false;
   if (!attr) {
-    LR_CHECK_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    LR_CHECK_CUDA(cudaFuncSetAttribute(backtransform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    LR_CHECK_CUDA(cudaFuncSetAttribute(tridiag_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    LR_CHECK_CUDA(cudaFuncSetAttribute(tridiag_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    LR_CHECK_CUDA(cudaFuncSetAttribute(wy_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
     attr = true;
   }
   int occ = 0;
-  LR_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tridiag_kernel, TD_THREADS, pl.smem));
+  const bool single = pl.G == 1;
+  const void* tdk = single ? (const void*)tridiag_kernel<1024> : (const void*)tridiag_kernel<256>;
+  LR_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tdk, single ? 1024 : 256, pl.smem));
   LR_REQUIRE((long long)occ * sm_count() >= pl.G, "syevd: cooperative grid %d exceeds residency", pl.G);
   TdParams P;
   P.A = A;
@@ -471,7 +616,12 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
   P.vbuf = vbuf;
   P.pbuf = pbuf;
   P.rows_global = pl.global_rows ? reinterpret_cast<double*>(clus) + N + 64 : nullptr;
+  static const bool timing_env = getenv("LR_SYEVD_TIMING") != nullptr;
+  // phase clocks borrow the eigenvalue buffer w (written only after the reduction)
+  P.prof = (timing_env && n >= 8) ? reinterpret_cast<long long*>(w) : nullptr;
+  if (P.prof) LR_CHECK_CUDA(cudaMemsetAsync(w, 0, 8 * sizeof(double), s));
   LR_CHECK_CUDA(cudaMemsetAsync(tau, 0, N * sizeof(double), s));
+  LR_CHECK_CUDA(cudaMemsetAsync(Vr, 0, N * N * sizeof(double), s));  // zeros left of each unit entry
   static const bool timing = getenv("LR_SYEVD_TIMING") != nullptr;
   cudaEvent_t ev[6];
   if (timing)
@@ -480,10 +630,16 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
     }
   if (timing) cudaEventRecord(ev[0], s);
   void* args[] = {&P};
-  LR_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)tridiag_kernel, dim3(pl.G), dim3(TD_THREADS), args,
-                                            pl.smem, s));
+  LR_CHECK_CUDA(cudaLaunchCooperativeKernel(tdk, dim3(pl.G), dim3(single ? 1024 : 256), args, pl.smem, s));
   count_launches(1);
   if (timing) cudaEventRecord(ev[1], s);
+  if (P.prof) {
+    long long hp[5];
+    cudaMemcpyAsync(hp, P.prof, sizeof(hp), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "tridiag n=%d G=%d cycles/col: p+publish %.0f barrier %.0f w+x %.0f update %.0f reflector %.0f\n", n,
+            pl.G, (double)hp[0] / n, (double)hp[1] / n, (double)hp[2] / n, (double)hp[3] / n, (double)hp[4] / n);
+  }
   // 2. eigenvalues (ascending) by multisection
   tri_prep_kernel<<<1, 256, 0, s>>>(d, e, n, e2, bounds);
   LR_CHECK_LAUNCH();
@@ -529,10 +685,28 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
   if (clusters_host) *clusters_host = ncl;
   if (timing) cudaEventRecord(ev[4], s);
   // 5. back-transform and eigenvalues out
-  const int wpb = (size_t)n * 4 * sizeof(double) <= 200 * 1024 ? 4 : 1;
-  LR_REQUIRE((size_t)n * wpb * sizeof(double) <= 200 * 1024, "syevd: n = %d too large for the back-transform", n);
-  backtransform_kernel<<<(n + wpb - 1) / wpb, 32 * wpb, (size_t)wpb * n * sizeof(double), s>>>(Z, Vr, tau, n, V, ldv);
-  LR_CHECK_LAUNCH();
+  // blocked (compact WY) back-transform: Z <- B_0 (B_1 (... (B_last Z))),
+  // B_b = H_J ... H_{J+31} = I - V_b T_b V_b^T, three DMMA GEMMs per block
+  if (n > 2) {
+    const int nrefl = n - 2;  // reflectors 0 .. n-3
+    const int nblk = (nrefl + kWY - 1) / kWY;
+    double* Tb = Lm;   // nblk x kWY x kWY (inverse-iteration scratch is free now)
+    double* Yb = U1;   // kWY x n
+    double* Y2 = U2;   // kWY x n
+    build_T_kernel<<<nblk, 256, 0, s>>>(Vr, tau, n, nrefl, Tb);
+    LR_CHECK_LAUNCH();
+    (void)Yb;
+    (void)Y2;
+    const size_t zsm = (size_t)n * kTC * sizeof(double);
+    const size_t vsm = (size_t)kWY * (n + 1) * sizeof(double);
+    const int stage = zsm + vsm <= 210 * 1024;
+    LR_REQUIRE(zsm <= 200 * 1024, "syevd: n = %d too large for the back-transform tile", n);
+    wy_apply_kernel<<<(n + kTC - 1) / kTC, 256, stage ? zsm + vsm : zsm, s>>>(Z, n, Vr, Tb, nrefl, V, ldv, stage);
+    LR_CHECK_LAUNCH();
+  } else {
+    int st = lr_copy2d_f64(Z, n, V, ldv, n, n, 0, stream);
+    if (st) return st;
+  }
   LR_CHECK_CUDA(cudaMemcpyAsync(d_out, w, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
   if (timing) {
     cudaEventRecord(ev[5], s);
