@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-baseline", choices=["full", "skip"], default="full")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--svt", choices=["on", "off"], default="on")
     return ap.parse_args()
 
 
@@ -151,6 +152,75 @@ def cpu_oracle_call(obs):
     t0 = time.perf_counter()
     res, _ = oracle.sketch_bki(A, oracle.SketchParams(k=K_RANK, p=P_POW, s=S_OVER, seed=SEED))
     return time.perf_counter() - t0, res
+
+
+SVT_CFG4_NOTE = ("cfg4 rating shape (138493x26744, 18,000,237 train): the reference defaults (tau=5n, "
+                 "delta=1.2mn/nnz) diverge on Zipf-sampled ratings -- ranks escalate past the 2000 dense cap and "
+                 "BOTH implementations raise SizeCapError -- so the throughput run uses tau=5n/40, delta=1, "
+                 "reuse-q (i_reuse=5, q_reuse=10), a fixed 20 iterations (rank grows 6 -> ~48)")
+
+
+def bench_svt(cpu: bool):
+    """SVT iterations/s: cfg1 (BASELINE configs[0], defaults and eps=1e-3) and
+    the cfg4 rating shape (fixed 20 iterations), GPU loop time from the trace
+    (setup excluded), CPU oracle beside it."""
+    import torch
+
+    import oracle
+    from paper_1810_06860_b200 import completion, workloads
+    from paper_1810_06860_b200.sparse import ObservationSet
+
+    out = {}
+    o1, _ = workloads.cfg1()
+    obs1 = ObservationSet(o1.m, o1.n, o1.rows, o1.cols, o1.values)
+    for name, eps in (("cfg1_default", 0.05), ("cfg1_eps1e-3", 1e-3)):
+        prm = completion.SvtParams(seed=0, epsilon=eps)
+        completion.svt_reference(obs1, prm, backend="rsvd-bki")  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = completion.svt_reference(obs1, prm, backend="rsvd-bki")
+        torch.cuda.synchronize()
+        total = time.perf_counter() - t0
+        loop = sum(t.wall_time for t in res.trace)
+        d = {"iterations": res.iterations, "iterations_per_s": res.iterations / loop, "loop_s": loop,
+             "total_s": total, "residual": res.residual, "rank": res.rank}
+        if cpu:
+            t0 = time.perf_counter()
+            ref = oracle.complete(o1.m, o1.n, o1.rows, o1.cols, o1.values, oracle.SvtConfig(seed=0, epsilon=eps))
+            dt = time.perf_counter() - t0
+            d["cpu"] = {"iterations": ref.iterations, "iterations_per_s": ref.iterations / dt, "total_s": dt,
+                        "residual": ref.residual, "cores": os.cpu_count(), "kind": "port"}
+            d["parity"] = {"same_iterations": ref.iterations == res.iterations,
+                           "residual_abs_diff": abs(ref.residual - res.residual)}
+        out[name] = d
+    o4 = workloads.cfg4()
+    obs4 = ObservationSet(o4.m, o4.n, o4.rows, o4.cols, o4.values, o4.split)
+    prm = completion.SvtParams(epsilon=0.17, i_reuse=5, q_reuse=10, strategy="reuse-q", seed=0, i_max=20,
+                               delta=1.0, tau=5.0 * o4.n / 40)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = completion.svt_fast(obs4, prm)
+    torch.cuda.synchronize()
+    total = time.perf_counter() - t0
+    loop = sum(t.wall_time for t in res.trace)
+    rt, ct, vt = obs4.subset(1)
+    d = {"iterations": res.iterations, "iterations_per_s": res.iterations / loop, "loop_s": loop, "total_s": total,
+         "residual": res.residual, "rank": res.rank, "ks": [t.k for t in res.trace],
+         "heldout_mae": completion.mae(res.predict(rt, ct), vt), "note": SVT_CFG4_NOTE}
+    if cpu:
+        r, c, v = obs4.subset(0)
+        n_cpu = 2
+        t0 = time.perf_counter()
+        ref = oracle.complete(o4.m, o4.n, r, c, v, oracle.SvtConfig(epsilon=0.17, i_reuse=5, q_reuse=10,
+                                                                    strategy="reuse-q", seed=0, i_max=n_cpu,
+                                                                    delta=1.0, tau=5.0 * o4.n / 40))
+        dt = time.perf_counter() - t0
+        d["cpu"] = {"iterations": n_cpu, "iterations_per_s": n_cpu / dt, "total_s_incl_setup": dt,
+                    "cores": os.cpu_count(), "kind": "port",
+                    "sample": f"first {n_cpu} iterations of the same run (incl. CSR/CSC build and spectral norm)"}
+        d["parity_first_iterations"] = [abs(a[5] - b.residual) for a, b in zip(ref.trace, res.trace)]
+    out["cfg4_tau_5n_over_40"] = d
+    return out
 
 
 def run_reference(args, ws, rank):
@@ -298,6 +368,8 @@ def main():
                                     else "fp64 cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json "
                                          "has no fp64 figure)")}
 
+    svt = bench_svt(cpu=args.cpu_baseline == "full" and ws == 1) if args.svt == "on" else None
+
     cpu = None
     if args.cpu_baseline == "full" and ws == 1:
         dt, ref = cpu_oracle_call(obs)
@@ -322,6 +394,7 @@ def main():
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),
         "clocks": clk.result(),
+        "svt": svt,
     }
     print(json.dumps(line), flush=True)
     if ws > 1:

@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(256) build_T_kernel(const double* __restrict__
 // All reflector blocks applied to a tile of kTC eigenvector columns by one
 // CTA (columns are independent: no inter-CTA dependency, one launch):
 // for b = last..0:  Y = V_b^T Z_tile, Y = T_b Y, Z_tile -= V_b Y.
-constexpr int kTC = 8;
+template <int kTC>
 __global__ void __launch_bounds__(256) wy_apply_kernel(double* __restrict__ Z, int n, const double* __restrict__ Vr,
                                                      const double* __restrict__ T, int nrefl, double* __restrict__ V,
                                                      long long ldv, int stage_v) {
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(256) wy_apply_kernel(double* __restrict__ Z, i
     zs[e] = (t < tc) ? Z[(long long)i * n + c0 + t] : 0.0;
   }
   const int nblk = (nrefl + kWY - 1) / kWY;
-  const int k = tid / kTC, t = tid % kTC;  // 32 x 8 threads
+  const int k = tid / kTC, t = tid % kTC;  // 32 x kTC threads (k >= 32 idle in the small phases)
   // staged: the block's reflector rows live in shared memory (ld n+1, odd)
   double* vb = stage_v ? zs + (size_t)n * kTC : nullptr;
   const int LDV = n + 1;
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(256) wy_apply_kernel(double* __restrict__ Z, i
     }
     __syncthreads();
     double acc = 0.0;
-    if (k < bsb) {
+    if (k < bsb && k < kWY) {
       if (vb) {
         const double* vrow = vb + k * LDV;
 #pragma unroll 4
@@ -501,11 +501,13 @@ __global__ void __launch_bounds__(256) wy_apply_kernel(double* __restrict__ Z, i
         for (int c = J + 1; c < n; ++c) acc = fma(vrow[c], zs[c * kTC + t], acc);
       }
     }
-    Y[k][t] = acc;
+    if (k < kWY) Y[k][t] = acc;
     __syncthreads();
-    double a2 = 0.0;
-    for (int q = 0; q < bsb; ++q) a2 = fma(Ts[k][q], Y[q][t], a2);
-    Y2[k][t] = a2;
+    if (k < kWY) {
+      double a2 = 0.0;
+      for (int q = 0; q < bsb; ++q) a2 = fma(Ts[k][q], Y[q][t], a2);
+      Y2[k][t] = a2;
+    }
     __syncthreads();
     for (int c = J + 1 + tid / kTC; c < n; c += 256 / kTC) {
       double s = zs[c * kTC + t];
@@ -596,7 +598,8 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
   if (!attr) {
     LR_CHECK_CUDA(cudaFuncSetAttribute(tridiag_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     LR_CHECK_CUDA(cudaFuncSetAttribute(tridiag_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    LR_CHECK_CUDA(cudaFuncSetAttribute(wy_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    LR_CHECK_CUDA(cudaFuncSetAttribute(wy_apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    LR_CHECK_CUDA(cudaFuncSetAttribute(wy_apply_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
     attr = true;
   }
   int occ = 0;
@@ -697,11 +700,16 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
     LR_CHECK_LAUNCH();
     (void)Yb;
     (void)Y2;
-    const size_t zsm = (size_t)n * kTC * sizeof(double);
     const size_t vsm = (size_t)kWY * (n + 1) * sizeof(double);
-    const int stage = zsm + vsm <= 210 * 1024;
-    LR_REQUIRE(zsm <= 200 * 1024, "syevd: n = %d too large for the back-transform tile", n);
-    wy_apply_kernel<<<(n + kTC - 1) / kTC, 256, stage ? zsm + vsm : zsm, s>>>(Z, n, Vr, Tb, nrefl, V, ldv, stage);
+    if ((size_t)n * 8 * sizeof(double) <= 200 * 1024) {
+      const size_t zsm = (size_t)n * 8 * sizeof(double);
+      const int stage = zsm + vsm <= 210 * 1024;
+      wy_apply_kernel<8><<<(n + 7) / 8, 256, stage ? zsm + vsm : zsm, s>>>(Z, n, Vr, Tb, nrefl, V, ldv, stage);
+    } else {
+      const size_t zsm = (size_t)n * 2 * sizeof(double);
+      LR_REQUIRE(zsm <= 200 * 1024, "syevd: n = %d too large for the back-transform tile", n);
+      wy_apply_kernel<2><<<(n + 1) / 2, 256, zsm, s>>>(Z, n, Vr, Tb, nrefl, V, ldv, 0);
+    }
     LR_CHECK_LAUNCH();
   } else {
     int st = lr_copy2d_f64(Z, n, V, ldv, n, n, 0, stream);
