@@ -23,6 +23,7 @@ device time is the max over ranks.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import sys
@@ -292,6 +293,8 @@ def main():
     barrier()
     torch.cuda.synchronize()
     use_prof = os.environ.get("BENCH_NO_PROFILE") is None
+    gc.collect()
+    gc.disable()  # no collector pauses inside the timed region (host-side harness hygiene)
     with ClockSampler(local if os.environ.get("BENCH_NO_CLOCKS") is None else -1) as clk:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         _native.PROFILER = prof if use_prof else None
@@ -302,6 +305,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         _native.PROFILER = None
+    gc.enable()
     barrier()
     launches = lib.lr_launch_count() - launches0
     ms = e0.elapsed_time(e1)
