@@ -205,21 +205,30 @@ def orth_dev(X):
     m, n = X.shape
     if m < n:
         raise ValueError(f"orth requires m >= n, got {m}x{n}")
-    G0 = gram_dev(X)
-    tr = float(np.sum(_diag_host(G0, n)))
+    return orth_core(X, m, gram_dev, _cholqr_pass, lambda: _fro_from_stats(_check_dev(X, "orth input"), X),
+                     lambda G: _diag_host(G, n))
+
+
+def orth_core(X, m, gram, cholqr, checked_norm, diag):
+    """CholeskyQR2 / shifted CholeskyQR3 with the reference's collapse test,
+    over callables so a row-sharded X (shards.py: gram = local Gram +
+    allreduce, m = global rows) runs the same decisions on every rank."""
+    n = X.shape[1]
+    G0 = gram(X)
+    tr = float(np.sum(diag(G0)))
     if np.isfinite(tr) and tr < 1e300:
         scale = float(np.sqrt(tr))
     else:
-        scale = _fro_from_stats(_check_dev(X, "orth input"), X)
+        scale = checked_norm()
     if scale == 0.0:
         raise RankDeficiencyError("cannot orthonormalize a zero matrix")
-    info, Q1, d1 = _cholqr_pass(X, G=G0)
+    info, Q1, d1 = cholqr(X, G=G0)
     if info == 0:
-        info2, Q, d2 = _cholqr_pass(Q1)
+        info2, Q, d2 = cholqr(Q1)
         if info2 == 0:
             rdiag = d2 * d1
             if np.max(np.abs(d2 - 1.0)) > 1e-6:  # Q1 was far from orthonormal: one more pass
-                info3, Q3, d3 = _cholqr_pass(Q)
+                info3, Q3, d3 = cholqr(Q)
                 if info3 == 0:
                     Q, rdiag = Q3, d3 * rdiag
     else:
@@ -227,13 +236,13 @@ def orth_dev(X):
     if info != 0 or info2 != 0:
         # shifted CholeskyQR3 (Fukaya et al.): well defined for any full-rank X
         shift = 11.0 * (m * n + n * (n + 1)) * _U_ROUND * scale * scale
-        info, Q1, d1 = _cholqr_pass(X, shift)
+        info, Q1, d1 = cholqr(X, shift)
         if info:
             raise RankDeficiencyError(f"shifted Cholesky failed at column {info - 1}; cannot orthonormalize")
         rdiag = d1
         Q = Q1
         for _ in range(2):
-            info, Qn, dn = _cholqr_pass(Q)
+            info, Qn, dn = cholqr(Q)
             if info:
                 raise RankDeficiencyError(
                     f"column norm collapse at column {info - 1} (|R[{info - 1},{info - 1}]| = 0.000e+00 < "
@@ -339,6 +348,21 @@ def sym_eig(B):
 
 # ------------------------------------------------------------------ eig_svd
 
+def gram_spectrum(dh):
+    """Singular values sqrt(max(d, 0)) of ascending Gram eigenvalues d, after
+    the reference's rank checks (linalg.py:190-198)."""
+    n = dh.shape[0]
+    dmax = dh[-1]
+    if dmax <= 0.0:
+        raise RankDeficiencyError("Gram matrix has no positive eigenvalue (zero input?)")
+    bad = np.flatnonzero(dh <= GRAM_RANK_TOL * dmax)
+    if bad.size:
+        raise RankDeficiencyError(
+            f"Gram eigenvalue {bad.size} of {n} at/below rank tolerance "
+            f"(index {bad[0]}: {dh[bad[0]]:.3e} <= {GRAM_RANK_TOL:.0e} * {dmax:.3e})")
+    return np.sqrt(np.maximum(dh, 0.0))
+
+
 def eig_svd_dev(A, cols=None, check=True):
     """Gram-route SVD of tall A (linalg.py:172-202), device in/out.
 
@@ -355,16 +379,7 @@ def eig_svd_dev(A, cols=None, check=True):
     if check and not np.isfinite(np.sum(_diag_host(G, n))):
         _check_dev(A, "eig_svd input")  # raises ValueError on non-finite input
     V, d = sym_eig_dev(G, symmetrize=False)
-    dh = device.to_host(d)
-    dmax = dh[-1]
-    if dmax <= 0.0:
-        raise RankDeficiencyError("Gram matrix has no positive eigenvalue (zero input?)")
-    bad = np.flatnonzero(dh <= GRAM_RANK_TOL * dmax)
-    if bad.size:
-        raise RankDeficiencyError(
-            f"Gram eigenvalue {bad.size} of {n} at/below rank tolerance "
-            f"(index {bad[0]}: {dh[bad[0]]:.3e} <= {GRAM_RANK_TOL:.0e} * {dmax:.3e})")
-    S = np.sqrt(np.maximum(dh, 0.0))
+    S = gram_spectrum(device.to_host(d))
     _native.call("lr_fix_signs_f64", device.ptr(V), device.ld(V), n, n, None, 0, 0, _st())
     if cols is None:
         cols = np.arange(n)

@@ -1,0 +1,648 @@
+"""Sharded SVT / rSVD-BKI: one matrix spread over ranks.
+
+One process per GPU.  The observed pattern is cut twice, by nnz-balanced
+prefix sums (ShardPlan):
+  row shard  R_g  CSR block Y[R_g, :]   -> products Y X      (rows R_g)
+  col shard  C_g  CSR block Y[:, C_g]   -> products Y^T X    (rows C_g, via
+                                            the block's CSC copy)
+Every m x . dense block is either replicated (Krylov blocks H_i, the basis
+Q) or row-sharded by R_g (U factors); every n x . block is replicated
+(T, Omega) or row-sharded by C_g (V factors).  Per fresh BKI call:
+
+  Omega (n x w)            generated on every rank from the same Philox seed
+  H_0 = Y Omega            local rows -> allgather -> GEPP replicated
+  T = Y^T H_{i-1}          local rows -> allgather; H_i = Y T -> allgather -> GEPP
+  Q = orth(H)              CholeskyQR2 on row shards: local Gram -> allreduce
+                           -> replicated Cholesky -> local Q rows -> allgather
+  B^T = Y^T Q              local rows (C_g); eig_svd: local Gram -> allreduce
+                           -> replicated eigensolver -> V rows C_g, U = Q V rows R_g
+  SVT step                 CSR side needs full V (allgather n x r), CSC side full
+                           U (allgather m x r); both sides compute each entry
+                           with the same kernel from the same U row / V row, so
+                           the two value copies of Y stay bit-identical; the
+                           residual partials are allgathered and summed in rank
+                           order on every rank.
+
+Allreduce results are identical on every rank, so every replicated solve and
+every host decision (ranks, escalation, fallbacks, convergence) agrees across
+ranks without further communication.  The single-GPU engine
+(completion.DeviceEngine) is the world-size-1 special case of the same loop;
+results at N ranks equal it within fp64 rounding (Gram sums are split
+differently), never bit-for-bit.
+
+The collectives go through torch.distributed (`Exchange`): NCCL between GPUs,
+gloo for the host-side tests (tests/test_shards_gloo.py runs world size 2 on
+the CPU with a numpy kernel set injected through `kernels=`).  The product
+kernel set is DeviceKernels -- the sm_100a library; nothing here computes on
+the host.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native, device
+from .errors import DataError, RankDeficiencyError
+from .linalg import DevSvd, SvdResult, gram_spectrum, orth_core
+from .rsvd import RsvdParams, Subspace, _Fallback
+from .sparse import ObservationSet, SparseMatrix
+
+__all__ = ["ShardPlan", "Exchange", "DeviceKernels", "ShardedEngine", "svt_sharded", "rsvd_bki_sharded"]
+
+
+# ------------------------------------------------------------------ plan
+
+def balanced_bounds(ptr, parts: int) -> np.ndarray:
+    """Contiguous cut of len(ptr)-1 rows into `parts` blocks with about
+    nnz/parts entries each (prefix-sum search); every block gets >= 1 row."""
+    ptr = np.asarray(ptr, dtype=np.int64)
+    size = ptr.shape[0] - 1
+    if parts < 1:
+        raise ValueError(f"parts must be >= 1, got {parts}")
+    if size < parts:
+        raise ValueError(f"cannot cut {size} rows into {parts} non-empty shards")
+    nnz = int(ptr[-1])
+    b = np.empty(parts + 1, dtype=np.int64)
+    b[0], b[parts] = 0, size
+    for g in range(1, parts):
+        target = (g * nnz) // parts
+        i = int(np.searchsorted(ptr, target, side="left"))
+        b[g] = min(max(i, b[g - 1] + 1), size - (parts - g))
+    return b
+
+
+class ShardPlan:
+    """Row bounds (CSR indptr) and column bounds (CSC indptr) of a pattern."""
+
+    def __init__(self, indptr, t_indptr, world: int):
+        self.world = int(world)
+        self.row_bounds = balanced_bounds(indptr, world)
+        self.col_bounds = balanced_bounds(t_indptr, world)
+        ip, tp = np.asarray(indptr), np.asarray(t_indptr)
+        self.row_nnz = ip[self.row_bounds[1:]] - ip[self.row_bounds[:-1]]
+        self.col_nnz = tp[self.col_bounds[1:]] - tp[self.col_bounds[:-1]]
+
+    def rows(self, g: int):
+        return int(self.row_bounds[g]), int(self.row_bounds[g + 1])
+
+    def cols(self, g: int):
+        return int(self.col_bounds[g]), int(self.col_bounds[g + 1])
+
+    def describe(self) -> dict:
+        return {"row_bounds": self.row_bounds.tolist(), "col_bounds": self.col_bounds.tolist(),
+                "row_nnz": self.row_nnz.tolist(), "col_nnz": self.col_nnz.tolist()}
+
+
+# ------------------------------------------------------------ collectives
+
+class Exchange:
+    """The sharded path's collectives over torch.distributed: uneven row
+    allgather, in-place sum allreduce, small scalar allgather.  Counts bytes
+    moved for the bench line."""
+
+    def __init__(self, group=None, always_collective=False):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        if dist.is_available() and dist.is_initialized():
+            self.rank = dist.get_rank(group)
+            self.world = dist.get_world_size(group)
+            self.backend = str(dist.get_backend(group))
+        else:
+            self.rank, self.world, self.backend = 0, 1, "none"
+        # world size 1 short-circuits to local copies unless asked to run the
+        # collectives anyway (the one-GPU NCCL test exercises them that way)
+        self.collective = self.world > 1 or (always_collective and self.backend != "none")
+        self.bytes = 0
+        self.calls = 0
+
+    def gather_rows(self, local, bounds, out):
+        """out[bounds[g]:bounds[g+1]] = rank g's `local`, on every rank."""
+        import torch
+
+        w = int(local.shape[1])
+        if not self.collective:
+            if out.data_ptr() != local.data_ptr() or out.stride() != local.stride():
+                out.copy_(local)
+            return out
+        if w == 0:
+            return out
+        counts = np.diff(bounds)
+        cmax = int(counts.max())
+        send = torch.empty((cmax, w), dtype=local.dtype, device=local.device)
+        send[: local.shape[0]].copy_(local)
+        if local.shape[0] < cmax:
+            send[local.shape[0]:].zero_()
+        recv = torch.empty((self.world * cmax, w), dtype=local.dtype, device=local.device)
+        if self.backend == "nccl":
+            self.dist.all_gather_into_tensor(recv, send, group=self.group)
+        else:
+            self.dist.all_gather(list(recv.chunk(self.world)), send, group=self.group)
+        for g in range(self.world):
+            c = int(counts[g])
+            out[int(bounds[g]):int(bounds[g]) + c].copy_(recv[g * cmax:g * cmax + c])
+        self.bytes += int(recv.numel()) * 8
+        self.calls += 1
+        return out
+
+    def allreduce_sum(self, t):
+        if not self.collective:
+            return t
+        flat = t if t.is_contiguous() else t.contiguous()
+        self.dist.all_reduce(flat, group=self.group)
+        if flat is not t:
+            t.copy_(flat)
+        self.bytes += int(flat.numel()) * 8
+        self.calls += 1
+        return t
+
+    def gather_scalars(self, vec) -> np.ndarray:
+        """(world, k) host array of every rank's k-vector (a tensor on the
+        engine's device), identical on all ranks."""
+        import torch
+
+        if not self.collective:
+            return vec.detach().cpu().numpy().reshape(1, -1).astype(np.float64)
+        k = int(vec.numel())
+        send = vec.reshape(-1).contiguous()
+        recv = torch.empty((self.world * k,), dtype=send.dtype, device=send.device)
+        if self.backend == "nccl":
+            self.dist.all_gather_into_tensor(recv, send, group=self.group)
+        else:
+            self.dist.all_gather(list(recv.chunk(self.world)), send, group=self.group)
+        self.calls += 1
+        return recv.cpu().numpy().reshape(self.world, k).astype(np.float64)
+
+
+# ------------------------------------------------------------ kernel set
+
+class DeviceKernels:
+    """Per-rank operations of the sharded engine on the sm_100a library
+    (the same entry points the single-GPU path calls)."""
+
+    def __init__(self):
+        _native.load()
+
+    # memory
+    def empty(self, rows, cols):
+        return device.empty(rows, cols)
+
+    def vector(self, values):
+        return device.f64_buffer(np.asarray(values, dtype=np.float64))
+
+    def from_host(self, a):
+        return device.to_device(np.ascontiguousarray(a, dtype=np.float64))
+
+    def to_host(self, t):
+        return device.to_host(t)
+
+    def copy(self, src, dst):
+        if src.shape[0] * src.shape[1]:
+            _native.call("lr_copy2d_f64", device.ptr(src), device.ld(src), device.ptr(dst), device.ld(dst),
+                         src.shape[0], src.shape[1], 0, device.stream())
+
+    # sparse blocks
+    def block(self, rows, cols, indptr, indices, data):
+        A = SparseMatrix(rows, cols, indptr, indices, data)
+        A.device_values()
+        return A
+
+    def block_like(self, A, data):
+        B = SparseMatrix(A.rows, A.cols, A.indptr, A.indices, data)
+        B.share_pattern(A)
+        B.device_values()
+        return B
+
+    def host_values(self, A):
+        return A.data
+
+    def values(self, A):
+        return A.device_values()[0]
+
+    def densify(self, A):
+        return A.densify()
+
+    def spmm(self, A, X, out):
+        from .sparse import spmm_dev
+
+        return spmm_dev(A, X, out=out)
+
+    def spmm_t(self, A, X, out):
+        from .sparse import spmm_t_dev
+
+        return spmm_t_dev(A, X, out=out)
+
+    def svt_step(self, A, m_vals, U, S_dev, V, r, step):
+        """Fused residual + update of A's two value copies; device [sumsq, max|x-m|]."""
+        dp = A.pattern()
+        npart = int(_native.load().lr_svt_step_partials())
+        part = device.arena().get("svt_partial", npart + 8)
+        out2 = device.vector(2)
+        yc, yt = A.device_values()
+        _native.call("lr_svt_step_f64", device.ptr(dp.csr.ptr), device.ptr(dp.csr.idx), dp.csr.rows,
+                     device.ptr(dp.csr.items), dp.csr.n_items, device.ptr(U), device.ld(U) if r else 1,
+                     device.ptr(S_dev), device.ptr(V), device.ld(V) if r else 1, r, device.ptr(m_vals),
+                     device.ptr(yc), device.ptr(yt), device.ptr(dp.inv_perm), float(step), 1,
+                     device.ptr(part), npart, device.ptr(out2), device.stream(),
+                     meta={"nnz": A.nnz, "m": A.rows, "n": A.cols, "r": r})
+        A._host_stale = True
+        return out2
+
+    def project(self, A, U, S_dev, V, r):
+        from .sparse import project_pattern_dev
+
+        return project_pattern_dev(U, S_dev, V, A) if r else device.vector(A.nnz).zero_()
+
+    def stats(self, x):
+        """Device [sum of squares, max|x|, #non-finite] of a vector / block."""
+        if x.dim() == 1:
+            rows, cols, ldx = x.shape[0], 1, 1
+        else:
+            rows, cols, ldx = x.shape[0], x.shape[1], device.ld(x)
+        out = device.vector(3)
+        if rows * cols == 0:
+            return out.zero_()
+        part = device.arena().get("stats_partial", _native.load().lr_stats_partials() + 8)
+        _native.call("lr_block_stats_f64", device.ptr(x), rows, cols, ldx, device.ptr(part), device.ptr(out),
+                     device.stream())
+        return out
+
+    def scaled_stats(self, x, big):
+        xs = x.reshape(-1, 1) if x.dim() == 1 else x
+        rows, cols = xs.shape
+        y = device.empty(rows, cols)
+        scale = device.f64_buffer(np.full(max(cols, 1), big))
+        _native.call("lr_scale_columns_f64", device.ptr(xs), device.ld(xs) if x.dim() == 2 else 1, rows, None,
+                     cols, device.ptr(scale), 1, device.ptr(y), device.ld(y), device.stream())
+        return self.stats(y)
+
+    def power(self, x0_host):
+        from .sparse import PowerIteration
+
+        return PowerIteration(x0_host)
+
+    # dense
+    def gram(self, X):
+        from .linalg import gram_dev
+
+        return gram_dev(X)
+
+    def matmul(self, A, B, b_upper=False):
+        from .linalg import matmul_dev
+
+        return matmul_dev(A, B, b_upper=b_upper)
+
+    def potrf_inv(self, G, shift=0.0):
+        from .linalg import potrf_inv_dev
+
+        return potrf_inv_dev(G, shift)
+
+    def diag(self, G):
+        from .linalg import _diag_host
+
+        return _diag_host(G, G.shape[0])
+
+    def sym_eig(self, G):
+        from .linalg import sym_eig_dev
+
+        V, d = sym_eig_dev(G, symmetrize=False)
+        return V, device.to_host(d)
+
+    def fix_signs(self, V):
+        n = V.shape[0]
+        _native.call("lr_fix_signs_f64", device.ptr(V), device.ld(V), n, V.shape[1], None, 0, 0, device.stream())
+
+    def select_columns(self, V, cols, S=None):
+        """V[:, cols] (divided column-wise by S[cols] when S is given)."""
+        cols = np.asarray(cols, dtype=np.int64)
+        B = device.empty(V.shape[0], cols.shape[0])
+        ci = device.int_buffer(cols)
+        Sd = device.f64_buffer(S) if S is not None else None
+        _native.call("lr_scale_columns_f64", device.ptr(V), device.ld(V), V.shape[0], device.ptr(ci),
+                     cols.shape[0], device.ptr(Sd), 1 if S is not None else 0, device.ptr(B), device.ld(B),
+                     device.stream())
+        return B
+
+    def lu_pl(self, X):
+        from .linalg import lu_pl_dev
+
+        return lu_pl_dev(X)
+
+    def gaussian(self, seed, rows, cols):
+        from .rng import gaussian_matrix_device
+
+        return gaussian_matrix_device(seed, rows, cols)
+
+    def dense_svd(self, X):
+        from .linalg import oracle_svd_dev
+
+        return oracle_svd_dev(X)
+
+
+# ---------------------------------------------------------------- engine
+
+class ShardedEngine:
+    """completion._svt_loop's matrix side spread over ranks; also the
+    sharded rSVD-BKI (`bki`).  Factors U are row-sharded by R_g, V by C_g."""
+
+    def __init__(self, obs: ObservationSet, exchange: Exchange = None, kernels=None):
+        self.ex = exchange if exchange is not None else Exchange()
+        self.K = kernels if kernels is not None else DeviceKernels()
+        self.rank, self.world = self.ex.rank, self.ex.world
+        r, c, v = obs.subset(ObservationSet.TRAIN)
+        phi = SparseMatrix.from_coo(obs.m, obs.n, r, c, v)  # host: same ordering / validation everywhere
+        if phi.nnz == 0:
+            raise DataError("no observed entries to complete from")
+        self._setup(phi)
+
+    @classmethod
+    def from_matrix(cls, A: SparseMatrix, exchange: Exchange = None, kernels=None) -> "ShardedEngine":
+        self = cls.__new__(cls)
+        self.ex = exchange if exchange is not None else Exchange()
+        self.K = kernels if kernels is not None else DeviceKernels()
+        self.rank, self.world = self.ex.rank, self.ex.world
+        self._setup(A)
+        return self
+
+    def _setup(self, phi: SparseMatrix) -> None:
+        K = self.K
+        self.m, self.n = phi.shape
+        self.nnz = phi.nnz
+        _, t_indptr, _ = phi._transpose_index()
+        self.plan = ShardPlan(phi.indptr, t_indptr, self.world)
+        self.r0, self.r1 = self.plan.rows(self.rank)
+        self.c0, self.c1 = self.plan.cols(self.rank)
+        ip, ix, dv = phi.indptr, phi.indices, phi.data
+        lo, hi = int(ip[self.r0]), int(ip[self.r1])
+        self.phi_r = K.block(self.r1 - self.r0, self.n, ip[self.r0:self.r1 + 1] - lo, ix[lo:hi], dv[lo:hi])
+        sel = (ix >= self.c0) & (ix < self.c1)
+        rows_of = phi.coo_rows()[sel]
+        cptr = np.zeros(self.m + 1, dtype=np.int64)
+        np.cumsum(np.bincount(rows_of, minlength=self.m), out=cptr[1:])
+        self.phi_c = K.block(self.m, self.c1 - self.c0, cptr, ix[sel] - self.c0, dv[sel])
+        self.m_r = K.values(self.phi_r)
+        self.m_c = K.values(self.phi_c)
+        self.Y_r, self.Y_c = self.phi_r, self.phi_c  # rsvd on the observed matrix itself until start()
+        self.m_norm = None
+
+    # ------------------------------------------------------------ helpers
+    def vector(self, values):
+        return self.K.vector(values)
+
+    def gather_m(self, local, out=None):
+        if out is None:
+            out = self.K.empty(self.m, local.shape[1])
+        return self.ex.gather_rows(local, self.plan.row_bounds, out)
+
+    def gather_n(self, local, out=None):
+        if out is None:
+            out = self.K.empty(self.n, local.shape[1])
+        return self.ex.gather_rows(local, self.plan.col_bounds, out)
+
+    def _reduced_gram(self, X):
+        G = self.K.gram(X)
+        return self.ex.allreduce_sum(G)
+
+    def _global_stats(self, x) -> np.ndarray:
+        return self.ex.gather_scalars(self.K.stats(x))  # (world, 3)
+
+    def _global_norm(self, x) -> float:
+        st = self._global_stats(x)
+        sumsq, big = float(np.sum(st[:, 0])), float(np.max(st[:, 1]))
+        if big == 0.0:
+            return 0.0
+        if np.isfinite(sumsq) and 1e-150 < big < 1e150:
+            return float(np.sqrt(sumsq))
+        st2 = self.ex.gather_scalars(self.K.scaled_stats(x, big))
+        return float(big * np.sqrt(np.sum(st2[:, 0])))
+
+    def _check_finite(self, X, name):
+        if np.sum(self._global_stats(X)[:, 2]):
+            raise ValueError(f"{name} contains non-finite entries")
+
+    # --------------------------------------------------- loop interface
+    def observed_norm(self) -> float:
+        return self._global_norm(self.m_r)
+
+    def spectral_norm(self, rng) -> float:
+        from .sparse import _SPECTRAL_BATCH, _SPECTRAL_MAX_ITERS
+
+        K = self.K
+        pw = K.power(rng.normal_pairs(self.n))
+        # unit-stride columns: the power-update kernel reads z as a flat vector
+        y_loc = K.vector(np.zeros(self.r1 - self.r0)).view(-1, 1)
+        y = K.vector(np.zeros(self.m)).view(-1, 1)
+        z_loc = K.vector(np.zeros(self.c1 - self.c0)).view(-1, 1)
+        z = K.vector(np.zeros(self.n)).view(-1, 1)
+        for it in range(_SPECTRAL_MAX_ITERS):
+            if it and it % _SPECTRAL_BATCH == 0 and pw.done():
+                break
+            K.spmm(self.phi_r, pw.x, out=y_loc)
+            self.gather_m(y_loc, out=y)
+            K.spmm_t(self.phi_c, y, out=z_loc)
+            self.gather_n(z_loc, out=z)
+            pw.update(z)
+        return pw.result()
+
+    def start(self, scale: float) -> None:
+        K = self.K
+        self.Y_r = K.block_like(self.phi_r, scale * K.host_values(self.phi_r))
+        self.Y_c = K.block_like(self.phi_c, scale * K.host_values(self.phi_c))
+
+    def step(self, U_s, S_s, V_s, r: int, step: float):
+        K = self.K
+        S_dev = K.vector(S_s) if r else K.vector(np.zeros(0))
+        if r:
+            V_full = self.gather_n(V_s)
+            U_full = self.gather_m(U_s)
+        else:
+            V_full, U_full = V_s, U_s
+        part = K.svt_step(self.Y_r, self.m_r, U_s, S_dev, V_full, r, step)
+        K.svt_step(self.Y_c, self.m_c, U_full, S_dev, V_s, r, step)
+        st = self.ex.gather_scalars(part)
+        sumsq, big = float(np.sum(st[:, 0])), float(np.max(st[:, 1]))
+        if big == 0.0:
+            return 0.0, None
+        if np.isfinite(sumsq) and 1e-150 < big < 1e150:
+            return float(np.sqrt(sumsq)) / self.m_norm, None
+        x = K.project(self.Y_r, U_s, S_dev, V_full, r)
+        return self._global_norm(x - self.m_r) / self.m_norm, None
+
+    def factors_host(self, U_s, V_s, r: int):
+        if not r:
+            return np.zeros((self.m, 0)), np.zeros((self.n, 0))
+        return self.K.to_host(self.gather_m(U_s)), self.K.to_host(self.gather_n(V_s))
+
+    # ------------------------------------------------------ inner SVDs
+    def _empty(self, k=0):
+        K = self.K
+        return DevSvd(K.empty(self.r1 - self.r0, k), K.vector(np.zeros(k)), K.empty(self.c1 - self.c0, k),
+                      np.zeros(k))
+
+    def _lu_block(self, block, fb: _Fallback):
+        K = self.K
+        keep = None
+        if fb.enabled:
+            keep = K.empty(*block.shape)
+            K.copy(block, keep)
+        try:
+            K.lu_pl(block)
+        except RankDeficiencyError as exc:
+            fb.fail(exc)
+            U, _, _ = K.dense_svd(keep)
+            K.copy(U, block)
+
+    def _cholqr(self, X, shift=0.0, G=None):
+        K = self.K
+        if G is None:
+            G = self._reduced_gram(X)
+        info, Rinv = K.potrf_inv(G, shift)
+        if info:
+            return info, None, None
+        return 0, K.matmul(X, Rinv, b_upper=True), K.diag(G)
+
+    def _orth_rows(self, X_loc):
+        """orth of the row-sharded block whose local rows are X_loc."""
+        return orth_core(X_loc, self.m, self._reduced_gram, self._cholqr,
+                         lambda: (self._check_finite(X_loc, "orth input"), self._global_norm(X_loc))[1],
+                         self.K.diag)
+
+    def _eig_svd(self, A_loc, cols):
+        """eig_svd of the row-sharded n x W block whose local rows are A_loc
+        (rows C_g): returns (S ascending, V replicated, U_loc, cols)."""
+        K = self.K
+        G = self._reduced_gram(A_loc)
+        if not np.isfinite(np.sum(K.diag(G))):
+            self._check_finite(A_loc, "eig_svd input")
+        V, d = K.sym_eig(G)
+        S = gram_spectrum(d)
+        K.fix_signs(V)
+        cols = np.asarray(cols, dtype=np.int64)
+        B = K.select_columns(V, cols, S)
+        return S, V, K.matmul(A_loc, B), cols
+
+    def _windowed(self, Bt_loc, idx, fb: _Fallback):
+        K = self.K
+        try:
+            S, V, U_loc, cols = self._eig_svd(Bt_loc, idx)
+            return S[cols], K.select_columns(V, cols), U_loc
+        except RankDeficiencyError as exc:
+            fb.fail(exc)
+            Bt = self.gather_n(Bt_loc)
+            Ud, Sd, Vd = K.dense_svd(Bt)  # descending
+            W = Bt.shape[1]
+            desc = W - 1 - np.asarray(idx)
+            return Sd[desc], K.select_columns(Vd, desc), K.select_columns(Ud, desc)[self.c0:self.c1]
+
+    def _project_and_solve(self, Q, k: int, fb: _Fallback) -> DevSvd:
+        K = self.K
+        W = int(Q.shape[1])
+        Bt_loc = K.spmm_t(self.Y_c, Q, out=K.empty(self.c1 - self.c0, W))
+        idx = np.arange(W - 1, W - k - 1, -1)
+        S_sel, Vsel, Usel = self._windowed(Bt_loc, idx, fb)
+        U_loc = K.matmul(Q[self.r0:self.r1], Vsel)
+        S_sel = np.asarray(S_sel, dtype=np.float64)
+        return DevSvd(U_loc, K.vector(S_sel), Usel, S_sel)
+
+    def bki(self, rp: RsvdParams, allow_fallback: bool = True):
+        """Sharded Alg. 5 -> (DevSvd with local factor rows, Q replicated, fallbacks)."""
+        K = self.K
+        rp.check_against(self, krylov=True)
+        fb = _Fallback(allow_fallback, "Krylov blocks are near-collinear, reduce p or use a larger matrix")
+        w = rp.k + rp.s
+        W = w * (rp.p + 1)
+        mg, ng = self.r1 - self.r0, self.c1 - self.c0
+        Om = K.gaussian(rp.seed, self.n, w)
+        H = K.empty(self.m, W)
+        H_loc = K.empty(mg, w)
+        K.spmm(self.Y_r, Om, out=H_loc)
+        self.gather_m(H_loc, out=H[:, 0:w])
+        self._lu_block(H[:, 0:w], fb)
+        T_loc = K.empty(ng, w)
+        T = K.empty(self.n, w)
+        for i in range(1, rp.p + 1):
+            K.spmm_t(self.Y_c, H[:, (i - 1) * w:i * w], out=T_loc)
+            self.gather_n(T_loc, out=T)
+            K.spmm(self.Y_r, T, out=H_loc)
+            self.gather_m(H_loc, out=H[:, i * w:(i + 1) * w])
+            self._lu_block(H[:, i * w:(i + 1) * w], fb)
+        try:
+            Q_loc = self._orth_rows(H[self.r0:self.r1])
+            Q = self.gather_m(Q_loc, out=K.empty(self.m, W))
+        except RankDeficiencyError as exc:
+            fb.fail(exc)
+            Q = K.dense_svd(H)[0]
+        res = self._project_and_solve(Q, rp.k, fb)
+        return res, Q, fb.count
+
+    def recycle_q(self, cached: Subspace, k: int) -> DevSvd:
+        width = cached.width
+        if k > width:
+            raise ValueError(f"requested rank {k} exceeds cached subspace width {width}")
+        if k == 0:
+            return self._empty()
+        return self._project_and_solve(cached.Q_dev, k, _Fallback(False, None))
+
+    def recycle_u(self, U_prev_loc) -> DevSvd:
+        K = self.K
+        k = int(U_prev_loc.shape[1])
+        if k == 0:
+            return self._empty()
+        U_full = self.gather_m(U_prev_loc)
+        try:
+            Bt_loc = K.spmm_t(self.Y_c, U_full, out=K.empty(self.c1 - self.c0, k))
+            desc = np.arange(k - 1, -1, -1)
+            S, V, Usm, cols = self._eig_svd(Bt_loc, desc)
+        except RankDeficiencyError as exc:
+            raise RankDeficiencyError(f"projection onto cached U lost rank ({exc}); refresh the subspace") from exc
+        U = K.matmul(U_prev_loc, K.select_columns(V, cols))
+        Sd = np.asarray(S[cols], dtype=np.float64)
+        return DevSvd(U, K.vector(Sd), Usm, Sd)
+
+    def dense_full(self):
+        """Descending dense SVD of the current Y (replicated), local rows."""
+        K = self.K
+        D_loc = K.from_host(K.densify(self.Y_r))
+        D = self.gather_m(D_loc)
+        U, S, V = K.dense_svd(D)
+        return U[self.r0:self.r1], S, V[self.c0:self.c1]
+
+    def dense_truncated(self, k: int) -> DevSvd:
+        U, S, V = self.dense_full()
+        return DevSvd(U[:, :k], self.K.vector(S[:k]), V[:, :k], S[:k].copy())
+
+    # width guard of RsvdParams.check_against reads .rows / .cols
+    @property
+    def rows(self):
+        return self.m
+
+    @property
+    def cols(self):
+        return self.n
+
+
+# ------------------------------------------------------------ public API
+
+def svt_sharded(obs: ObservationSet, params, backend: str = "rsvd-bki", strategy: str = None,
+                exchange: Exchange = None, kernels=None):
+    """SVT over all ranks of the default process group (every rank calls it
+    with the same obs / params); the result (factors gathered) is returned on
+    every rank.  strategy defaults to params.strategy (svt_fast semantics)."""
+    from .completion import _svt_loop
+
+    eng = ShardedEngine(obs, exchange, kernels)
+    res = _svt_loop(obs, params, backend, params.strategy if strategy is None else strategy, engine=eng)
+    res.plan = eng.plan.describe()
+    return res
+
+
+def rsvd_bki_sharded(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False,
+                     exchange: Exchange = None, kernels=None, engine: ShardedEngine = None):
+    """rsvd_bki over ranks: (SvdResult gathered on every rank, Subspace)."""
+    eng = engine if engine is not None else ShardedEngine.from_matrix(A, exchange, kernels)
+    res, Q, nfb = eng.bki(params, allow_fallback)
+    k = params.k
+    U = eng.K.to_host(eng.gather_m(res.U)) if k else np.zeros((eng.m, 0))
+    V = eng.K.to_host(eng.gather_n(res.V)) if k else np.zeros((eng.n, 0))
+    return SvdResult(U, res.S_host.copy(), V, "descending"), Subspace(Q, "bki", params.p, nfb)

@@ -438,36 +438,57 @@ def frobenius(values) -> float:
     return frobenius_dev(device.f64_buffer(v))
 
 
+class PowerIteration:
+    """Device state of the power iteration on A^T A (sparse.py:231-256):
+    x = x0 / ||x0||; each `update(z)` with z = A^T A x records the estimate
+    sqrt(x.z), the 1e-3 relative-agreement latch and x <- z / ||z||, all on
+    the device, so the host polls `done()` only every few steps."""
+
+    def __init__(self, x0_host: np.ndarray):
+        n = int(np.asarray(x0_host).size)
+        self.n = n
+        # unit-stride (n, 1) views: the dot / power kernels treat them as flat vectors
+        x = device.f64_buffer(np.asarray(x0_host, dtype=np.float64).ravel()).view(n, 1)
+        self.part = device.arena().get("power_partial", 2 * 4096)
+        nrm2 = device.vector(1)
+        _native.call("lr_dot_f64", device.ptr(x), device.ptr(x), n, device.ptr(self.part), device.ptr(nrm2),
+                     device.stream())
+        nrm = float(np.sqrt(device.to_host(nrm2)[0]))
+        inv = device.f64_buffer(np.array([nrm]))
+        xs = device.vector(n).view(n, 1)
+        _native.call("lr_scale_columns_f64", device.ptr(x), 1, n, None, 1, device.ptr(inv), 1,
+                     device.ptr(xs), 1, device.stream())
+        self.x = xs
+        self.state = device.f64_buffer(np.zeros(6))
+
+    def update(self, z) -> None:
+        _native.call("lr_power_update_f64", device.ptr(self.x), device.ptr(z), self.n, _SPECTRAL_TOL,
+                     device.ptr(self.state), device.ptr(self.part), device.stream())
+
+    def done(self) -> bool:
+        return device.to_host(self.state)[2] != 0.0
+
+    def result(self) -> float:
+        st = device.to_host(self.state)
+        if st[4] != 0.0:
+            return 0.0
+        return float(max(st[0], st[1]))
+
+
 def spectral_norm_est_dev(A: SparseMatrix, x0_host: np.ndarray) -> float:
     """Power iteration on A^T A from x0 (sparse.py:231-256): stop at 1e-3
     relative agreement or 200 steps; return the larger of the last two."""
     n, m = A.cols, A.rows
-    # unit-stride (n, 1) views: the dot / power kernels treat them as flat vectors
-    x = device.f64_buffer(np.asarray(x0_host, dtype=np.float64).ravel()).view(n, 1)
-    part = device.arena().get("power_partial", 2 * 4096)
-    nrm2 = device.vector(1)
-    _native.call("lr_dot_f64", device.ptr(x), device.ptr(x), n, device.ptr(part), device.ptr(nrm2),
-                 device.stream())
-    nrm = float(np.sqrt(device.to_host(nrm2)[0]))
-    inv = device.f64_buffer(np.array([nrm]))
-    xs = device.vector(n).view(n, 1)
-    _native.call("lr_scale_columns_f64", device.ptr(x), 1, n, None, 1, device.ptr(inv), 1,
-                 device.ptr(xs), 1, device.stream())
-    x = xs
+    pw = PowerIteration(x0_host)
     y = device.vector(m).view(m, 1)
     z = device.vector(n).view(n, 1)
-    state = device.f64_buffer(np.zeros(6))
     for it in range(_SPECTRAL_MAX_ITERS):
-        if it and it % _SPECTRAL_BATCH == 0 and device.to_host(state)[2] != 0.0:
+        if it and it % _SPECTRAL_BATCH == 0 and pw.done():
             break
-        spmm_dev(A, x, out=y)
+        spmm_dev(A, pw.x, out=y)
         spmm_t_dev(A, y, out=z)
-        _native.call("lr_power_update_f64", device.ptr(x), device.ptr(z), n, _SPECTRAL_TOL,
-                     device.ptr(state), device.ptr(part), device.stream())
-    st = device.to_host(state)
-    if st[4] != 0.0:
-        return 0.0
-    return float(max(st[0], st[1]))
+        pw.update(z)
+    return pw.result()
 
 
 def spectral_norm_est(A: SparseMatrix, rng) -> float:
