@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--cpu-baseline", choices=["full", "skip"], default="full")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--svt", choices=["on", "off"], default="on")
+    ap.add_argument("--shard", action="store_true",
+                    help="one cfg2 call sharded over all ranks (shards.py; strong scaling) instead of "
+                         "independent replicas; at N=1 the NCCL collectives still run (world size 1)")
     return ap.parse_args()
 
 
@@ -263,9 +266,18 @@ def main():
     import torch
 
     torch.cuda.set_device(local)
-    if ws > 1:
+    if ws > 1 or args.shard:
+        import socket
+
         import torch.distributed as dist
 
+        if ws == 1:
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                os.environ.setdefault("MASTER_PORT", str(sk.getsockname()[1]))
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1810_06860_b200 import _native, device, profiling
     from paper_1810_06860_b200.rsvd import RsvdParams, rsvd_bki, rsvd_bki_dev
@@ -277,8 +289,17 @@ def main():
     A.device_values()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
 
-    def step():
-        return rsvd_bki_dev(A, params, allow_fallback=False, omega="device")
+    if args.shard:
+        from paper_1810_06860_b200.shards import Exchange, ShardedEngine, rsvd_bki_sharded
+
+        ex = Exchange(always_collective=True)
+        eng = ShardedEngine.from_matrix(A, ex)
+
+        def step():
+            return eng.bki(params, allow_fallback=False)
+    else:
+        def step():
+            return rsvd_bki_dev(A, params, allow_fallback=False, omega="device")
 
     for _ in range(args.warmup):
         step()
@@ -313,7 +334,10 @@ def main():
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    value = ws * args.steps / (ms * 1e-3)
+    # replicas: every rank runs its own call (weak); shard: one call over all ranks (strong)
+    calls = args.steps if args.shard else ws * args.steps
+    value = calls / (ms * 1e-3)
+    comm_bytes = (ex.bytes / (args.warmup + args.steps)) if args.shard else 0
 
     summary = prof.summary()
     step_ms = ms / args.steps
@@ -325,7 +349,10 @@ def main():
         torch.cuda.synchronize()
         t_h2d, t_d2h = device.TRAFFIC["h2d"], device.TRAFFIC["d2h"]
         t0 = time.perf_counter()
-        r_host, sub = rsvd_bki(A, params)
+        if args.shard:  # shard blocks cut and uploaded inside the timed call
+            r_host, sub = rsvd_bki_sharded(A, params, engine=ShardedEngine.from_matrix(A, ex))
+        else:
+            r_host, sub = rsvd_bki(A, params)
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
         h2d.append(device.TRAFFIC["h2d"] - t_h2d)
@@ -333,13 +360,14 @@ def main():
     if len(e2e_times) > 1:  # the first call warms the upload path
         e2e_times, h2d, d2h = e2e_times[1:], h2d[1:], d2h[1:]
     e2e_ms = float(np.mean(e2e_times)) * 1e3
+    e2e_calls = 1 if args.shard else ws
     if ws > 1:
         t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
     if rank != 0:
-        if ws > 1:
+        if torch.distributed.is_initialized():
             torch.distributed.destroy_process_group()
         return
 
@@ -385,12 +413,16 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "rSVD-BKI calls/s (cfg2, k=100)", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg2 generator)",
-        "config": {"workload": WORKLOAD, "parallelism": f"replicas x{ws}",
+        "scaling": "strong" if args.shard else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded cfg2 generator)",
+        "config": {"workload": WORKLOAD,
+                   "parallelism": (f"sharded x{ws} (row/column nnz shards, NCCL allgather + allreduce)"
+                                   if args.shard else f"replicas x{ws}"),
                    "omega": "device Philox4x64-10 (bit-exact numpy uniforms), value and e2e",
                    "l2": "256 MB flush between timed steps"},
         "rsvd_bki_time_s": step_ms * 1e-3,
-        "e2e": {"value": ws / (e2e_ms * 1e-3), "unit": "rSVD-BKI calls/s (cfg2, k=100)",
+        "comm_bytes_per_step": comm_bytes,
+        "e2e": {"value": e2e_calls / (e2e_ms * 1e-3), "unit": "rSVD-BKI calls/s (cfg2, k=100)",
                 "h2d_bytes_per_step": int(np.mean(h2d)), "d2h_bytes_per_step": int(np.mean(d2h)),
                 "ms_per_step": e2e_ms, "note": "public rsvd_bki(A, params) with pageable host numpy buffers"},
         "roofline": roofline,
@@ -401,7 +433,7 @@ def main():
         "svt": svt,
     }
     print(json.dumps(line), flush=True)
-    if ws > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
 
 

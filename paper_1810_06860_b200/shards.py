@@ -203,9 +203,15 @@ class DeviceKernels:
                          src.shape[0], src.shape[1], 0, device.stream())
 
     # sparse blocks
-    def block(self, rows, cols, indptr, indices, data):
+    def block(self, rows, cols, indptr, indices, data, prep=None, slot=0):
+        """Device block; prep[slot] caches its host prep (transpose index,
+        schedules) across re-uploads of the same pattern."""
         A = SparseMatrix(rows, cols, indptr, indices, data)
+        if prep is not None and prep[slot] is not None:
+            A._hprep = prep[slot]
         A.device_values()
+        if prep is not None:
+            prep[slot] = A._hprep
         return A
 
     def block_like(self, A, data):
@@ -362,25 +368,41 @@ class ShardedEngine:
         self.ex = exchange if exchange is not None else Exchange()
         self.K = kernels if kernels is not None else DeviceKernels()
         self.rank, self.world = self.ex.rank, self.ex.world
-        self._setup(A)
+        self._setup(A, A.__dict__.setdefault("_shard_cache", {}))
         return self
 
-    def _setup(self, phi: SparseMatrix) -> None:
+    def _setup(self, phi: SparseMatrix, cache: dict = None) -> None:
+        """Cut phi into this rank's row and column blocks.  The integer side
+        (plan, slices, block patterns and their host prep) is cached in
+        `cache` (A._shard_cache for from_matrix), like the single-GPU host
+        prep, so a re-upload re-slices only the values."""
         K = self.K
         self.m, self.n = phi.shape
         self.nnz = phi.nnz
-        _, t_indptr, _ = phi._transpose_index()
-        self.plan = ShardPlan(phi.indptr, t_indptr, self.world)
+        key = (self.world, self.rank)
+        st = cache.get(key) if cache is not None else None
+        if st is None:
+            _, t_indptr, _ = phi._transpose_index()
+            plan = ShardPlan(phi.indptr, t_indptr, self.world)
+            r0, r1 = plan.rows(self.rank)
+            c0, c1 = plan.cols(self.rank)
+            ip, ix = phi.indptr, phi.indices
+            lo, hi = int(ip[r0]), int(ip[r1])
+            sel = np.flatnonzero((ix >= c0) & (ix < c1))
+            cptr = np.zeros(self.m + 1, dtype=np.int64)
+            np.cumsum(np.bincount(phi.coo_rows()[sel], minlength=self.m), out=cptr[1:])
+            st = {"plan": plan, "lo": lo, "hi": hi, "rptr": ip[r0:r1 + 1] - lo, "ridx": ix[lo:hi], "sel": sel,
+                  "cptr": cptr, "cidx": ix[sel] - c0, "prep": [None, None]}
+            if cache is not None:
+                cache[key] = st
+        self.plan = st["plan"]
         self.r0, self.r1 = self.plan.rows(self.rank)
         self.c0, self.c1 = self.plan.cols(self.rank)
-        ip, ix, dv = phi.indptr, phi.indices, phi.data
-        lo, hi = int(ip[self.r0]), int(ip[self.r1])
-        self.phi_r = K.block(self.r1 - self.r0, self.n, ip[self.r0:self.r1 + 1] - lo, ix[lo:hi], dv[lo:hi])
-        sel = (ix >= self.c0) & (ix < self.c1)
-        rows_of = phi.coo_rows()[sel]
-        cptr = np.zeros(self.m + 1, dtype=np.int64)
-        np.cumsum(np.bincount(rows_of, minlength=self.m), out=cptr[1:])
-        self.phi_c = K.block(self.m, self.c1 - self.c0, cptr, ix[sel] - self.c0, dv[sel])
+        dv = phi.data
+        self.phi_r = K.block(self.r1 - self.r0, self.n, st["rptr"], st["ridx"], dv[st["lo"]:st["hi"]],
+                             prep=st["prep"], slot=0)
+        self.phi_c = K.block(self.m, self.c1 - self.c0, st["cptr"], st["cidx"], dv[st["sel"]],
+                             prep=st["prep"], slot=1)
         self.m_r = K.values(self.phi_r)
         self.m_c = K.values(self.phi_c)
         self.Y_r, self.Y_c = self.phi_r, self.phi_c  # rsvd on the observed matrix itself until start()

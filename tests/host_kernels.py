@@ -72,7 +72,7 @@ class HostKernels:
         dst.copy_(src)
 
     # sparse blocks (oracle Pattern)
-    def block(self, rows, cols, indptr, indices, data):
+    def block(self, rows, cols, indptr, indices, data, prep=None, slot=0):
         return ocsr.Pattern(rows, cols, indptr, indices, np.array(data, dtype=np.float64))
 
     def block_like(self, A, data):
