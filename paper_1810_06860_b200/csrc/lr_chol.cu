@@ -4,9 +4,14 @@
 // 64x64 blocks are factored and inverted in shared memory by one CTA; panel
 // and trailing updates are DMMA GEMMs (lr_gemm.cu).  A device flag makes the
 // remaining work a no-op after a non-positive pivot; the host reads `info`.
+#include <cooperative_groups.h>
+#include <stdlib.h>
+
 #include "lr_common.cuh"
 
 namespace lr {
+
+namespace cg = cooperative_groups;
 
 constexpr int CH_NB = 64;
 constexpr int CH_THREADS = 256;
@@ -131,6 +136,319 @@ __global__ void inv_place_diag_kernel(double* X, long long ldx, int n, int I, in
   }
 }
 
+// ------------------------------------------------------------------------
+// One cooperative kernel for W <= kCoopMaxN (every W of the BASELINE configs):
+// the host-driven blocked path above costs ~50 launches of tiny GEMMs per
+// call (2.5 ms at W = 660); here the whole factorization + inverse is one
+// launch with ONE grid barrier per 32-column block step.
+//
+// Step J (after the barrier; R_JJ and inv(R_JJ) are final):
+//   every trailing tile (K, L), J < K <= L, is updated by exactly one CTA:
+//     P_K = inv(R_JJ)^T A[J,K] (and P_L), A[K,L] -= P_K^T P_L
+//   (the panel products are recomputed per tile instead of paying a second
+//   barrier); the owner of the diagonal tile (K,K) parks P_K = R[J,K] in a
+//   double-buffered panel workspace that step J+1 copies into A[J,K] (A[J,*]
+//   is still being read during step J).  CTA 0 owns tile (J+1, J+1) and
+//   factors it in shared memory right after updating it: the next step's
+//   diagonal block is ready at the barrier.
+// Inverse: X = R^{-1} by independent (block column, 8-column slice) units,
+// bottom-up inside a unit with the slice kept in shared memory.
+constexpr int CB = 32;
+constexpr int CB_THREADS = 256;
+constexpr int CB_LD = CB + 1;
+constexpr int kCoopMaxN = 2048;  // nb <= 64
+constexpr int kCoopSmemDoubles = 6 * CB * CB_LD;
+
+__device__ __forceinline__ void cb_load(const double* __restrict__ A, long long lda, int n, int I, int K,
+                                        double (*t)[CB_LD]) {
+  for (int e = threadIdx.x; e < CB * CB; e += CB_THREADS) {
+    const int i = e >> 5, c = e & 31;
+    const int gi = I * CB + i, gc = K * CB + c;
+    t[i][c] = (gi < n && gc < n) ? A[(long long)gi * lda + gc] : 0.0;
+  }
+}
+
+__device__ __forceinline__ void cb_store(double* __restrict__ A, long long lda, int n, int I, int K,
+                                         const double (*t)[CB_LD]) {
+  for (int e = threadIdx.x; e < CB * CB; e += CB_THREADS) {
+    const int i = e >> 5, c = e & 31;
+    const int gi = I * CB + i, gc = K * CB + c;
+    if (gi < n && gc < n) A[(long long)gi * lda + gc] = t[i][c];
+  }
+}
+
+// out = D^T X (D upper: D^T lower -> k <= i), 32 x 32; thread owns row i, 4 cols
+__device__ __forceinline__ void cb_dtx(const double (*D)[CB_LD], const double (*X)[CB_LD], double (*out)[CB_LD]) {
+  const int i = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 4;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (int k = 0; k <= i; ++k) {
+    const double d = D[k][i];
+    a0 = fma(d, X[k][c0], a0);
+    a1 = fma(d, X[k][c0 + 1], a1);
+    a2 = fma(d, X[k][c0 + 2], a2);
+    a3 = fma(d, X[k][c0 + 3], a3);
+  }
+  out[i][c0] = a0;
+  out[i][c0 + 1] = a1;
+  out[i][c0 + 2] = a2;
+  out[i][c0 + 3] = a3;
+}
+
+// T -= P^T Q (32 x 32 x 32)
+__device__ __forceinline__ void cb_sub_ptq(const double (*P)[CB_LD], const double (*Q)[CB_LD], double (*T)[CB_LD]) {
+  const int i = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 4;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll 8
+  for (int k = 0; k < CB; ++k) {
+    const double p = P[k][i];
+    a0 = fma(p, Q[k][c0], a0);
+    a1 = fma(p, Q[k][c0 + 1], a1);
+    a2 = fma(p, Q[k][c0 + 2], a2);
+    a3 = fma(p, Q[k][c0 + 3], a3);
+  }
+  T[i][c0] -= a0;
+  T[i][c0 + 1] -= a1;
+  T[i][c0 + 2] -= a2;
+  T[i][c0 + 3] -= a3;
+}
+
+// Factor the (updated) diagonal tile t of block J in place (upper R, strict
+// lower part zeroed; rows / cols >= n padded with the identity) and write
+// x = inv(R).  Warp-synchronous: lane c keeps column c of the tile in
+// registers and every row broadcast is a shuffle, so the 32-step recurrences
+// carry no block barriers (a __syncthreads per step made this 25x slower).
+// Returns the 1-based global column of a non-positive pivot, 0 if fine;
+// called by ALL threads (warp 0 computes), result block-uniform.
+__device__ int cb_factor(double (*t)[CB_LD], double (*x)[CB_LD], double* rowbuf, int J, int n) {
+  __shared__ int s_bad;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x;
+    double a[CB];
+#pragma unroll
+    for (int i = 0; i < CB; ++i) {
+      const bool pad = (J * CB + i >= n) || (J * CB + lane >= n);
+      a[i] = pad ? (i == lane ? 1.0 : 0.0) : t[i][lane];
+    }
+    int bad = 0;
+    double rinv_lane = 1.0;  // lane j keeps 1 / R[j][j]
+#pragma unroll
+    for (int j = 0; j < CB; ++j) {
+      const double d = __shfl_sync(FULL, a[j], j);
+      if (!(d > 0.0)) {
+        bad = J * CB + j + 1;
+        break;
+      }
+      // LAPACK dpotf2 scales the row by 1/R_jj; sqrt and rsqrt issue in parallel
+      const double r = sqrt(d);
+      const double ri = rsqrt(d);
+      double v = (lane == j) ? r : a[j] * ri;  // R[j][lane]
+      if (lane < j) v = 0.0;
+      if (lane == j) rinv_lane = ri;
+      a[j] = v;
+#pragma unroll
+      for (int i = j + 1; i < CB; ++i) a[i] = fma(-__shfl_sync(FULL, v, i), v, a[i]);
+    }
+    if (lane == 0) s_bad = bad;
+    if (!bad) {
+      double xr[CB];
+#pragma unroll
+      for (int i = CB - 1; i >= 0; --i) {
+        double s0 = (i == lane) ? 1.0 : 0.0, s1 = 0.0;
+#pragma unroll
+        for (int k = i + 1; k < CB; k += 2) {
+          s0 = fma(-__shfl_sync(FULL, a[i], k), xr[k], s0);
+          if (k + 1 < CB) s1 = fma(-__shfl_sync(FULL, a[i], k + 1), xr[k + 1], s1);
+        }
+        xr[i] = (s0 + s1) * __shfl_sync(FULL, rinv_lane, i);
+      }
+#pragma unroll
+      for (int i = 0; i < CB; ++i) {
+        t[i][lane] = (lane < i) ? 0.0 : a[i];
+        x[i][lane] = xr[i];
+      }
+    }
+  }
+  __syncthreads();
+  return s_bad;
+}
+
+__device__ __forceinline__ void cb_tile_of(int t, int J, int nb, int& K, int& L) {
+  int len = nb - J - 1;
+  K = J + 1;
+  while (t >= len) {
+    t -= len;
+    ++K;
+    --len;
+  }
+  L = K + t;
+}
+
+__device__ __forceinline__ unsigned long long cb_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// trace (debug, LR_POTRF_TRACE): CTA 0 stamps globaltimer at phase ends
+#define CB_STAMP(k)                                                  \
+  do {                                                               \
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0 && (k) < 128) \
+      trace[k] = cb_now();                                           \
+  } while (0)
+
+__global__ void __launch_bounds__(CB_THREADS) chol_coop_kernel(int n, double* A, long long lda, double shift,
+                                                               double* Rinv, long long ldr, double* ws,
+                                                               int* info, unsigned long long* trace) {
+  cg::grid_group grid = cg::this_grid();
+  CB_STAMP(0);
+  extern __shared__ double cb_smem[];
+  double(*dinv)[CB_LD] = reinterpret_cast<double(*)[CB_LD]>(cb_smem);
+  double(*pk)[CB_LD] = reinterpret_cast<double(*)[CB_LD]>(cb_smem + 1 * CB * CB_LD);
+  double(*pl)[CB_LD] = reinterpret_cast<double(*)[CB_LD]>(cb_smem + 2 * CB * CB_LD);
+  double(*ld)[CB_LD] = reinterpret_cast<double(*)[CB_LD]>(cb_smem + 3 * CB * CB_LD);
+  double(*tt)[CB_LD] = reinterpret_cast<double(*)[CB_LD]>(cb_smem + 4 * CB * CB_LD);
+  double(*al)[CB_LD] = reinterpret_cast<double(*)[CB_LD]>(cb_smem + 5 * CB * CB_LD);
+  __shared__ double rowbuf[CB];
+  __shared__ int s_flag;
+  const int nb = (n + CB - 1) / CB;
+  const int np = nb * CB;  // padded order of the inverse accumulator
+  const int G = gridDim.x, b = blockIdx.x;
+  double* Dinv = ws;                                 // nb x CB x CB
+  double* Pws = ws + (long long)nb * CB * CB;        // 2 x nb x CB x CB
+  double* Acc = Pws + 2LL * nb * CB * CB;            // np x np: E - sum R^T W (inverse, right-looking)
+  const bool want_inv = Rinv != nullptr;
+
+  if (shift != 0.0)
+    for (int i = b * CB_THREADS + threadIdx.x; i < n; i += G * CB_THREADS) A[(long long)i * lda + i] += shift;
+  if (shift != 0.0) grid.sync();
+  if (want_inv)
+    for (long long e = (long long)b * CB_THREADS + threadIdx.x; e < (long long)np * np;
+         e += (long long)G * CB_THREADS)
+      Acc[e] = (e / np == e % np) ? 1.0 : 0.0;
+
+  if (b == 0) {
+    cb_load(A, lda, n, 0, 0, tt);
+    const int bad = cb_factor(tt, pk, rowbuf, 0, n);
+    if (bad) {
+      if (threadIdx.x == 0) *info = bad;
+    } else {
+      cb_store(A, lda, n, 0, 0, tt);
+      for (int e = threadIdx.x; e < CB * CB; e += CB_THREADS) Dinv[e] = pk[e >> 5][e & 31];
+    }
+  }
+  CB_STAMP(1);
+  grid.sync();
+  CB_STAMP(2);
+
+  for (int J = 0; J < nb; ++J) {
+    if (threadIdx.x == 0) s_flag = *reinterpret_cast<volatile int*>(info);
+    __syncthreads();
+    if (s_flag != 0) return;  // uniform: every CTA read the flag after the same barrier
+    // park the previous step's panel R[J-1, K] (K >= J) into A
+    if (J > 0) {
+      const double* P = Pws + (long long)((J - 1) & 1) * nb * CB * CB;
+      for (int K = J + b; K < nb; K += G) {
+        const double* src = P + (long long)K * CB * CB;
+        for (int e = threadIdx.x; e < CB * CB; e += CB_THREADS) {
+          const int i = e >> 5, c = e & 31;
+          const int gi = (J - 1) * CB + i, gc = K * CB + c;
+          if (gi < n && gc < n) A[(long long)gi * lda + gc] = src[e];
+        }
+      }
+    }
+    // work items of step J:
+    //   [0, Tc)        Cholesky trailing tiles (K, L), J < K <= L     (t = 0: CTA 0, then factor)
+    //   [Tc, Tc+Ti)    inverse updates Acc[K, L] -= R_JK^T W_JL, K > J >= L
+    //   [Tc+Ti, T)     finalize W_JL = inv(R_JJ)^T Acc[J, L] -> Rinv[L, J] = W_JL^T, L <= J
+    const int nr = nb - J - 1;
+    const int Tc = nr * (nr + 1) / 2;
+    const int Ti = want_inv ? nr * (J + 1) : 0;
+    const int T = Tc + Ti + (want_inv ? J + 1 : 0);
+    bool have_dinv = false;
+    const int first = (b == 0) ? 0 : (G == 1 ? 1 : b);
+    const int stride = (G == 1) ? 1 : G - 1;
+    for (int t = first; t < T; t = (b == 0 && G > 1) ? T : (t == 0 ? 1 : t + stride)) {
+      if (!have_dinv) {
+        const double* D = Dinv + (long long)J * CB * CB;
+        for (int e = threadIdx.x; e < CB * CB; e += CB_THREADS) dinv[e >> 5][e & 31] = D[e];
+        have_dinv = true;
+      }
+      if (t < Tc) {
+        int K, L;
+        cb_tile_of(t, J, nb, K, L);
+        // all four operand tiles in flight at once (one L2 round trip per tile)
+        cb_load(A, lda, n, J, K, ld);
+        if (K != L) cb_load(A, lda, n, J, L, al);
+        cb_load(A, lda, n, K, L, tt);
+        __syncthreads();
+        cb_dtx(dinv, ld, pk);
+        if (K != L) cb_dtx(dinv, al, pl);
+        __syncthreads();
+        cb_sub_ptq(pk, K == L ? pk : pl, tt);
+        __syncthreads();
+        if (K == L) {
+          double* dst = Pws + (long long)(J & 1) * nb * CB * CB + (long long)K * CB * CB;
+          for (int e = threadIdx.x; e < CB * CB; e += CB_THREADS) dst[e] = pk[e >> 5][e & 31];
+        }
+        if (t == 0) {  // CTA 0: next diagonal block
+          const int bad = cb_factor(tt, pl, rowbuf, K, n);
+          if (bad) {
+            if (threadIdx.x == 0) atomicExch(info, bad);
+          } else {
+            cb_store(A, lda, n, K, K, tt);
+            double* D = Dinv + (long long)K * CB * CB;
+            for (int e = threadIdx.x; e < CB * CB; e += CB_THREADS) D[e] = pl[e >> 5][e & 31];
+          }
+        } else {
+          cb_store(A, lda, n, K, L, tt);
+        }
+      } else if (t < Tc + Ti) {
+        const int u = t - Tc;
+        const int K = J + 1 + u / (J + 1), L = u % (J + 1);
+        cb_load(A, lda, n, J, K, ld);
+        cb_load(Acc, np, np, J, L, al);
+        cb_load(Acc, np, np, K, L, tt);
+        __syncthreads();
+        cb_dtx(dinv, ld, pk);   // R_JK
+        cb_dtx(dinv, al, pl);   // W_JL
+        __syncthreads();
+        cb_sub_ptq(pk, pl, tt);
+        __syncthreads();
+        cb_store(Acc, np, np, K, L, tt);
+      } else {
+        const int L = t - Tc - Ti;
+        cb_load(Acc, np, np, J, L, al);
+        __syncthreads();
+        cb_dtx(dinv, al, pl);
+        __syncthreads();
+        for (int e = threadIdx.x; e < CB * CB; e += CB_THREADS) {
+          const int i = e >> 5, c = e & 31;  // W_JL[i][c] -> Rinv[L*CB + c][J*CB + i]
+          const int gr = L * CB + c, gc = J * CB + i;
+          if (gr < n && gc < n) Rinv[(long long)gr * ldr + gc] = pl[i][c];
+        }
+      }
+      __syncthreads();
+    }
+    CB_STAMP(3 + 2 * J);
+    grid.sync();
+    CB_STAMP(4 + 2 * J);
+  }
+
+  // zero the strict lower block triangle of R (diagonal tiles were cleaned by
+  // cb_factor) and of R^{-1}
+  for (long long e = (long long)b * CB_THREADS + threadIdx.x; e < (long long)n * n;
+       e += (long long)G * CB_THREADS) {
+    const int i = (int)(e / n), c = (int)(e % n);
+    if (i / CB > c / CB) {
+      A[(long long)i * lda + c] = 0.0;
+      if (want_inv) Rinv[(long long)i * ldr + c] = 0.0;
+    }
+  }
+  CB_STAMP(120);
+}
+
 }  // namespace lr
 
 using namespace lr;
@@ -138,15 +456,60 @@ using namespace lr;
 extern "C" {
 
 long long lr_potrf_workspace_doubles(int n) {
-  // Dinv blocks + panel temp + gemm split workspace (none: transA gemms here are tiny-K)
+  // blocked path: Dinv blocks + panel temp; cooperative path: Dinv + 2 panels
   long long nblk = (n + CH_NB - 1) / CH_NB;
-  return nblk * CH_NB * CH_NB + (long long)CH_NB * n + 64;
+  long long blocked = nblk * CH_NB * CH_NB + (long long)CH_NB * n + 64;
+  long long nb = (n + CB - 1) / CB;
+  long long coop = 3 * nb * CB * CB + (nb * CB) * (nb * CB) + 64;
+  return blocked > coop ? blocked : coop;
+}
+
+static int potrf_coop(int n, double* A, long long lda, double shift, double* Rinv, long long ldr,
+                      double* work, int* info_host, cudaStream_t s) {
+  const int nb = (n + CB - 1) / CB;
+  const size_t smem = (size_t)kCoopSmemDoubles * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    LR_CHECK_CUDA(cudaFuncSetAttribute(chol_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  int occ = 0;
+  LR_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chol_coop_kernel, CB_THREADS, smem));
+  // widest step: Cholesky tiles + inverse updates + finalize ~ nb^2 / 2
+  int G = (nb * nb) / 2 + 2;
+  if (G > sm_count()) G = sm_count();
+  if (G > occ * sm_count()) G = occ * sm_count();
+  if (G < 1) G = 1;
+  int* info = reinterpret_cast<int*>(work + 3LL * nb * CB * CB + (long long)nb * CB * nb * CB);
+  LR_CHECK_CUDA(cudaMemsetAsync(info, 0, sizeof(int), s));
+  static const bool tracing = getenv("LR_POTRF_TRACE") != nullptr;
+  static unsigned long long* trace = nullptr;
+  if (tracing && !trace) LR_CHECK_CUDA(cudaMallocManaged(&trace, 128 * sizeof(unsigned long long)));
+  void* args[] = {&n, &A, &lda, &shift, &Rinv, &ldr, &work, &info, &trace};
+  LR_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)chol_coop_kernel, dim3((unsigned)G), dim3(CB_THREADS),
+                                            args, smem, s));
+  LR_CHECK_LAUNCH();
+  if (info_host) {
+    LR_CHECK_CUDA(cudaMemcpyAsync(info_host, info, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LR_CHECK_CUDA(cudaStreamSynchronize(s));
+  }
+  if (tracing) {
+    LR_CHECK_CUDA(cudaStreamSynchronize(s));
+    fprintf(stderr, "potrf_coop n=%d G=%d:", n, G);
+    for (int k = 1; k < 4 + 2 * nb; ++k)
+      if (trace[k]) fprintf(stderr, " %d:%.1f", k, (trace[k] - trace[0]) * 1e-3);
+    fprintf(stderr, " end:%.1f us\n", (trace[120] - trace[0]) * 1e-3);
+    for (int k = 0; k < 128; ++k) trace[k] = 0;
+  }
+  return LR_OK;
 }
 
 int lr_potrf_inv_f64(int n, double* A, long long lda, double shift, double* Rinv, long long ldr,
                      double* work, int* info_host, void* stream) {
   LR_REQUIRE(n >= 1 && lda >= n && ldr >= n, "potrf: bad shape");
   cudaStream_t s = as_stream(stream);
+  static const bool blocked_only = getenv("LR_POTRF_BLOCKED") != nullptr;
+  if (n <= kCoopMaxN && !blocked_only) return potrf_coop(n, A, lda, shift, Rinv, ldr, work, info_host, s);
   const long long nblk = (n + CH_NB - 1) / CH_NB;
   double* Dinv = work;
   double* T = work + nblk * CH_NB * CH_NB;  // CH_NB x n

@@ -329,21 +329,40 @@ int lr_spmm_f64(const int* ptr, const int* idx, const double* val, int rows, con
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     spmv_kernel<<<(int)blocks, 256, 0, s>>>(ptr, idx, val, items, n_items, X, ldx, Y, ldy, scratch);
-  } else {
-    const bool v2 = (ldx % 2 == 0) && (ldy % 2 == 0) && aligned16(X) && aligned16(Y) &&
-                    (scratch == nullptr || aligned16(scratch));
-    if (v2)
-      dispatch_spmm<true>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
-    else
-      dispatch_spmm<false>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
-  }
-  LR_CHECK_LAUNCH();
-  if (n_splits > 0) {
-    long long total = (long long)n_splits * w;
-    long long blocks = (total + 255) / 256;
-    if (blocks > sm_count() * 8) blocks = sm_count() * 8;
-    spmm_split_reduce_kernel<<<(int)blocks, 256, 0, s>>>(splits, n_splits, scratch, w, Y, ldy);
     LR_CHECK_LAUNCH();
+    if (n_splits > 0) {
+      long long rb = ((long long)n_splits + 255) / 256;
+      if (rb > sm_count() * 8) rb = sm_count() * 8;
+      spmm_split_reduce_kernel<<<(int)rb, 256, 0, s>>>(splits, n_splits, scratch, 1, Y, ldy);
+      LR_CHECK_LAUNCH();
+    }
+    return LR_OK;
+  }
+  // Wide products (the W-column Y^T Q of BKI / recycle-q) run as column
+  // chunks of <= kChunkCols: each chunk's slice of X (rows x chunk doubles)
+  // stays L2-resident while every stored entry gathers from it, instead of
+  // all W columns of X (m x W, 528 MB at cfg2) streaming through L2 at once.
+  constexpr int kChunkCols = 128;
+  const int n_chunks = (w + kChunkCols - 1) / kChunkCols;
+  const int cw_even = (((w + n_chunks - 1) / n_chunks) + 1) & ~1;
+  for (int c0 = 0; c0 < w; c0 += cw_even) {
+    const int cw = (w - c0 < cw_even) ? (w - c0) : cw_even;
+    const double* Xc = X + c0;
+    double* Yc = Y + c0;
+    const bool v2 = (ldx % 2 == 0) && (ldy % 2 == 0) && aligned16(Xc) && aligned16(Yc) &&
+                    (scratch == nullptr || (aligned16(scratch) && cw % 2 == 0));
+    if (v2)
+      dispatch_spmm<true>(ptr, idx, val, items, n_items, Xc, ldx, cw, Yc, ldy, scratch, s);
+    else
+      dispatch_spmm<false>(ptr, idx, val, items, n_items, Xc, ldx, cw, Yc, ldy, scratch, s);
+    LR_CHECK_LAUNCH();
+    if (n_splits > 0) {
+      long long total = (long long)n_splits * cw;
+      long long blocks = (total + 255) / 256;
+      if (blocks > sm_count() * 8) blocks = sm_count() * 8;
+      spmm_split_reduce_kernel<<<(int)blocks, 256, 0, s>>>(splits, n_splits, scratch, cw, Yc, ldy);
+      LR_CHECK_LAUNCH();
+    }
   }
   return LR_OK;
 }

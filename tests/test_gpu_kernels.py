@@ -152,7 +152,7 @@ def test_upper_triangular_b_and_potrf_inverse():
     from paper_1810_06860_b200 import device
     from paper_1810_06860_b200.linalg import matmul_dev, potrf_inv_dev
 
-    for n in (1, 5, 64, 65, 130, 300):
+    for n in (1, 5, 31, 32, 33, 64, 65, 130, 300, 660, 1220, 2048, 2050):
         X = np.random.default_rng(n).standard_normal((3 * n + 10, n))
         G = X.T @ X
         Gd = device.to_device(G)
@@ -166,9 +166,23 @@ def test_upper_triangular_b_and_potrf_inverse():
         assert rel(Ri @ R, np.eye(n)) <= 1e-10
         Q = device.to_host(matmul_dev(device.to_device(X), Rinv, b_upper=True))
         assert rel(Q.T @ Q, np.eye(n)) <= 1e-9
-    # breakdown is reported, not raised
+    # breakdown is reported, not raised (1-based column of the first bad pivot)
     info, _ = potrf_inv_dev(device.to_device(np.array([[1.0, 2.0], [2.0, 1.0]])))
     assert info == 2
+    for n, bad in ((100, 70), (660, 33), (660, 659)):
+        X = np.random.default_rng(bad).standard_normal((2 * n, n))
+        X[:, bad] = X[:, :bad] @ np.random.default_rng(1).standard_normal(bad)  # dependent column
+        G = X.T @ X
+        G[bad, bad] -= 1e-6 * G[bad, bad]  # push the Schur complement negative
+        info, _ = potrf_inv_dev(device.to_device(G))
+        assert info == bad + 1, (n, bad, info)
+    # shifted factorization (shifted CholeskyQR3): R^T R = G + shift I
+    X = np.random.default_rng(7).standard_normal((500, 200))
+    G = X.T @ X
+    Gd = device.to_device(G)
+    info, Rinv = potrf_inv_dev(Gd, 3.5)
+    R = device.to_host(Gd)
+    assert info == 0 and rel(R.T @ R, G + 3.5 * np.eye(200)) <= 1e-13
 
 
 @pytest.mark.parametrize("m,n", [(25, 7), (300, 40), (5000, 110), (100000, 110), (138493, 65), (40, 40)])
