@@ -82,6 +82,19 @@ __global__ void __launch_bounds__(T::THREADS) gemm_kernel(int M, int N, int K, d
 #pragma unroll
     for (int j = 0; j < T::NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  // Warp-uniform pruning: a warp whose sub-tile lies outside C or strictly
+  // below the diagonal (SYRK) issues no DMMA, and with an upper-triangular B
+  // a warp stops at its last column's k (B[k][c] = 0 for k > c).  (Per-
+  // fragment predication was tried: it breaks the DMMA issue stream.)
+  bool warp_live;
+  int warp_klim;
+  {
+    const int rbase = m0 + wm * T::WM, cbase = n0 + wn * T::WN;
+    warp_live = rbase < M && cbase < N;
+    if ((flags & LR_GEMM_SYRK_UPPER) && cbase + T::WN - 1 < rbase) warp_live = false;
+    warp_klim = (flags & LR_GEMM_B_UPPER) ? min(k_end, cbase + T::WN) : k_end;
+  }
+
   auto load_stage = [&](int st, int kt) {
     const int k0 = k_begin + kt * BK;
     double* as = As + st * T::A_STAGE;
@@ -149,6 +162,8 @@ __global__ void __launch_bounds__(T::THREADS) gemm_kernel(int M, int N, int K, d
     }
     const double* as = As + (kt % STAGES) * T::A_STAGE;
     const double* bs = Bs + (kt % STAGES) * T::B_STAGE;
+    const int kg0 = k_begin + kt * BK;
+    if (!warp_live || kg0 >= warp_klim) continue;  // warp-uniform; barriers are at the loop top
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[T::MT], bf[T::NT];

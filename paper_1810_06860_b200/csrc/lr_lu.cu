@@ -64,9 +64,6 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
   __shared__ double red_v[LU_THREADS / 32];
   __shared__ int red_r[LU_THREADS / 32];
   __shared__ double win_v;
-  __shared__ int win_r, win_c;
-  __shared__ double red_v2[LU_THREADS / 32];
-  __shared__ int red_r2[LU_THREADS / 32];
   long long* prof = (blockIdx.x == 0 && threadIdx.x == 0) ? p.prof : nullptr;
   long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
   double cbv = -1.0;  // look-ahead candidate for the next column
@@ -132,13 +129,15 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
       if (prof) t1 = clock64();
       grid.sync();
       if (prof) t2 = clock64();
-      {
-        // global winner, same in every CTA: all threads load candidates at
-        // once (one L2 round trip), warps reduce, warp 0 folds
+      if (wid == 0) {
+        // global winner, same in every CTA: warp 0 alone loads the G
+        // candidates (G/32 independent L2 loads per lane), folds them with
+        // shuffles and fetches the winner's panel row -- no block-level
+        // reduction between the two L2 round trips
         double v = -1.0;
         int r = 0x7fffffff;
-        for (int c = tid; c < G; c += LU_THREADS) {
-          const double2 cr = reinterpret_cast<const double2*>(p.cand)[par * G + c];
+        for (int c = lane; c < G; c += 32) {
+          const double2 cr = __ldcg(reinterpret_cast<const double2*>(p.cand) + par * G + c);
           better(v, r, cr.x, (int)cr.y);
         }
 #pragma unroll
@@ -147,30 +146,11 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
           int r2 = __shfl_xor_sync(0xffffffffu, r, o);
           better(v, r, v2, r2);
         }
-        if (lane == 0) {
-          red_v2[wid] = v;
-          red_r2[wid] = r;
-        }
-      }
-      __syncthreads();
-      if (wid == 0) {
-        double v = (lane < LU_THREADS / 32) ? red_v2[lane] : -1.0;
-        int r = (lane < LU_THREADS / 32) ? red_r2[lane] : 0x7fffffff;
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
-          double v2 = __shfl_xor_sync(0xffffffffu, v, o);
-          int r2 = __shfl_xor_sync(0xffffffffu, r, o);
-          better(v, r, v2, r2);
-        }
-        v = __shfl_sync(0xffffffffu, v, 0);
-        r = __shfl_sync(0xffffffffu, r, 0);
         const int wc = r / p.rows_per;  // slabs are contiguous
         const double* wrow = p.prow + ((long long)par * G + wc) * nb;
-        for (int c = lane; c < jb; c += 32) urow[c] = wrow[c];
+        for (int c = lane; c < jb; c += 32) urow[c] = __ldcg(wrow + c);
         if (lane == 0) {
           win_v = v;
-          win_r = r;
-          win_c = wc;
           if (r >= r0 && r < r1 && v >= tol && v != 0.0) pivflag[r - r0] = j;
           if (cta == 0) p.pivrow[j] = r;
         }
@@ -185,14 +165,14 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
         return;  // uniform across the grid
       }
       if (prof) t3 = clock64();
-      const double upiv = urow[jj];
+      const double rpiv = 1.0 / urow[jj];  // LAPACK dgetf2/dgetrf2: scale by 1/pivot
       cbv = -1.0;
       cbr = 0x7fffffff;
       const bool look = jj + 1 < jb;
       for (int i = tid; i < nr; i += LU_THREADS) {
         if (pivflag[i] >= 0) continue;
         double* row = P + i * LD;
-        const double l = row[jj] / upiv;
+        const double l = row[jj] * rpiv;
         row[jj] = l;
         for (int c = jj + 1; c < jb; ++c) row[c] = fma(-l, urow[c], row[c]);
         if (look) better(cbv, cbr, fabs(row[jj + 1]), r0 + i);
