@@ -90,11 +90,39 @@ def to_device(x, *, copy=True) -> torch.Tensor:
     return out
 
 
+# Device -> host copies of at least this many bytes land in page-locked
+# memory from torch's caching host allocator (full-rate DMA, no staging copy);
+# the returned numpy array keeps its pinned block alive and hands it back to
+# the cache when it dies.
+PINNED_D2H_MIN_BYTES = 1 << 20
+
+
 def to_host(t) -> np.ndarray:
     if isinstance(t, np.ndarray):
         return t
-    out = t.detach().contiguous().cpu().numpy()
+    t = t.detach()
+    nbytes = t.numel() * t.element_size()
+    if t.device.type == "cuda" and nbytes >= PINNED_D2H_MIN_BYTES:
+        host = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+        host.copy_(t)
+        out = host.numpy()
+    else:
+        out = t.contiguous().cpu().numpy()
     TRAFFIC["d2h"] += out.nbytes
+    return out
+
+
+_NP_TO_TORCH = {np.dtype(np.float64): torch.float64, np.dtype(np.int64): torch.int64,
+                np.dtype(np.int32): torch.int32, np.dtype(np.uint8): torch.uint8}
+
+
+def pinned_copy(a: np.ndarray) -> np.ndarray:
+    """A page-locked copy of a host array (numpy view of a pinned torch
+    buffer): host -> device uploads from it are direct DMA transfers."""
+    a = np.ascontiguousarray(a)
+    t = torch.empty(a.shape, dtype=_NP_TO_TORCH[a.dtype], pin_memory=True)
+    out = t.numpy()
+    out[...] = a
     return out
 
 

@@ -89,6 +89,16 @@ class _Side:
 
 
 class _HostPrep:
+    def pin(self) -> None:
+        """Move every upload source into page-locked memory."""
+        for side in (self.csr, self.csc):
+            for name in ("ptr", "idx", "items", "splits"):
+                a = getattr(side, name)
+                if a is not None:
+                    setattr(side, name, device.pinned_copy(a))
+        self.perm = device.pinned_copy(self.perm)
+        self.inv_perm = device.pinned_copy(self.inv_perm)
+
     def __init__(self, A: "SparseMatrix"):
         perm, t_indptr, t_indices = A._transpose_index()
         inv = np.empty(A.nnz, dtype=np.int32)
@@ -242,6 +252,16 @@ class SparseMatrix:
         if self._pattern is None:
             self._pattern = DevicePattern(self)
         return self._pattern
+
+    def pin_memory(self) -> "SparseMatrix":
+        """Keep the host side (values and the prepared CSR/CSC index arrays)
+        in page-locked memory, so every (re-)upload of this matrix is a
+        direct DMA.  Returns self."""
+        if self._host_stale:
+            _ = self.data
+        self._data = device.pinned_copy(self._data)
+        self._host_prep().pin()
+        return self
 
     def drop_device(self) -> None:
         """Release the device mirror (pattern and values); host data stay."""
