@@ -14,7 +14,7 @@ import os
 from .errors import NumericalError, RankDeficiencyError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_native", "liblowrank_b200.so")
+LIB_PATH = os.environ.get("LR_NATIVE_LIB") or os.path.join(_HERE, "_native", "liblowrank_b200.so")  # override: experiments only
 
 LR_OK, LR_ERR_ARG, LR_ERR_RANK, LR_ERR_NOCONV, LR_ERR_CUDA = 0, 1, 2, 3, 4
 LR_GEMM_B_UPPER, LR_GEMM_SYRK_UPPER = 1, 2

@@ -38,7 +38,10 @@ __device__ __forceinline__ Item load_item(const int* __restrict__ items, const i
 // c = 2*(g + G*t), t < T, of a column tile of width 2*G*T starting at c0.
 // VEC2: double2 loads/stores (requires 16B-aligned rows); tail columns scalar.
 template <int G, int T, bool VEC2>
-__global__ void __launch_bounds__(256) spmm_kernel(const int* __restrict__ ptr,
+#ifndef LR_SPMM_MINB
+#define LR_SPMM_MINB 4
+#endif
+__global__ void __launch_bounds__(256, LR_SPMM_MINB) spmm_kernel(const int* __restrict__ ptr,
                                                    const int* __restrict__ idx,
                                                    const double* __restrict__ val,
                                                    const int* __restrict__ items, int n_items,
