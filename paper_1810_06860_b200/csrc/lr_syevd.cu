@@ -31,7 +31,6 @@ namespace cg = cooperative_groups;
 
 namespace lr {
 
-constexpr int TD_THREADS = 256;
 
 struct TdParams {
   const double* A;
@@ -310,7 +309,7 @@ __global__ void inviter_kernel(const double* __restrict__ d, const double* __res
     if (fabs(a) >= fabs(c)) {
       const double piv = (a == 0.0) ? tiny : a;
       const double l = c / piv;
-      Dg[IX(i)] = piv;
+      Dg[IX(i)] = piv;  // replaced by its clamped reciprocal below (off the recurrence)
       U1[IX(i)] = b;
       U2[IX(i)] = 0.0;
       Lm[IX(i)] = l;
@@ -329,10 +328,22 @@ __global__ void inviter_kernel(const double* __restrict__ d, const double* __res
     }
   }
   Dg[IX(n - 1)] = (a == 0.0) ? tiny : a;
+  // reciprocal diagonal (clamped away from zero like the solve below would):
+  // independent per i, so the back substitutions carry FMAs only instead of a
+  // 125-cycle division per step (tools/dp_latency.cu)
+#pragma unroll 4
+  for (int i = 0; i < n; ++i) {
+    double dg = Dg[IX(i)];
+    if (fabs(dg) < tiny) dg = (dg < 0.0) ? -tiny : tiny;
+    Dg[IX(i)] = 1.0 / dg;
+  }
   unsigned long long s = 0x9E3779B97F4A7C15ULL * (unsigned long long)(k + 1);
   double scale = 1.0;
   // two solves: the shift is accurate to ~1e-3 eps ||T|| (bisection), so the
-  // first solve already amplifies the wanted direction by ~1/(eps*||T||)
+  // first solve already amplifies the wanted direction by ~1/(eps*||T||).
+  // The recurrences are branch-free and their operands are fetched 8 steps
+  // at a time, so the L2 latency is paid once per 8 steps, not per step.
+  constexpr int PF = 8;
   for (int it = 0; it < 2; ++it) {
     // forward: z <- L^{-1} P (scale * z); the start vector is generated in pass 0
     double zc;
@@ -342,47 +353,70 @@ __global__ void inviter_kernel(const double* __restrict__ d, const double* __res
     } else {
       zc = Z[IX(0)] * scale;
     }
-#pragma unroll 4
-    for (int i = 0; i < n - 1; ++i) {
-      double zn;
-      if (it == 0) {
-        s ^= s >> 12; s ^= s << 25; s ^= s >> 27;
-        zn = (double)((s * 2685821657736338717ULL) >> 11) * (2.0 / 9007199254740992.0) - 1.0;
-      } else {
-        zn = Z[IX(i + 1)] * scale;
+    for (int i0 = 0; i0 < n - 1; i0 += PF) {
+      double lv[PF], zv[PF];
+      int pv[PF];
+#pragma unroll
+      for (int q = 0; q < PF; ++q) {
+        const int i = i0 + q;
+        const bool ok = i < n - 1;
+        lv[q] = ok ? Lm[IX(i)] : 0.0;
+        pv[q] = ok ? Pv[IX(i)] : 0;
+        if (it == 0) {
+          s ^= s >> 12; s ^= s << 25; s ^= s >> 27;
+          zv[q] = (double)((s * 2685821657736338717ULL) >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+        } else {
+          zv[q] = ok ? Z[IX(i + 1)] * scale : 0.0;
+        }
       }
-      const double l = Lm[IX(i)];
-      if (Pv[IX(i)]) {
-        Z[IX(i)] = zn;
-        zc = zc - l * zn;
-      } else {
-        Z[IX(i)] = zc;
-        zc = zn - l * zc;
+#pragma unroll
+      for (int q = 0; q < PF; ++q) {
+        const int i = i0 + q;
+        if (i < n - 1) {
+          const double zn = zv[q], l = lv[q];
+          const double keep = pv[q] ? zn : zc;       // value stored at row i
+          const double next = pv[q] ? zc - l * zn : zn - l * zc;
+          Z[IX(i)] = keep;
+          zc = next;
+        }
       }
     }
     Z[IX(n - 1)] = zc;
-    // backward: U x = y, track max |x| for the next scale
+    // backward: U x = y (Dg holds reciprocal pivots), track max |x| for the next scale
     double x1 = 0.0, x2 = 0.0, mx = 0.0;
-#pragma unroll 4
-    for (int i = n - 1; i >= 0; --i) {
-      double dg = Dg[IX(i)];
-      if (fabs(dg) < tiny) dg = (dg < 0.0) ? -tiny : tiny;
-      const double xi = (Z[IX(i)] - U1[IX(i)] * x1 - U2[IX(i)] * x2) / dg;
-      Z[IX(i)] = xi;
-      x2 = x1;
-      x1 = xi;
-      mx = fmax(mx, fabs(xi));
+    for (int i0 = n - 1; i0 >= 0; i0 -= PF) {
+      double zv[PF], u1[PF], u2[PF], rd[PF];
+#pragma unroll
+      for (int q = 0; q < PF; ++q) {
+        const int i = i0 - q;
+        const bool ok = i >= 0;
+        zv[q] = ok ? Z[IX(i)] : 0.0;
+        u1[q] = ok ? U1[IX(i)] : 0.0;
+        u2[q] = ok ? U2[IX(i)] : 0.0;
+        rd[q] = ok ? Dg[IX(i)] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < PF; ++q) {
+        const int i = i0 - q;
+        if (i >= 0) {
+          const double xi = (zv[q] - u1[q] * x1 - u2[q] * x2) * rd[q];
+          Z[IX(i)] = xi;
+          x2 = x1;
+          x1 = xi;
+          mx = fmax(mx, fabs(xi));
+        }
+      }
     }
     scale = (mx > 0.0) ? 1.0 / mx : 1.0;
   }
   double ss = 0.0;
-#pragma unroll 4
+#pragma unroll 8
   for (int i = 0; i < n; ++i) {
     const double z = Z[IX(i)] * scale;
     ss = fma(z, z, ss);
   }
   const double inv = scale / sqrt(ss);
-#pragma unroll 4
+#pragma unroll 8
   for (int i = 0; i < n; ++i) Z[IX(i)] *= inv;
 #undef IX
 }
@@ -457,15 +491,20 @@ __global__ void __launch_bounds__(256) build_T_kernel(const double* __restrict__
 // All reflector blocks applied to a tile of kTC eigenvector columns by one
 // CTA (columns are independent: no inter-CTA dependency, one launch):
 // for b = last..0:  Y = V_b^T Z_tile, Y = T_b Y, Z_tile -= V_b Y.
+// Register-blocked for shared-memory bandwidth: in Y = V^T Z a lane owns one
+// reflector k and all kTC columns (Z row broadcast, V row conflict-free), four
+// warps split the reflector length and fold in fixed order; in Z -= V Y a
+// thread owns one row c and all kTC columns.  ~2.6x fewer shared-memory
+// wavefronts per FMA than one output per thread.
+constexpr int kWyRedWarps = 4;
 template <int kTC>
 __global__ void __launch_bounds__(256) wy_apply_kernel(double* __restrict__ Z, int n, const double* __restrict__ Vr,
                                                      const double* __restrict__ T, int nrefl, double* __restrict__ V,
                                                      long long ldv, int stage_v) {
-  extern __shared__ double zs[];  // n x kTC
-  __shared__ double Y[kWY][kTC];
+  extern __shared__ double zs[];  // n x kTC, then (staged) the block's reflector rows
+  __shared__ double red[kWyRedWarps][kWY][kTC];  // per-warp partials; red[0] then holds Y
   __shared__ double Y2[kWY][kTC];
-  __shared__ double Ts[kWY][kWY + 1];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
   const int c0 = blockIdx.x * kTC;
   const int tc = min(kTC, n - c0);
   for (int e = tid; e < n * kTC; e += 256) {
@@ -473,14 +512,11 @@ __global__ void __launch_bounds__(256) wy_apply_kernel(double* __restrict__ Z, i
     zs[e] = (t < tc) ? Z[(long long)i * n + c0 + t] : 0.0;
   }
   const int nblk = (nrefl + kWY - 1) / kWY;
-  const int k = tid / kTC, t = tid % kTC;  // 32 x kTC threads (k >= 32 idle in the small phases)
-  // staged: the block's reflector rows live in shared memory (ld n+1, odd)
   double* vb = stage_v ? zs + (size_t)n * kTC : nullptr;
   const int LDV = n + 1;
   for (int b = nblk - 1; b >= 0; --b) {
     const int J = b * kWY;
     const int bsb = min(kWY, nrefl - J);
-    for (int e = tid; e < kWY * kWY; e += 256) Ts[e / kWY][e % kWY] = T[(long long)b * kWY * kWY + e];
     if (vb) {
       const int L = n - J - 1;
       for (int e = tid; e < bsb * L; e += 256) {
@@ -489,34 +525,53 @@ __global__ void __launch_bounds__(256) wy_apply_kernel(double* __restrict__ Z, i
       }
     }
     __syncthreads();
-    double acc = 0.0;
-    if (k < bsb && k < kWY) {
-      if (vb) {
-        const double* vrow = vb + k * LDV;
-#pragma unroll 4
-        for (int c = J + 1; c < n; ++c) acc = fma(vrow[c], zs[c * kTC + t], acc);
-      } else {
-        const double* vrow = Vr + (long long)(J + k) * n;
-#pragma unroll 4
-        for (int c = J + 1; c < n; ++c) acc = fma(vrow[c], zs[c * kTC + t], acc);
+    // (1) partials of Y[k][:] over a quarter of the reflector length
+    if (wp < kWyRedWarps) {
+      double acc[kTC];
+#pragma unroll
+      for (int t = 0; t < kTC; ++t) acc[t] = 0.0;
+      if (lane < bsb) {
+        const double* vrow = vb ? vb + lane * LDV : Vr + (long long)(J + lane) * n;
+        for (int c = J + 1 + wp; c < n; c += kWyRedWarps) {
+          const double v = vrow[c];
+          const double* zr = zs + c * kTC;
+#pragma unroll
+          for (int t = 0; t < kTC; ++t) acc[t] = fma(v, zr[t], acc[t]);
+        }
       }
+#pragma unroll
+      for (int t = 0; t < kTC; ++t) red[wp][lane][t] = acc[t];
     }
-    if (k < kWY) Y[k][t] = acc;
     __syncthreads();
-    if (k < kWY) {
+    if (tid < kWY * kTC) {  // fixed-order fold -> Y (in red[0])
+      const int k = tid / kTC, t = tid % kTC;
+      double y = red[0][k][t];
+#pragma unroll
+      for (int w = 1; w < kWyRedWarps; ++w) y += red[w][k][t];
+      red[0][k][t] = y;
+    }
+    __syncthreads();
+    // (2) Y2 = T_b Y (T from global; 32 x 32, read through L1)
+    if (tid < kWY * kTC) {
+      const int k = tid / kTC, t = tid % kTC;
+      const double* Trow = T + (long long)b * kWY * kWY + k * kWY;
       double a2 = 0.0;
-      for (int q = 0; q < bsb; ++q) a2 = fma(Ts[k][q], Y[q][t], a2);
+      for (int q = 0; q < bsb; ++q) a2 = fma(Trow[q], red[0][q][t], a2);
       Y2[k][t] = a2;
     }
     __syncthreads();
-    for (int c = J + 1 + tid / kTC; c < n; c += 256 / kTC) {
-      double s = zs[c * kTC + t];
-      if (vb) {
-        for (int q = 0; q < bsb; ++q) s = fma(-vb[q * LDV + c], Y2[q][t], s);
-      } else {
-        for (int q = 0; q < bsb; ++q) s = fma(-Vr[(long long)(J + q) * n + c], Y2[q][t], s);
+    // (3) Z rows -= V_b^T-row . Y2
+    for (int c = J + 1 + tid; c < n; c += 256) {
+      double acc[kTC];
+#pragma unroll
+      for (int t = 0; t < kTC; ++t) acc[t] = zs[c * kTC + t];
+      for (int q = 0; q < bsb; ++q) {
+        const double v = vb ? vb[q * LDV + c] : Vr[(long long)(J + q) * n + c];
+#pragma unroll
+        for (int t = 0; t < kTC; ++t) acc[t] = fma(-v, Y2[q][t], acc[t]);
       }
-      zs[c * kTC + t] = s;
+#pragma unroll
+      for (int t = 0; t < kTC; ++t) zs[c * kTC + t] = acc[t];
     }
     __syncthreads();
   }
@@ -598,8 +653,8 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
   if (!attr) {
     LR_CHECK_CUDA(cudaFuncSetAttribute(tridiag_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     LR_CHECK_CUDA(cudaFuncSetAttribute(tridiag_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    LR_CHECK_CUDA(cudaFuncSetAttribute(wy_apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
-    LR_CHECK_CUDA(cudaFuncSetAttribute(wy_apply_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    LR_CHECK_CUDA(cudaFuncSetAttribute(wy_apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 214 * 1024));
+    LR_CHECK_CUDA(cudaFuncSetAttribute(wy_apply_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 214 * 1024));
     attr = true;
   }
   int occ = 0;
@@ -694,16 +749,12 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
     const int nrefl = n - 2;  // reflectors 0 .. n-3
     const int nblk = (nrefl + kWY - 1) / kWY;
     double* Tb = Lm;   // nblk x kWY x kWY (inverse-iteration scratch is free now)
-    double* Yb = U1;   // kWY x n
-    double* Y2 = U2;   // kWY x n
     build_T_kernel<<<nblk, 256, 0, s>>>(Vr, tau, n, nrefl, Tb);
     LR_CHECK_LAUNCH();
-    (void)Yb;
-    (void)Y2;
     const size_t vsm = (size_t)kWY * (n + 1) * sizeof(double);
     if ((size_t)n * 8 * sizeof(double) <= 200 * 1024) {
       const size_t zsm = (size_t)n * 8 * sizeof(double);
-      const int stage = zsm + vsm <= 210 * 1024;
+      const int stage = zsm + vsm <= 214 * 1024;  // + ~10 KB static fits the 227 KB per CTA
       wy_apply_kernel<8><<<(n + 7) / 8, 256, stage ? zsm + vsm : zsm, s>>>(Z, n, Vr, Tb, nrefl, V, ldv, stage);
     } else {
       const size_t zsm = (size_t)n * 2 * sizeof(double);
