@@ -158,20 +158,48 @@ def cpu_oracle_call(obs):
     return time.perf_counter() - t0, res
 
 
+L2_READ_GBS = 18000.0  # tools/l2_bw.cu on this pool's B200 (profiles/r01_l2_bw.txt), for the gather diagnostic
+
+
+def kernel_table(summary, total_ms, steps, hbm_peak, fp64_peak):
+    """Per native call: time per step, share, and the SURVEY 8(d) roofline
+    fraction (HBM on compulsory bytes for the sparse kernels, fp64 tensor for
+    the GEMMs); SpMM also gets its L2-gather rate (8 nnz w bytes)."""
+    from paper_1810_06860_b200 import profiling
+
+    kernels = []
+    for name, d in sorted(summary.items(), key=lambda kv: -kv[1]["ms"]):
+        entry = {"call": name, "calls_per_step": d["calls"] / steps, "ms_per_step": d["ms"] / steps,
+                 "share": d["ms"] / total_ms}
+        if name in profiling.MODELS and d["ms"] > 0:
+            bound = profiling.MODELS[name][0]
+            if bound == "hbm":
+                ach = d["bytes"] / (d["ms"] * 1e-3) / 1e9
+                entry.update(bound="hbm", achieved=ach, unit="GB/s", peak=hbm_peak, frac=ach / hbm_peak)
+                if name == "lr_spmm_f64":
+                    g = (d["flops"] / 2 * 8) / (d["ms"] * 1e-3) / 1e9
+                    entry.update(gather_gbs=g, gather_frac_of_l2_read=g / L2_READ_GBS)
+            else:
+                ach = d["flops"] / (d["ms"] * 1e-3) / 1e12
+                entry.update(bound="tensor", achieved=ach, unit="TFLOP/s", peak=fp64_peak, frac=ach / fp64_peak)
+        kernels.append(entry)
+    return kernels
+
+
 SVT_CFG4_NOTE = ("cfg4 rating shape (138493x26744, 18,000,237 train): the reference defaults (tau=5n, "
                  "delta=1.2mn/nnz) diverge on Zipf-sampled ratings -- ranks escalate past the 2000 dense cap and "
                  "BOTH implementations raise SizeCapError -- so the throughput run uses tau=5n/40, delta=1, "
                  "reuse-q (i_reuse=5, q_reuse=10), a fixed 20 iterations (rank grows 6 -> ~48)")
 
 
-def bench_svt(cpu: bool):
+def bench_svt(cpu: bool, peaks=None):
     """SVT iterations/s: cfg1 (BASELINE configs[0], defaults and eps=1e-3) and
     the cfg4 rating shape (fixed 20 iterations), GPU loop time from the trace
     (setup excluded), CPU oracle beside it."""
     import torch
 
     import oracle
-    from paper_1810_06860_b200 import completion, workloads
+    from paper_1810_06860_b200 import _native, completion, profiling, workloads
     from paper_1810_06860_b200.sparse import ObservationSet
 
     out = {}
@@ -211,6 +239,14 @@ def bench_svt(cpu: bool):
     d = {"iterations": res.iterations, "iterations_per_s": res.iterations / loop, "loop_s": loop, "total_s": total,
          "residual": res.residual, "rank": res.rank, "ks": [t.k for t in res.trace],
          "heldout_mae": completion.mae(res.predict(rt, ct), vt), "note": SVT_CFG4_NOTE}
+    if peaks is not None:  # kernel breakdown from a second, profiled run (events around every native call)
+        prof = profiling.Profiler()
+        _native.PROFILER = prof
+        res_p = completion.svt_fast(obs4, prm)
+        torch.cuda.synchronize()
+        _native.PROFILER = None
+        loop_p = sum(t.wall_time for t in res_p.trace) * 1e3
+        d["kernels_profiled_run"] = kernel_table(prof.summary(), loop_p, res_p.iterations, *peaks)
     if cpu:
         r, c, v = obs4.subset(0)
         n_cpu = 2
@@ -389,20 +425,7 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     fp64_peak = fp64_peak_tflops()
 
-    kernels = []
-    for name, d in sorted(summary.items(), key=lambda kv: -kv[1]["ms"]):
-        entry = {"call": name, "calls_per_step": d["calls"] / args.steps, "ms_per_step": d["ms"] / args.steps,
-                 "share": d["ms"] / ms}
-        if name in profiling.MODELS and d["ms"] > 0:
-            bound = profiling.MODELS[name][0]
-            if bound == "hbm":
-                ach = d["bytes"] / (d["ms"] * 1e-3) / 1e9
-                entry.update(bound="hbm", achieved=ach, unit="GB/s", peak=hbm_peak, frac=ach / hbm_peak,
-                             gather_gbs=(d["flops"] / 2 * 8) / (d["ms"] * 1e-3) / 1e9)
-            else:
-                ach = d["flops"] / (d["ms"] * 1e-3) / 1e12
-                entry.update(bound="tensor", achieved=ach, unit="TFLOP/s", peak=fp64_peak, frac=ach / fp64_peak)
-        kernels.append(entry)
+    kernels = kernel_table(summary, ms, args.steps, hbm_peak, fp64_peak)
     dominant = next((k for k in kernels if "bound" in k), None)
     roofline = None
     if dominant:
@@ -413,7 +436,8 @@ def main():
                                     else "fp64 cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json "
                                          "has no fp64 figure)")}
 
-    svt = bench_svt(cpu=args.cpu_baseline == "full" and ws == 1) if args.svt == "on" else None
+    svt = bench_svt(cpu=args.cpu_baseline == "full" and ws == 1, peaks=(hbm_peak, fp64_peak)) \
+        if args.svt == "on" else None
 
     cpu = None
     if args.cpu_baseline == "full" and ws == 1:
