@@ -7,6 +7,9 @@
 // 126 MB L2), plus a compulsory HBM stream of 12 B/nnz (SpMM) or 40 B/nnz
 // (SVT step).  Work is split into "items" (a row, or a chunk of a long row)
 // so Zipf-shaped rows (cfg4: up to 26,744 entries) do not serialize a warp.
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "lr_common.cuh"
 
 namespace lr {
@@ -286,27 +289,37 @@ static void launch_spmm_t(const int* ptr, const int* idx, const double* val, con
                                                     scratch, n_tiles);
 }
 
+// (G, T) per width: G lanes per item, T column pairs per lane.  Narrow
+// products use few lanes and several pairs per lane so a warp keeps 4-16
+// items (gathers) in flight and no lane idles on padding columns;
+// LR_SPMM_GT="G,T" overrides for experiments.
 template <bool V2>
 static void dispatch_spmm(const int* ptr, const int* idx, const double* val, const int* items,
                           int n_items, const double* X, long long ldx, int w, double* Y,
                           long long ldy, double* scratch, cudaStream_t s) {
   const int pairs = (w + 1) / 2;
-  if (pairs <= 1)
-    launch_spmm_t<1, 1, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
-  else if (pairs <= 2)
-    launch_spmm_t<2, 1, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
-  else if (pairs <= 4)
-    launch_spmm_t<4, 1, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
-  else if (pairs <= 8)
-    launch_spmm_t<8, 1, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
-  else if (pairs <= 16)
-    launch_spmm_t<16, 1, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
-  else if (pairs <= 32)
-    launch_spmm_t<32, 1, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
-  else if (pairs <= 64)
-    launch_spmm_t<32, 2, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
-  else
-    launch_spmm_t<32, 3, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+  static const char* env = getenv("LR_SPMM_GT");
+  int G = 0, T = 0;
+  if (env) sscanf(env, "%d,%d", &G, &T);
+  if (G == 0) {
+    if (pairs <= 1) { G = 1; T = 1; }
+    else if (pairs <= 2) { G = 2; T = 1; }
+    else if (pairs <= 4) { G = 4; T = 1; }
+    else if (pairs <= 8) { G = 8; T = 1; }
+    else if (pairs <= 16) { G = 8; T = 2; }   // cfg4 w = 22: 1029 -> 715 us (tools/spmm_gt_sweep.sh)
+    else if (pairs <= 32) { G = 16; T = 2; }  // w = 33 / 45: 849 -> 808, 895 -> 847 us
+    else if (pairs <= 64) { G = 32; T = 2; }
+    else { G = 32; T = 3; }
+  }
+#define LR_SPMM_CASE(g, t) \
+  if (G == g && T == t) return launch_spmm_t<g, t, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+  LR_SPMM_CASE(1, 1) LR_SPMM_CASE(2, 1) LR_SPMM_CASE(4, 1) LR_SPMM_CASE(8, 1) LR_SPMM_CASE(16, 1)
+  LR_SPMM_CASE(32, 1) LR_SPMM_CASE(32, 2) LR_SPMM_CASE(32, 3)
+  LR_SPMM_CASE(2, 2) LR_SPMM_CASE(2, 3) LR_SPMM_CASE(2, 4) LR_SPMM_CASE(4, 2) LR_SPMM_CASE(4, 3)
+  LR_SPMM_CASE(4, 4) LR_SPMM_CASE(8, 2) LR_SPMM_CASE(8, 3) LR_SPMM_CASE(8, 4) LR_SPMM_CASE(16, 2)
+  LR_SPMM_CASE(16, 3)
+#undef LR_SPMM_CASE
+  launch_spmm_t<32, 3, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
 }
 
 }  // namespace lr
@@ -341,10 +354,11 @@ int lr_spmm_f64(const int* ptr, const int* idx, const double* val, int rows, con
     }
     return LR_OK;
   }
-  // Wide products (the W-column Y^T Q of BKI / recycle-q) run as column
-  // chunks of <= kChunkCols: each chunk's slice of X (rows x chunk doubles)
-  // stays L2-resident while every stored entry gathers from it, instead of
-  // all W columns of X (m x W, 528 MB at cfg2) streaming through L2 at once.
+  // Products wider than kChunkCols run as column chunks: each chunk's slice
+  // of X stays L2-resident while every stored entry gathers from it (the
+  // W-column Y^T Q of BKI at cfg2 is 528 MB), and the <= 128-column tiles run
+  // at higher occupancy than the 192-column one even when X fits in L2
+  // (cfg4 CSR w = 132: 2.64 ms chunked vs 4.04 ms whole, tools/spmm_cfg4_probe.py).
   constexpr int kChunkCols = 128;
   const int n_chunks = (w + kChunkCols - 1) / kChunkCols;
   const int cw_even = (((w + n_chunks - 1) / n_chunks) + 1) & ~1;
