@@ -263,6 +263,118 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
   if (cta == 0 && tid == 0) p.status[0] = -1.0;
 }
 
+// ---------------------------------------------------------------------------
+// Small blocks (the whole m x n block fits one CTA's shared memory: cfg1 /
+// the SVT loop's 1000 x 16 Krylov blocks): one CTA, no grid barrier.  Same
+// pivot rule (largest |x| among rows not yet pivoted, ties -> smallest row),
+// same reciprocal scaling, same P^T L output and status codes as lu_kernel.
+constexpr int LUS_THREADS = 1024;
+
+__global__ void __launch_bounds__(LUS_THREADS) lu_small_kernel(double* X, long long ldx, int m, int n,
+                                                              double* status) {
+  extern __shared__ double lus[];
+  const int LD = n + 1;
+  double* P = lus;                                        // m x LD
+  int* pivflag = reinterpret_cast<int*>(P + (long long)m * LD);  // m
+  __shared__ double rv[LUS_THREADS / 32];
+  __shared__ int rr[LUS_THREADS / 32];
+  __shared__ double s_v, s_rpiv;
+  __shared__ int s_r, s_bad;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double mx = 0.0;
+  int nonfin = 0;
+  for (int e = tid; e < m * n; e += LUS_THREADS) {
+    const int i = e / n, c = e - (e / n) * n;
+    const double x = X[(long long)i * ldx + c];
+    P[i * LD + c] = x;
+    if (!isfinite(x)) nonfin = 1;
+    mx = fmax(mx, fabs(x));
+  }
+  for (int i = tid; i < m; i += LUS_THREADS) pivflag[i] = -1;
+  mx = block_max<LUS_THREADS>(mx, rv);
+  nonfin = __syncthreads_or(nonfin);
+  if (tid == 0) s_v = mx;
+  __syncthreads();
+  const double maxabs = s_v;
+  if (nonfin || maxabs == 0.0) {
+    if (tid == 0) status[0] = nonfin ? -3.0 : -2.0;
+    return;
+  }
+  const double tol = 1e-14 * maxabs;
+  // candidate for column 0; later columns get theirs from the fused update pass
+  double bv = -1.0;
+  int br = 0x7fffffff;
+  for (int i = tid; i < m; i += LUS_THREADS) better(bv, br, fabs(P[i * LD]), i);
+  for (int j = 0; j < n; ++j) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int r2 = __shfl_xor_sync(0xffffffffu, br, o);
+      better(bv, br, v2, r2);
+    }
+    if (lane == 0) {
+      rv[wid] = bv;
+      rr[wid] = br;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      double v = lane < LUS_THREADS / 32 ? rv[lane] : -1.0;
+      int r = lane < LUS_THREADS / 32 ? rr[lane] : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        const int r2 = __shfl_xor_sync(0xffffffffu, r, o);
+        better(v, r, v2, r2);
+      }
+      if (lane == 0) {
+        s_v = v;
+        s_r = r;
+        s_bad = !(v >= tol) || v == 0.0;
+        if (!s_bad) {
+          pivflag[r] = j;
+          s_rpiv = 1.0 / P[r * LD + j];  // LAPACK dgetf2: scale by 1/pivot
+        }
+      }
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (tid == 0) {
+        status[0] = (double)j;
+        status[1] = s_v;
+        status[2] = tol;
+      }
+      return;
+    }
+    const double* up = P + s_r * LD;  // the pivot row (never modified again)
+    const double rpiv = s_rpiv;
+    // one pass per row: multiplier, trailing update, next column's candidate
+    bv = -1.0;
+    br = 0x7fffffff;
+    for (int i = tid; i < m; i += LUS_THREADS) {
+      if (pivflag[i] >= 0) continue;
+      double* row = P + i * LD;
+      const double l = row[j] * rpiv;
+      row[j] = l;
+      for (int c = j + 1; c < n; ++c) row[c] = fma(-l, up[c], row[c]);
+      if (j + 1 < n) better(bv, br, fabs(row[j + 1]), i);
+    }
+  }
+  // pivot rows: unit entry at their step, zeros to the right; write back
+  for (int e = tid; e < m * n; e += LUS_THREADS) {
+    const int i = e / n, c = e - (e / n) * n;
+    const int pj = pivflag[i];
+    double x = P[i * LD + c];
+    if (pj >= 0 && c >= pj) x = (c == pj) ? 1.0 : 0.0;
+    X[(long long)i * ldx + c] = x;
+  }
+  if (tid == 0) status[0] = -1.0;
+}
+
+static size_t lu_small_smem(int m, int n) {
+  return (size_t)m * (n + 1) * sizeof(double) + (size_t)m * sizeof(int) + 16;
+}
+constexpr size_t kLuSmallMaxSmem = 200 * 1024;
+
 struct LuPlan {
   int G, nb, rows_per;
   size_t smem;
@@ -319,6 +431,25 @@ int lr_lu_pl_f64(int m, int n, double* X, long long ldx, double* work, double* s
   LR_REQUIRE(m >= n && n >= 1, "lu_pl requires m >= n, got %dx%d", m, n);
   LR_REQUIRE(ldx >= n, "lu_pl: ldx < n");
   cudaStream_t s = as_stream(stream);
+  static const bool no_small = getenv("LR_LU_NO_SMALL") != nullptr;
+  if (!no_small && lu_small_smem(m, n) <= kLuSmallMaxSmem) {
+    static bool attr_small = false;
+    if (!attr_small) {
+      LR_CHECK_CUDA(cudaFuncSetAttribute(lu_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kLuSmallMaxSmem));
+      attr_small = true;
+    }
+    double* status = work;
+    lu_small_kernel<<<1, LUS_THREADS, lu_small_smem(m, n), s>>>(X, ldx, m, n, status);
+    LR_CHECK_LAUNCH();
+    double host[4];
+    LR_CHECK_CUDA(cudaMemcpyAsync(host, status, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    LR_CHECK_CUDA(cudaStreamSynchronize(s));
+    status_host[0] = host[0];
+    status_host[1] = host[1];
+    status_host[2] = host[2];
+    return LR_OK;
+  }
   LuPlan pl = lu_plan(m, n);
   LR_REQUIRE(pl.G > 0, "lu_pl: %d rows do not fit the cooperative plan", m);
   const long long G = pl.G;
