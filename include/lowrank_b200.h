@@ -85,6 +85,16 @@ int lr_pattern_axpy_f64(double* y_csr, double* y_csc, const int* inv_perm, const
 /* dst[t] = src[perm[t]] : builds/refreshes the CSC value copy. */
 int lr_gather_f64(const double* src, const int* perm, double* dst, long long n, void* stream);
 
+/* CSR -> CSC transpose index of a pattern on the device (the reference's
+ * SparseMatrix._transpose_index, sparse.py:129-139: stable argsort of the
+ * column indices): t_ptr (n+1), t_idx = CSR row of each CSC slot (nnz),
+ * perm = CSR slot of each CSC slot, inv_perm = its inverse.  Bit-exact with a
+ * stable host argsort.  work: lr_csr_transpose_workspace_ints(m, n) ints. */
+long long lr_csr_transpose_workspace_ints(int m, int n);
+int lr_csr_transpose_i32(int m, int n, long long nnz, const int* ptr, const int* idx, int* t_ptr,
+                         int* t_idx, int* perm, int* inv_perm, int* work, long long work_ints,
+                         void* stream);
+
 /* ----------------------------------------------------------- reductions */
 /* out[0] = sum x^2, out[1] = max |x|, out[2] = #non-finite  over an
  * rows x cols block (ld); deterministic fixed-order tree.  Backs

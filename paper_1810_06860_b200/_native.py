@@ -32,6 +32,8 @@ SIGNATURES = {
     "lr_sm_count": (_I, []),
     "lr_launch_count": (_LL, []),
     "lr_spmm_f64": (_I, [_P, _P, _P, _I, _P, _I, _P, _I, _P, _LL, _I, _P, _LL, _P, _P]),
+    "lr_csr_transpose_workspace_ints": (_LL, [_I, _I]),
+    "lr_csr_transpose_i32": (_I, [_I, _I, _LL, _P, _P, _P, _P, _P, _P, _P, _LL, _P]),
     "lr_sddmm_f64": (_I, [_P, _P, _I, _P, _I, _P, _LL, _P, _P, _LL, _I, _P, _P]),
     "lr_svt_step_f64": (_I, [_P, _P, _I, _P, _I, _P, _LL, _P, _P, _LL, _I, _P, _P, _P, _P, _D, _I,
                              _P, _I, _P, _P]),

@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(LUS_THREADS) lu_small_kernel(double* X, long l
       if (j + 1 < n) better(bv, br, fabs(row[j + 1]), i);
     }
   }
+  __syncthreads();  // the last pass's rows are read by other threads below
   // pivot rows: unit entry at their step, zeros to the right; write back
   for (int e = tid; e < m * n; e += LUS_THREADS) {
     const int i = e / n, c = e - (e / n) * n;

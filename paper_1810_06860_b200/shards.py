@@ -382,7 +382,8 @@ class ShardedEngine:
         key = (self.world, self.rank)
         st = cache.get(key) if cache is not None else None
         if st is None:
-            _, t_indptr, _ = phi._transpose_index()
+            t_indptr = np.zeros(self.n + 1, dtype=np.int64)  # CSC offsets only (no host argsort)
+            np.cumsum(np.bincount(phi.indices, minlength=self.n), out=t_indptr[1:])
             plan = ShardPlan(phi.indptr, t_indptr, self.world)
             r0, r1 = plan.rows(self.rank)
             c0, c1 = plan.cols(self.rank)

@@ -79,48 +79,73 @@ class _HostSide:
 class _Side:
     """One compressed orientation of the pattern on the device."""
 
-    def __init__(self, hs: _HostSide):
-        self.rows = hs.rows
-        self.ptr = device.int_buffer(hs.ptr)
-        self.idx = device.int_buffer(hs.idx)
-        self.items = None if hs.items is None else device.int_buffer(hs.items)
-        self.splits = None if hs.splits is None else device.int_buffer(hs.splits)
-        self.n_items, self.n_splits, self.n_slots = hs.n_items, hs.n_splits, hs.n_slots
+    def __init__(self, hs: _HostSide = None, *, rows=None, ptr=None, idx=None, sched=None):
+        if hs is not None:
+            self.rows = hs.rows
+            self.ptr = device.int_buffer(hs.ptr)
+            self.idx = device.int_buffer(hs.idx)
+            items, splits = hs.items, hs.splits
+            self.n_items, self.n_splits, self.n_slots = hs.n_items, hs.n_splits, hs.n_slots
+        else:  # built on the device; only the work schedule comes from the host
+            self.rows, self.ptr, self.idx = rows, ptr, idx
+            items, splits, n_slots = sched
+            self.n_items = rows if items is None else int(items.shape[0])
+            self.n_splits = 0 if splits is None else int(splits.shape[0])
+            self.n_slots = n_slots
+            items = None if items is None else items.ravel()
+            splits = None if splits is None else splits.ravel()
+        self.items = None if items is None else device.int_buffer(items)
+        self.splits = None if splits is None else device.int_buffer(splits)
 
 
 class _HostPrep:
+    """Host side of a pattern's upload: the CSR arrays as int32 and their
+    work schedule (built once per pattern; pinned by SparseMatrix.pin_memory).
+    The CSC side is derived on the device (lr_csr_transpose_i32)."""
+
     def pin(self) -> None:
         """Move every upload source into page-locked memory."""
-        for side in (self.csr, self.csc):
-            for name in ("ptr", "idx", "items", "splits"):
-                a = getattr(side, name)
-                if a is not None:
-                    setattr(side, name, device.pinned_copy(a))
-        self.perm = device.pinned_copy(self.perm)
-        self.inv_perm = device.pinned_copy(self.inv_perm)
+        for name in ("ptr", "idx", "items", "splits"):
+            a = getattr(self.csr, name)
+            if a is not None:
+                setattr(self.csr, name, device.pinned_copy(a))
 
     def __init__(self, A: "SparseMatrix"):
-        perm, t_indptr, t_indices = A._transpose_index()
-        inv = np.empty(A.nnz, dtype=np.int32)
-        inv[perm] = np.arange(A.nnz, dtype=np.int32)
         self.csr = _HostSide(A.indptr, A.indices, A.rows)
-        self.csc = _HostSide(t_indptr, t_indices, A.cols)
-        self.perm = np.ascontiguousarray(perm, dtype=np.int32)
-        self.inv_perm = inv
+
+
+def _device_transpose(csr: _Side, m: int, n: int, nnz: int):
+    """CSC structure (t_ptr, t_idx, perm, inv_perm) of a device CSR pattern,
+    bit-exact with the host's stable argsort (sparse.py:129-139)."""
+    import torch
+
+    dev = device.require_cuda()
+    i32 = torch.int32
+    t_ptr = torch.empty(n + 1, dtype=i32, device=dev)
+    t_idx = torch.empty(max(nnz, 1), dtype=i32, device=dev)
+    perm = torch.empty(max(nnz, 1), dtype=i32, device=dev)
+    inv = torch.empty(max(nnz, 1), dtype=i32, device=dev)
+    ws = int(_native.load().lr_csr_transpose_workspace_ints(m, n))
+    work = torch.empty(ws, dtype=i32, device=dev)
+    _native.call("lr_csr_transpose_i32", m, n, nnz, device.ptr(csr.ptr), device.ptr(csr.idx), device.ptr(t_ptr),
+                 device.ptr(t_idx), device.ptr(perm), device.ptr(inv), device.ptr(work), ws, device.stream())
+    return t_ptr, t_idx, perm, inv
 
 
 class DevicePattern:
     """CSR + CSC structure of one pattern on the device (shared by every
-    matrix with that pattern, e.g. Y and P_Phi(M) in the SVT loop)."""
+    matrix with that pattern, e.g. Y and P_Phi(M) in the SVT loop).  Only the
+    CSR arrays are uploaded; the transpose index is built on the device and
+    just the n+1 CSC offsets come back for the host-side work schedule."""
 
     def __init__(self, A: "SparseMatrix"):
         self.shape = (A.rows, A.cols)
         self.nnz = A.nnz
         hp = A._host_prep()
         self.csr = _Side(hp.csr)
-        self.csc = _Side(hp.csc)
-        self.perm = device.int_buffer(hp.perm)
-        self.inv_perm = device.int_buffer(hp.inv_perm)
+        t_ptr, t_idx, self.perm, self.inv_perm = _device_transpose(self.csr, A.rows, A.cols, A.nnz)
+        t_ptr_host = device.to_host(t_ptr).astype(np.int64)
+        self.csc = _Side(rows=A.cols, ptr=t_ptr, idx=t_idx, sched=_schedule(t_ptr_host))
 
     def values(self, host_vals: np.ndarray):
         """(csr, csc) device value copies of host values in CSR order."""
@@ -130,7 +155,6 @@ class DevicePattern:
             _native.call("lr_gather_f64", device.ptr(vc), device.ptr(self.perm), device.ptr(vt),
                          self.nnz, device.stream())
         return vc, vt
-
 
 class SparseMatrix:
     """CSR matrix with an immutable pattern (sparse.py:28-150 contract).

@@ -327,3 +327,41 @@ def test_device_gaussian_matches_host():
         dev = device.to_host(gaussian_matrix_device(seed, rows, cols))
         # uniform words are bit-exact; log/sincos differ by a few ulp
         np.testing.assert_allclose(dev, host, rtol=4e-15, atol=4e-15)
+
+
+def _patterns():
+    rng = np.random.default_rng(11)
+    yield "uniform", 3000, 2000, rng.choice(3000 * 2000, 40000, replace=False)
+    yield "tiny", 1, 1, np.array([0])
+    yield "empty rows/cols", 500, 700, rng.choice(250 * 700, 3000, replace=False) * 2 % (500 * 700)
+    # long rows (> SPLIT_CHUNK) and a dense column
+    rows = np.r_[np.full(1500, 7), np.arange(0, 900, 1), rng.integers(0, 900, 4000)]
+    cols = np.r_[np.arange(1500), np.full(900, 3), rng.integers(0, 1600, 4000)]
+    yield "long rows", 900, 1600, np.unique(rows * 1600 + cols)
+    # Zipf-ish columns
+    z = np.minimum(rng.zipf(1.3, 60000), 5000) - 1
+    r = rng.integers(0, 20000, 60000)
+    yield "zipf cols", 20000, 5000, np.unique(r * 5000 + z)
+
+
+@pytest.mark.parametrize("case", list(range(5)))
+def test_device_transpose_matches_host_stable_argsort(case):
+    """The CSC built on the device (lr_csr_transpose_i32) is bit-identical to
+    the reference's host transpose index (stable argsort, sparse.py:129-139)."""
+    from paper_1810_06860_b200 import device
+    from paper_1810_06860_b200.sparse import SparseMatrix
+
+    name, m, n, flat = list(_patterns())[case]
+    flat = np.asarray(flat, dtype=np.int64)
+    i, j = np.divmod(flat, n)
+    A = SparseMatrix.from_coo(m, n, i, j, np.arange(flat.size, dtype=np.float64) + 0.5)
+    dp = A.pattern()
+    perm, t_ptr, t_idx = A._transpose_index()
+    assert np.array_equal(device.to_host(dp.csc.ptr), t_ptr), name
+    assert np.array_equal(device.to_host(dp.csc.idx)[:A.nnz], t_idx), name
+    assert np.array_equal(device.to_host(dp.perm)[:A.nnz], perm), name
+    inv = np.empty(A.nnz, dtype=np.int64)
+    inv[perm] = np.arange(A.nnz)
+    assert np.array_equal(device.to_host(dp.inv_perm)[:A.nnz], inv), name
+    vc, vt = A.device_values()
+    assert np.array_equal(device.to_host(vt)[:A.nnz], A.data[perm]), name
