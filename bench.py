@@ -225,6 +225,21 @@ def bench_svt(cpu: bool, peaks=None):
             d["parity"] = {"same_iterations": ref.iterations == res.iterations,
                            "residual_abs_diff": abs(ref.residual - res.residual)}
         out[name] = d
+    # cfg3 (image shape, SURVEY 8(d) recorded variant): k escalates to 316 in the first iteration
+    o3, _ = workloads.cfg3()
+    obs3 = ObservationSet(o3.m, o3.n, o3.rows, o3.cols, o3.values)
+    prm3 = completion.SvtParams(strategy="reuse-u", i_reuse=100, q_reuse=10, seed=0, epsilon=0.05)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res3 = completion.svt_fast(obs3, prm3)
+    torch.cuda.synchronize()
+    total3 = time.perf_counter() - t0
+    loop3 = sum(t.wall_time for t in res3.trace)
+    out["cfg3_reuse_u"] = {"iterations": res3.iterations, "iterations_per_s": res3.iterations / loop3,
+                           "loop_s": loop3, "total_s": total3, "residual": res3.residual, "rank": res3.rank,
+                           "ks": [t.k for t in res3.trace],
+                           "cpu_note": "CPU oracle, same run on this pool: 3 iterations in 93.2 s, residual "
+                                       "equal to 7e-14 (profiles/r01_cfg3_svt.txt); not re-run by default"}
     o4 = workloads.cfg4()
     obs4 = ObservationSet(o4.m, o4.n, o4.rows, o4.cols, o4.values, o4.split)
     prm = completion.SvtParams(epsilon=0.17, i_reuse=5, q_reuse=10, strategy="reuse-q", seed=0, i_max=20,

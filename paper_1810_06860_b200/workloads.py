@@ -9,9 +9,9 @@ the CSR/CSC patterns are bit-identical for every implementation.
 cfg1  1000x1000, rank-10 N(0,1) factors, 200,000 observed uniformly (seed 0)
 cfg2  100000x50000, 5,000,000 uniform positions, N(0,1) values (seed 1)
 cfg3  2048x2048 image shape, 50% observed.  BASELINE's wording is
-      underspecified; recorded variant: 128 + G1 diag(255*0.9^i)
-      G2^T / sqrt(50) with G1, G2 iid N(0,1) (rank 50) + N(0,1) noise,
-      clipped to [0, 255]                                   (seed 3)
+      underspecified; recorded variant: 128 + U diag(255*0.9^i)
+      V^T with orthonormal rank-50 U, V + N(0,1) noise, clipped to [0, 255]
+                                                            (seed 3)
 cfg4  138493x26744, 20,000,263 ratings: row counts Zipf(1.0) floor 20 capped
       at n; columns weighted Zipf(0.9) without replacement per row
       (exponential races for heavy rows, oversampled i.i.d. draws + dedup
@@ -76,11 +76,16 @@ def cfg2(seed=1, m=100_000, n=50_000, nnz=5_000_000):
 
 
 def cfg3(seed=3, m=2048, n=2048, rank=50, density=0.5):
+    """SURVEY.md 8(d)'s recorded variant: orthonormal rank-50 factors (QR of
+    Gaussians) with singular values 255 * 0.9^i, + N(0,1) noise, a +128 gray
+    offset, clipped to [0, 255].  (Without the offset half the entries clip to
+    0 and SVT stalls; with it k escalates to ~316 in the first iteration,
+    W ~ 1284, and the loop converges in a few iterations.)"""
     rng = np.random.default_rng(seed)
     sig = 255.0 * 0.9 ** np.arange(rank)
-    G1 = rng.standard_normal((m, rank))
-    G2 = rng.standard_normal((n, rank))
-    X = 128.0 + (G1 * sig) @ G2.T / np.sqrt(rank) + rng.standard_normal((m, n))
+    U, _ = np.linalg.qr(rng.standard_normal((m, rank)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, rank)))
+    X = 128.0 + (U * sig) @ V.T + rng.standard_normal((m, n))
     X = np.clip(X, 0.0, 255.0)
     flat = rng.choice(m * n, size=int(density * m * n), replace=False).astype(np.int64)
     i, j = np.divmod(flat, n)
