@@ -300,50 +300,40 @@ __global__ void inviter_kernel(const double* __restrict__ d, const double* __res
   const double tiny = fmax(2.220446049250313e-16 * tnorm, 1e-300);
 #define IX(i) ((long long)(i) * n + k)
   // LU with partial pivoting of T - lam I (dlagtf): U = diag Dg, super U1, 2nd super U2
+  // Branch-free (lanes hold different shifts, so a branch would run both
+  // sides): one reciprocal per step on the recurrence; Dg keeps the clamped
+  // reciprocal pivot for the back substitutions.
+  auto clamp_rcp = [&](double dg) {
+    if (fabs(dg) < tiny) dg = (dg < 0.0) ? -tiny : tiny;
+    return 1.0 / dg;
+  };
   double a = d[0] - lam;
   double b = n > 1 ? e[0] : 0.0;
   for (int i = 0; i < n - 1; ++i) {
     const double c = e[i];
     const double a_next = d[i + 1] - lam;
     const double b_next = (i + 2 < n) ? e[i + 1] : 0.0;
-    if (fabs(a) >= fabs(c)) {
-      const double piv = (a == 0.0) ? tiny : a;
-      const double l = c / piv;
-      Dg[IX(i)] = piv;  // replaced by its clamped reciprocal below (off the recurrence)
-      U1[IX(i)] = b;
-      U2[IX(i)] = 0.0;
-      Lm[IX(i)] = l;
-      Pv[IX(i)] = 0;
-      a = a_next - l * b;
-      b = b_next;
-    } else {
-      const double l = a / c;
-      Dg[IX(i)] = c;
-      U1[IX(i)] = a_next;
-      U2[IX(i)] = b_next;
-      Lm[IX(i)] = l;
-      Pv[IX(i)] = 1;
-      a = b - l * a_next;
-      b = -l * b_next;
-    }
+    const bool keep = fabs(a) >= fabs(c);  // no interchange
+    const double piv = keep ? ((a == 0.0) ? tiny : a) : c;
+    const double rp = 1.0 / piv;
+    const double l = (keep ? c : a) * rp;
+    Dg[IX(i)] = (fabs(piv) < tiny) ? clamp_rcp(piv) : rp;
+    U1[IX(i)] = keep ? b : a_next;
+    U2[IX(i)] = keep ? 0.0 : b_next;
+    Lm[IX(i)] = l;
+    Pv[IX(i)] = keep ? 0 : 1;
+    const double a2 = keep ? a_next - l * b : b - l * a_next;
+    b = keep ? b_next : -l * b_next;
+    a = a2;
   }
-  Dg[IX(n - 1)] = (a == 0.0) ? tiny : a;
-  // reciprocal diagonal (clamped away from zero like the solve below would):
-  // independent per i, so the back substitutions carry FMAs only instead of a
-  // 125-cycle division per step (tools/dp_latency.cu)
-#pragma unroll 4
-  for (int i = 0; i < n; ++i) {
-    double dg = Dg[IX(i)];
-    if (fabs(dg) < tiny) dg = (dg < 0.0) ? -tiny : tiny;
-    Dg[IX(i)] = 1.0 / dg;
-  }
+  Dg[IX(n - 1)] = clamp_rcp((a == 0.0) ? tiny : a);
   unsigned long long s = 0x9E3779B97F4A7C15ULL * (unsigned long long)(k + 1);
   double scale = 1.0;
   // two solves: the shift is accurate to ~1e-3 eps ||T|| (bisection), so the
   // first solve already amplifies the wanted direction by ~1/(eps*||T||).
   // The recurrences are branch-free and their operands are fetched 8 steps
   // at a time, so the L2 latency is paid once per 8 steps, not per step.
-  constexpr int PF = 8;
+  constexpr int PF = 16;
   for (int it = 0; it < 2; ++it) {
     // forward: z <- L^{-1} P (scale * z); the start vector is generated in pass 0
     double zc;
@@ -409,14 +399,18 @@ __global__ void inviter_kernel(const double* __restrict__ d, const double* __res
     }
     scale = (mx > 0.0) ? 1.0 / mx : 1.0;
   }
-  double ss = 0.0;
-#pragma unroll 8
+  double ss = 0.0, ss1 = 0.0;
+#pragma unroll 16
   for (int i = 0; i < n; ++i) {
     const double z = Z[IX(i)] * scale;
-    ss = fma(z, z, ss);
+    if (i & 1)
+      ss1 = fma(z, z, ss1);
+    else
+      ss = fma(z, z, ss);
   }
+  ss += ss1;
   const double inv = scale / sqrt(ss);
-#pragma unroll 8
+#pragma unroll 16
   for (int i = 0; i < n; ++i) Z[IX(i)] *= inv;
 #undef IX
 }
