@@ -228,3 +228,30 @@ def test_svt_errors_and_flags():
     obs = ObservationSet(30, 25, i, j, M.ravel())
     res = completion.svt_reference(obs, completion.SvtParams(tau=1e-9, epsilon=0.9, i_max=3, seed=9), backend="oracle")
     assert res.hard_stops >= 1 and any("min(m, n)" in e for e in res.events)
+
+
+def test_svt_cfg3_matches_reference():
+    """cfg3 (image shape, SURVEY 8(d) recorded variant): the reference's own
+    svt_fast(reuse-u) trace (tests/golden/make_golden_cfg3.py) -- k escalates
+    to 316 in the first iteration (W = 1284 eigensolver, 2048 x 1284 GEPP)."""
+    import os
+
+    from paper_1810_06860_b200 import completion, workloads
+    from paper_1810_06860_b200.sparse import ObservationSet
+
+    g = dict(np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_golden_cfg3.npz")))
+    o, _ = workloads.cfg3()
+    ob = ObservationSet(o.m, o.n, o.rows, o.cols, o.values)
+    got = completion.svt_fast(ob, completion.SvtParams(strategy="reuse-u", i_reuse=100, q_reuse=10, seed=0,
+                                                       epsilon=0.05))
+    tr = got.trace
+    assert [t.k for t in tr] == list(g["k"])
+    assert [t.r for t in tr] == list(g["r"])
+    assert [t.p for t in tr] == list(g["p"])
+    assert [t.q for t in tr] == list(g["q"])
+    assert [t.svd_source for t in tr] == list(g["source"])
+    np.testing.assert_allclose([t.residual for t in tr], g["residual"], rtol=1e-8)
+    np.testing.assert_allclose(got.S, g["S"], rtol=1e-10)
+    assert got.converged == bool(g["converged"])
+    pred = got.predict(g["pred_rows"], g["pred_cols"])
+    np.testing.assert_allclose(pred, g["pred"], rtol=1e-8, atol=1e-8 * np.abs(g["pred"]).max())
