@@ -40,7 +40,9 @@ __device__ __forceinline__ Item load_item(const int* __restrict__ items, const i
 // A group of G lanes owns one item; lane g covers column pairs
 // c = 2*(g + G*t), t < T, of a column tile of width 2*G*T starting at c0.
 // VEC2: double2 loads/stores (requires 16B-aligned rows); tail columns scalar.
-template <int G, int T, bool VEC2>
+// Q: stored entries per lane kept in flight (4; 8 for one-pair-per-lane
+// narrow products, whose gathers are too small to cover the L2 latency)
+template <int G, int T, bool VEC2, int Q = 4>
 #ifndef LR_SPMM_MINB
 #define LR_SPMM_MINB 4
 #endif
@@ -73,18 +75,18 @@ __global__ void __launch_bounds__(256, LR_SPMM_MINB) spmm_kernel(const int* __re
 
     if (active) {
       int e = it.beg;
-      // process 4 entries per step for memory-level parallelism
-      for (; e + 4 <= it.end; e += 4) {
-        int cj[4];
-        double vj[4];
+      // process Q entries per step for memory-level parallelism
+      for (; e + Q <= it.end; e += Q) {
+        int cj[Q];
+        double vj[Q];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < Q; ++q) {
           cj[q] = __ldg(idx + e + q);
           vj[q] = __ldg(val + e + q);
         }
-        double2 xv[4][T];
+        double2 xv[Q][T];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < Q; ++q) {
           const double* xr = X + (long long)cj[q] * ldx + c0;
 #pragma unroll
           for (int t = 0; t < T; ++t) {
@@ -98,7 +100,7 @@ __global__ void __launch_bounds__(256, LR_SPMM_MINB) spmm_kernel(const int* __re
           }
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < Q; ++q)
 #pragma unroll
           for (int t = 0; t < T; ++t) {
             acc[t].x = fma(vj[q], xv[q][t].x, acc[t].x);
@@ -273,7 +275,7 @@ __global__ void pattern_axpy_kernel(double* __restrict__ y_csr, double* __restri
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-template <int G, int T, bool V2>
+template <int G, int T, bool V2, int Q = 4>
 static void launch_spmm_t(const int* ptr, const int* idx, const double* val, const int* items,
                           int n_items, const double* X, long long ldx, int w, double* Y,
                           long long ldy, double* scratch, cudaStream_t s) {
@@ -285,8 +287,8 @@ static void launch_spmm_t(const int* ptr, const int* idx, const double* val, con
   long long cap = (long long)sm_count() * 16;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  spmm_kernel<G, T, V2><<<(int)blocks, 256, 0, s>>>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy,
-                                                    scratch, n_tiles);
+  spmm_kernel<G, T, V2, Q><<<(int)blocks, 256, 0, s>>>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy,
+                                                       scratch, n_tiles);
 }
 
 // (G, T) per width: G lanes per item, T column pairs per lane.  Narrow
@@ -311,8 +313,16 @@ static void dispatch_spmm(const int* ptr, const int* idx, const double* val, con
     else if (pairs <= 64) { G = 32; T = 2; }
     else { G = 32; T = 3; }
   }
-#define LR_SPMM_CASE(g, t) \
-  if (G == g && T == t) return launch_spmm_t<g, t, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+  static const int q_env = getenv("LR_SPMM_Q") ? atoi(getenv("LR_SPMM_Q")) : 0;
+  const int Qv = q_env ? q_env : (T == 1 ? 8 : 4);
+#define LR_SPMM_CASE(g, t)                                                                              \
+  if (G == g && T == t) {                                                                               \
+    if constexpr (t == 1) {                                                                             \
+      if (Qv == 8)                                                                                      \
+        return launch_spmm_t<g, t, V2, 8>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s); \
+    }                                                                                                   \
+    return launch_spmm_t<g, t, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);        \
+  }
   LR_SPMM_CASE(1, 1) LR_SPMM_CASE(2, 1) LR_SPMM_CASE(4, 1) LR_SPMM_CASE(8, 1) LR_SPMM_CASE(16, 1)
   LR_SPMM_CASE(32, 1) LR_SPMM_CASE(32, 2) LR_SPMM_CASE(32, 3)
   LR_SPMM_CASE(2, 2) LR_SPMM_CASE(2, 3) LR_SPMM_CASE(2, 4) LR_SPMM_CASE(4, 2) LR_SPMM_CASE(4, 3)
