@@ -611,7 +611,9 @@ extern "C" {
 long long lr_syevd_workspace_doubles(int n) {
   const long long N = n;
   // d, e, tau, e2, w, bounds | Vr | vbuf, pbuf | Z, U1, U2, Lm, Dg | Pv (ints) | clusters | global rows
-  return 6 * N + 8 + N * N + 4 * N + 5 * N * N + N * N / 2 + N + N + 64 + N * (N + 1);
+  // | WY T factors (one kWY x kWY block per 32 reflectors)
+  return 6 * N + 8 + N * N + 4 * N + 5 * N * N + N * N / 2 + N + N + 64 + N * (N + 1) +
+         ((N + kWY - 1) / kWY + 1) * kWY * kWY;
 }
 
 int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V, long long ldv, double* work,
@@ -742,7 +744,8 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
   if (n > 2) {
     const int nrefl = n - 2;  // reflectors 0 .. n-3
     const int nblk = (nrefl + kWY - 1) / kWY;
-    double* Tb = Lm;   // nblk x kWY x kWY (inverse-iteration scratch is free now)
+    // nblk x kWY x kWY T factors in their own region (reusing Lm overflowed it for n < ~32)
+    double* Tb = reinterpret_cast<double*>(clus) + N + 64 + N * (N + 1);
     build_T_kernel<<<nblk, 256, 0, s>>>(Vr, tau, n, nrefl, Tb);
     LR_CHECK_LAUNCH();
     const size_t vsm = (size_t)kWY * (n + 1) * sizeof(double);
