@@ -25,7 +25,10 @@ namespace cg = cooperative_groups;
 
 namespace lr {
 
-constexpr int LU_THREADS = 256;
+#ifndef LR_LU_THREADS
+#define LR_LU_THREADS 256
+#endif
+constexpr int LU_THREADS = LR_LU_THREADS;
 constexpr int LU_CHUNK = 64;  // trailing columns per U12 chunk
 
 struct LuParams {
@@ -112,7 +115,7 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
         double v = (lane < LU_THREADS / 32) ? red_v[lane] : -1.0;
         int r = (lane < LU_THREADS / 32) ? red_r[lane] : 0x7fffffff;
 #pragma unroll
-        for (int o = 4; o > 0; o >>= 1) {
+        for (int o = LU_THREADS / 64; o > 0; o >>= 1) {
           double v2 = __shfl_xor_sync(0xffffffffu, v, o);
           int r2 = __shfl_xor_sync(0xffffffffu, r, o);
           better(v, r, v2, r2);
