@@ -249,6 +249,101 @@ __global__ void __launch_bounds__(kSvtThreads) sddmm_kernel(
   }
 }
 
+// Group variant (r <= 256): G lanes per item share one CSR row, lane g holds
+// the U*S values of its column pairs in registers and gathers the matching
+// slice of each V row (one coalesced read of 8r bytes per entry per group
+// instead of 32 lanes each walking a different V row); the G partial dots are
+// folded with a fixed xor-butterfly and lane 0 of the group finishes the
+// entry.  Q entries in flight per group.  Every entry's value depends only on
+// (U row, S, V row): the sharded engine's two value copies stay identical.
+template <int G, int T, bool FUSED, int Q = 4>
+__global__ void __launch_bounds__(kSvtThreads) svt_group_kernel(
+    const int* __restrict__ ptr, const int* __restrict__ idx, const int* __restrict__ items, int n_items,
+    const double* __restrict__ U, long long ldu, const double* __restrict__ S, const double* __restrict__ V,
+    long long ldv, int r, double* __restrict__ x_out, const double* __restrict__ m_vals,
+    double* __restrict__ y_csr, double* __restrict__ y_csc, const int* __restrict__ inv_perm, double step,
+    int apply, double* __restrict__ partial) {
+  constexpr int GROUPS = 32 / G;
+  const int lane = threadIdx.x & 31, g = lane % G, grp = lane / G;
+  // groups of a warp walk items of different lengths: shuffles name only their own group
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
+  const long long warp_global = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long n_units = (n_items + GROUPS - 1) / GROUPS;
+  double ss = 0.0, mx = 0.0;
+  for (long long u = warp_global; u < n_units; u += n_warps) {
+    const int item_i = (int)u * GROUPS + grp;
+    if (item_i >= n_items) continue;  // group-uniform
+    const Item it = load_item(items, ptr, item_i);
+    double2 us[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int c = 2 * (g + G * t);
+      const double* ur = U + (long long)it.row * ldu;
+      us[t].x = (c < r) ? ur[c] * S[c] : 0.0;
+      us[t].y = (c + 1 < r) ? ur[c + 1] * S[c + 1] : 0.0;
+    }
+    for (int e0 = it.beg; e0 < it.end; e0 += Q) {
+      double part[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        part[q] = 0.0;
+        const int e = e0 + q;
+        if (e < it.end) {
+          const double* vr = V + (long long)__ldg(idx + e) * ldv;
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            const int c = 2 * (g + G * t);
+            double2 v;
+            if (c + 1 < r) {
+              v = __ldg(reinterpret_cast<const double2*>(vr + c));
+            } else {
+              v.x = (c < r) ? __ldg(vr + c) : 0.0;
+              v.y = 0.0;
+            }
+            part[q] = fma(us[t].x, v.x, part[q]);
+            part[q] = fma(us[t].y, v.y, part[q]);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) part[q] += __shfl_xor_sync(gmask, part[q], o);
+      if (g == 0) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int e = e0 + q;
+          if (e >= it.end) break;
+          const double acc = part[q];
+          if (FUSED) {
+            const double mv = __ldg(m_vals + e);
+            const double d = acc - mv;
+            ss = fma(d, d, ss);
+            mx = fmax(mx, fabs(d));
+            if (apply) {
+              const double ynew = add_rn(y_csr[e], mul_rn(step, add_rn(mv, -acc)));
+              y_csr[e] = ynew;
+              y_csc[__ldg(inv_perm + e)] = ynew;
+            }
+          } else {
+            x_out[e] = acc;
+          }
+        }
+      }
+    }
+  }
+  if (FUSED) {
+    __shared__ double red[32];
+    const double S2 = block_sum<kSvtThreads>(ss, red);
+    const double M2 = block_max<kSvtThreads>(mx, red);
+    if (threadIdx.x == 0) {
+      partial[2 * blockIdx.x] = S2;
+      partial[2 * blockIdx.x + 1] = M2;
+    }
+  }
+}
+
 __global__ void svt_finish_kernel(const double* partial, int n, double* out2) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double s = 0.0, m = 0.0;
@@ -402,6 +497,35 @@ static int launch_sddmm(bool fused, const int* ptr, const int* idx, int rows, co
   LR_REQUIRE(r <= kMaxRankSmem, "sddmm: rank %d exceeds %d", r, kMaxRankSmem);
   if (!items) n_items = rows;
   const int blocks = sm_count() * kSvtBlocksPerSm;
+  static const bool old_kernel = getenv("LR_SVT_WARP_KERNEL") != nullptr;
+  const bool v2ok = (ldv % 2 == 0) && aligned16(V) && (ldu >= r);
+  // the group kernel wins only for wide factors (cfg4, tools/sddmm_probe.py: r = 84 2.13 vs 2.26 ms,
+  // r = 160 2.99 vs 5.52 ms; r <= 40 the warp kernel is up to 2x faster)
+  if (!old_kernel && r >= 64 && r <= 256 && v2ok) {
+    const int pairs = (r + 1) / 2;
+#define LR_SVT_GROUP(g, t)                                                                                 \
+  do {                                                                                                     \
+    if (fused)                                                                                             \
+      svt_group_kernel<g, t, true><<<blocks, kSvtThreads, 0, s>>>(ptr, idx, items, n_items, U, ldu, S, V,  \
+                                                                  ldv, r, x, m_vals, y_csr, y_csc,         \
+                                                                  inv_perm, step, apply, partial);         \
+    else                                                                                                   \
+      svt_group_kernel<g, t, false><<<blocks, kSvtThreads, 0, s>>>(ptr, idx, items, n_items, U, ldu, S, V, \
+                                                                   ldv, r, x, m_vals, y_csr, y_csc,        \
+                                                                   inv_perm, step, apply, partial);        \
+  } while (0)
+    if (pairs <= 1) LR_SVT_GROUP(1, 1);
+    else if (pairs <= 2) LR_SVT_GROUP(2, 1);
+    else if (pairs <= 4) LR_SVT_GROUP(4, 1);
+    else if (pairs <= 8) LR_SVT_GROUP(8, 1);
+    else if (pairs <= 16) LR_SVT_GROUP(8, 2);
+    else if (pairs <= 32) LR_SVT_GROUP(16, 2);
+    else if (pairs <= 64) LR_SVT_GROUP(32, 2);
+    else LR_SVT_GROUP(32, 4);
+#undef LR_SVT_GROUP
+    LR_CHECK_LAUNCH();
+    return LR_OK;
+  }
   const size_t smem = (size_t)(kSvtThreads / 32) * (r > 0 ? r : 1) * sizeof(double);
   const bool v2 = (ldv % 2 == 0) && aligned16(V);
   if (smem > 48 * 1024) {
