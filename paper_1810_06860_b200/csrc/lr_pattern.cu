@@ -21,8 +21,8 @@ constexpr int TP_THREADS = 256;
 static int tp_blocks(int m, int n) {
   // B row blocks: ~1000 CTAs keep every SM busy while each walks its rows in
   // order (one row-latency chain per CTA); the counter table stays <= 256 Mi ints
-  long long B = (long long)m / 16 + 1;
-  if (B > 1024) B = 1024;
+  long long B = (long long)m / 32 + 1;
+  if (B > 512) B = 512;
   const long long cap = (256LL << 20) / (n > 0 ? n : 1);
   if (B > cap) B = cap;
   if (B < 1) B = 1;
@@ -40,9 +40,21 @@ __global__ void tp_hist_kernel(const int* __restrict__ ptr, const int* __restric
 
 // per column j: c_b[j] <- sum_{b' < b} c_b'[j]; tot[j] = sum_b c_b[j]
 __global__ void tp_colscan_kernel(int* __restrict__ cnt, int n, int B, int* __restrict__ tot) {
+  constexpr int U = 16;  // loads in flight per thread (the walk down a column is latency-bound)
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     int run = 0;
-    for (int b = 0; b < B; ++b) {
+    int b = 0;
+    for (; b + U <= B; b += U) {
+      int c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = cnt[(long long)(b + u) * n + j];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        cnt[(long long)(b + u) * n + j] = run;
+        run += c[u];
+      }
+    }
+    for (; b < B; ++b) {
       const long long o = (long long)b * n + j;
       const int c = cnt[o];
       cnt[o] = run;
