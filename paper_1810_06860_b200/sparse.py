@@ -36,7 +36,20 @@ _SPECTRAL_MAX_ITERS = 200
 _SPECTRAL_BATCH = 8
 
 
-def _schedule(indptr: np.ndarray, chunk: int = SPLIT_CHUNK):
+# enough work items to fill the GPU several times over: small patterns (cfg1:
+# 1000 rows of 200 entries) split their rows into short chunks so a product is
+# not a few hundred latency-bound row walks (cfg1 CSR w = 16: 28 -> ~8 us)
+TARGET_ITEMS = 148 * 64
+MIN_CHUNK = 32
+
+
+def _chunk_for(indptr: np.ndarray) -> int:
+    nnz = int(indptr[-1]) if indptr.size else 0
+    c = nnz // TARGET_ITEMS
+    return int(min(SPLIT_CHUNK, max(MIN_CHUNK, c)))
+
+
+def _schedule(indptr: np.ndarray, chunk: int = None):
     """Work items {row, beg, end, slot} (int32 x4) and split rows
     {row, slot_beg, slot_end, 0}; (None, None, 0) for a balanced pattern with
     no long row.  Items are ordered longest first: the lane groups of a warp
@@ -44,6 +57,8 @@ def _schedule(indptr: np.ndarray, chunk: int = SPLIT_CHUNK):
     groups idle behind the longest one) and the grid-stride loop drains the
     long items early.  Order does not affect results: every item owns its
     output row or split slot, and split slots are summed in slot order."""
+    if chunk is None:
+        chunk = _chunk_for(indptr)
     lens = np.diff(indptr)
     longm = lens > chunk
     skewed = lens.size > 0 and lens.max() > SKEW_RATIO * max(lens.mean(), 1.0)
