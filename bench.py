@@ -230,6 +230,7 @@ def bench_svt(cpu: bool, peaks=None):
     o3, _ = workloads.cfg3()
     obs3 = ObservationSet(o3.m, o3.n, o3.rows, o3.cols, o3.values)
     prm3 = completion.SvtParams(strategy="reuse-u", i_reuse=100, q_reuse=10, seed=0, epsilon=0.05)
+    completion.svt_fast(obs3, prm3)  # warm
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res3 = completion.svt_fast(obs3, prm3)
@@ -245,6 +246,7 @@ def bench_svt(cpu: bool, peaks=None):
     obs4 = ObservationSet(o4.m, o4.n, o4.rows, o4.cols, o4.values, o4.split)
     prm = completion.SvtParams(epsilon=0.17, i_reuse=5, q_reuse=10, strategy="reuse-q", seed=0, i_max=20,
                                delta=1.0, tau=5.0 * o4.n / 40)
+    completion.svt_fast(obs4, prm)  # warm: lazy module loads and arena growth stay out of the timed run
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = completion.svt_fast(obs4, prm)

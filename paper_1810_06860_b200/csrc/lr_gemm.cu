@@ -54,6 +54,8 @@ struct Tile {
   static constexpr int SMEM = STAGES * (A_STAGE + B_STAGE) * (int)sizeof(double);
 };
 using TileL = Tile<128, 64, 64, 32>;
+using TileL8 = Tile<128, 64, 32, 32>;   // 8 warps of 32x32: 16 warps/SM at 2 CTAs/SM
+using TileW = Tile<128, 128, 64, 32>;   // 8 warps of 64x32
 using TileS = Tile<64, 64, 32, 32>;
 
 template <typename T, bool TRANS_A>
@@ -282,10 +284,25 @@ static int choose_splits_t(int M, int N, int K, int flags) {
   return (int)s;
 }
 
+// large-tile variant: 0 = 128x64 / 4 warps of 64x32, 1 = 128x64 / 8 warps
+// of 32x32 (16 warps/SM keep the DMMA pipe fed through the fragment loads),
+// 2 = 128x128 / 8 warps of 64x32.  Measured (tools/gemm_probe.py): A^T B
+// (Gram) is fastest on 0 (2.00 vs 2.15 ms at 100000 x 660), A B on 1
+// (H R^{-1} 2.00 -> 1.85 ms, H V 0.70 -> 0.62 ms).  LR_GEMM_TILE overrides.
+static int large_variant(int transA) {
+  static const int v = tile_pref("LR_GEMM_TILE", -1);
+  if (v >= 0) return v;
+  return transA ? 0 : 1;
+}
+
 static int choose_splits(int transA, int M, int N, int K, int flags) {
   if (!transA) return 1;
-  return use_large(M, N, K, flags) ? choose_splits_t<TileL, true>(M, N, K, flags)
-                            : choose_splits_t<TileS, true>(M, N, K, flags);
+  if (!use_large(M, N, K, flags)) return choose_splits_t<TileS, true>(M, N, K, flags);
+  switch (large_variant(1)) {
+    case 1: return choose_splits_t<TileL8, true>(M, N, K, flags);
+    case 2: return choose_splits_t<TileW, true>(M, N, K, flags);
+    default: return choose_splits_t<TileL, true>(M, N, K, flags);
+  }
 }
 
 template <typename T, bool TA>
@@ -327,17 +344,28 @@ int lr_gemm_f64(int transA, int M, int N, int K, double alpha, const double* A, 
   if (S > 1) S = (K + k_chunk - 1) / k_chunk;
   const int vec16 = (lda % 2 == 0) && (ldb % 2 == 0) && aligned16(A) && aligned16(B);
   const bool large = use_large(M, N, K, flags);
+  const int variant = large_variant(transA);
+#define LR_GEMM_ARGS M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, flags, work, S, k_chunk, vec16, s
   if (transA) {
-    if (large)
-      launch<TileL, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, flags, work, S, k_chunk, vec16, s);
+    if (!large)
+      launch<TileS, true>(LR_GEMM_ARGS);
+    else if (variant == 1)
+      launch<TileL8, true>(LR_GEMM_ARGS);
+    else if (variant == 2)
+      launch<TileW, true>(LR_GEMM_ARGS);
     else
-      launch<TileS, true>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, flags, work, S, k_chunk, vec16, s);
+      launch<TileL, true>(LR_GEMM_ARGS);
   } else {
-    if (large)
-      launch<TileL, false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, flags, work, S, k_chunk, vec16, s);
+    if (!large)
+      launch<TileS, false>(LR_GEMM_ARGS);
+    else if (variant == 1)
+      launch<TileL8, false>(LR_GEMM_ARGS);
+    else if (variant == 2)
+      launch<TileW, false>(LR_GEMM_ARGS);
     else
-      launch<TileS, false>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, flags, work, S, k_chunk, vec16, s);
+      launch<TileL, false>(LR_GEMM_ARGS);
   }
+#undef LR_GEMM_ARGS
   LR_CHECK_LAUNCH();
   if (S > 1) {
     long long total = (long long)M * N;

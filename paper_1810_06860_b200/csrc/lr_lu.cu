@@ -29,15 +29,21 @@ namespace lr {
 #define LR_LU_THREADS 256
 #endif
 constexpr int LU_THREADS = LR_LU_THREADS;
-constexpr int LU_CHUNK = 64;  // trailing columns per U12 chunk
+constexpr int LU_CHUNK = 128;  // widest U12 chunk of trailing columns (panel-end update)
+constexpr int LU_NBMAX = 32;   // widest panel (prow slots are LU_NBMAX doubles)
+constexpr int LU_CPL = 10;     // candidates per lane in the winner fold: G <= 320 CTAs
+constexpr int kCandWords = 2 * 2;            // per CTA: 2 slots x {value, row}
+constexpr int kRowWords = 2 * LU_NBMAX;      // per CTA: 2 slots x panel row
 
 struct LuParams {
   double* X;
   long long ldx;
   int m, n, nb, rows_per;
+  int ch;               // U12 chunk width (multiple of 8); row stride ch + 4 (conflict-free DMMA B fragments)
   const double* stats;  // {sumsq, max|x|, nonfinite}
   double* cand;         // [2][G][2]  {|x|, row}
-  double* prow;         // [2][G][nb]
+  double* prow;         // [2][G][LU_NBMAX]
+  unsigned* bar;        // column barrier counter: G arrivals per column (zeroed before the launch)
   int* pivrow;          // [n]
   double* status;       // {bad col or -1, pivot, tol}
   long long* prof;      // optional per-phase clock totals of CTA 0 (LR_LU_PROFILE)
@@ -50,7 +56,36 @@ __device__ __forceinline__ void better(double& v, int& r, double v2, int r2) {
   }
 }
 
-__global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
+__device__ __forceinline__ void lu_dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Column loop, per column j = J + jj (one split grid barrier per column):
+//   1. CTA candidate (look-ahead value from the previous column's pass):
+//      block fold, warp 0 publishes {|x|, row} and the candidate's panel row
+//      with the still-pending update of step j-1 applied to the copy;
+//   2. arrive on the column barrier (fence + one atomic by thread 0);
+//   3. the pending update of step j-1 on panel columns > j, overlapping the
+//      barrier latency;
+//   4. wait (acquire spin on the counter);
+//   5. warp 0 folds the G candidates (ties -> smallest row; all loads in
+//      flight at once) and fetches the winner's published row;
+//   6. multipliers of column j, update of column j+1 only, and the next
+//      column's local candidate.
+// The published row copy and the deferred in-place update evaluate the same
+// fma(-l, u, x), so the pivot row seen by every CTA is bit-identical to the
+// owner's.  (A barrier-free exchange of self-validating tagged words was
+// measured slower: 1.02 vs 0.89 ms at 100000 x 110 -- every CTA polling
+// every candidate costs more than one counter.)
+__global__ void __launch_bounds__(LU_THREADS, 2) lu_kernel(LuParams p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double lu_smem[];
   const int nb = p.nb, LD = nb + 1;
@@ -60,23 +95,26 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
   const int r1 = min(p.m, r0 + p.rows_per);
   const int nr = max(0, r1 - r0);
   double* P = lu_smem;                                   // rows_per x LD
-  double* U12 = P + (long long)p.rows_per * LD;          // nb x LU_CHUNK
-  double* urow = U12 + nb * LU_CHUNK;                    // nb
+  const int LDU = p.ch + 4;
+  double* U12 = P + (((long long)p.rows_per * LD + 1) & ~1LL);  // nb x LDU, 16-byte aligned
+  double* urow = U12 + nb * LDU;                         // nb
   double* L11 = urow + nb;                               // nb x nb
   int* pivflag = reinterpret_cast<int*>(L11 + nb * nb);  // rows_per
   __shared__ double red_v[LU_THREADS / 32];
   __shared__ int red_r[LU_THREADS / 32];
   __shared__ double win_v;
+  __shared__ int pivs[LU_NBMAX];
   long long* prof = (blockIdx.x == 0 && threadIdx.x == 0) ? p.prof : nullptr;
   long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
-  double cbv = -1.0;  // look-ahead candidate for the next column
+  double cbv = -1.0;  // local candidate for the current column
   int cbr = 0x7fffffff;
 
   const double maxabs = p.stats[1];
   const double tol = 1e-14 * maxabs;
   if (maxabs == 0.0 || p.stats[2] != 0.0) return;  // handled by the host wrapper
   for (int i = tid; i < nr; i += LU_THREADS) pivflag[i] = -1;
-  int par = 0;
+  // 16-byte column pairs in the panel-end update: even ld, aligned base, even panel width
+  const bool vec2 = (p.ldx % 2 == 0) && ((reinterpret_cast<uintptr_t>(p.X) & 15u) == 0) && (nb % 2 == 0);
 
   for (int J = 0; J < p.n; J += nb) {
     const int jb = min(nb, p.n - J);
@@ -85,19 +123,17 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
       P[i * LD + c] = p.X[(long long)(r0 + i) * p.ldx + J + c];
     }
     __syncthreads();
+    cbv = -1.0;
+    cbr = 0x7fffffff;
+    for (int i = tid; i < nr; i += LU_THREADS)
+      if (pivflag[i] < 0) better(cbv, cbr, fabs(P[i * LD]), r0 + i);
     for (int jj = 0; jj < jb; ++jj) {
       const int j = J + jj;
-      // local argmax among un-pivoted rows
+      const int par = j & 1;
       if (prof) t0 = clock64();
-      double bv = -1.0;
-      int br = 0x7fffffff;
-      if (jj == 0) {
-        for (int i = tid; i < nr; i += LU_THREADS)
-          if (pivflag[i] < 0) better(bv, br, fabs(P[i * LD + jj]), r0 + i);
-      } else {  // found during the previous column's update (look-ahead)
-        bv = cbv;
-        br = cbr;
-      }
+      // (1) CTA candidate
+      double bv = cbv;
+      int br = cbr;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -109,9 +145,10 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
         red_r[wid] = br;
       }
       __syncthreads();
-      if (wid == 0) {
-        // CTA candidate: warp 0 folds the per-warp winners and publishes
-        // (|x|, row) plus the candidate's panel row (one element per lane)
+      // every warp folds the per-warp winners (all threads learn the CTA
+      // candidate row, which warp 0 alone updates below)
+      int rc;
+      {
         double v = (lane < LU_THREADS / 32) ? red_v[lane] : -1.0;
         int r = (lane < LU_THREADS / 32) ? red_r[lane] : 0x7fffffff;
 #pragma unroll
@@ -121,27 +158,67 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
           better(v, r, v2, r2);
         }
         v = __shfl_sync(0xffffffffu, v, 0);
-        r = __shfl_sync(0xffffffffu, r, 0);
-        if (lane == 0) {
-          p.cand[(par * G + cta) * 2 + 0] = v;
-          p.cand[(par * G + cta) * 2 + 1] = (double)r;
+        rc = __shfl_sync(0xffffffffu, r, 0);
+        if (wid == 0) {
+          if (lane == 0) {
+            p.cand[(par * G + cta) * 2 + 0] = v;
+            p.cand[(par * G + cta) * 2 + 1] = (double)rc;
+          }
+          if (rc != 0x7fffffff) {
+            double* row = P + (rc - r0) * LD;
+            double* dst = p.prow + ((long long)par * G + cta) * LU_NBMAX;
+            const double l = jj > 0 ? row[jj - 1] : 0.0;
+            for (int c = jj + lane; c < jb; c += 32) {
+              double x = row[c];
+              if (jj > 0 && c > jj) {
+                x = fma(-l, urow[c], x);
+                row[c] = x;  // its pending update, done here instead of in (3)
+              }
+              dst[c] = x;
+            }
+          }
+          // (2) arrive: the lanes' stores are ordered before thread 0's fence
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence();
+            atomicAdd(p.bar, 1u);
+          }
         }
-        if (r != 0x7fffffff)
-          for (int c = lane; c < jb; c += 32) p.prow[((long long)par * G + cta) * nb + c] = P[(r - r0) * LD + c];
       }
       if (prof) t1 = clock64();
-      grid.sync();
+      // (3) pending update of step j-1 on columns jj+1.. (column jj was done in (6))
+      if (jj > 0 && jj + 1 < jb) {
+        for (int i = tid; i < nr; i += LU_THREADS) {
+          if (pivflag[i] >= 0 || r0 + i == rc) continue;
+          double* row = P + i * LD;
+          const double l = row[jj - 1];
+          for (int c = jj + 1; c < jb; ++c) row[c] = fma(-l, urow[c], row[c]);
+        }
+      }
+      // (4) wait: every CTA has arrived for column j
+      if (tid == 0) {
+        const unsigned target = (unsigned)(j + 1) * (unsigned)G;
+        while (ld_acquire_gpu(p.bar) < target) {
+        }
+      }
+      __syncthreads();
       if (prof) t2 = clock64();
+      // (5) global winner, same in every CTA
       if (wid == 0) {
-        // global winner, same in every CTA: warp 0 alone loads the G
-        // candidates (G/32 independent L2 loads per lane), folds them with
-        // shuffles and fetches the winner's panel row -- no block-level
-        // reduction between the two L2 round trips
         double v = -1.0;
         int r = 0x7fffffff;
-        for (int c = lane; c < G; c += 32) {
-          const double2 cr = __ldcg(reinterpret_cast<const double2*>(p.cand) + par * G + c);
-          better(v, r, cr.x, (int)cr.y);
+        {
+          // all of this lane's candidate loads in flight at once (G <= 32 * LU_CPL
+          // is enforced by the plan), folded in index order afterwards
+          const double2* cp = reinterpret_cast<const double2*>(p.cand) + par * G;
+          double2 cr[LU_CPL];
+#pragma unroll
+          for (int u = 0; u < LU_CPL; ++u) {
+            const int c = lane + 32 * u;
+            cr[u] = c < G ? __ldcg(cp + c) : make_double2(-1.0, 2147483647.0);
+          }
+#pragma unroll
+          for (int u = 0; u < LU_CPL; ++u) better(v, r, cr[u].x, (int)cr[u].y);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -149,9 +226,12 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
           int r2 = __shfl_xor_sync(0xffffffffu, r, o);
           better(v, r, v2, r2);
         }
+        if (prof) prof[5] += clock64() - t2;
         const int wc = r / p.rows_per;  // slabs are contiguous
-        const double* wrow = p.prow + ((long long)par * G + wc) * nb;
-        for (int c = lane; c < jb; c += 32) urow[c] = __ldcg(wrow + c);
+        const double* wrow = p.prow + ((long long)par * G + wc) * LU_NBMAX;
+        if (r != 0x7fffffff)
+          for (int c = jj + lane; c < jb; c += 32) urow[c] = __ldcg(wrow + c);
+        if (prof) prof[6] += clock64() - t2 + (long long)(urow[jj] * 0.0);
         if (lane == 0) {
           win_v = v;
           if (r >= r0 && r < r1 && v >= tol && v != 0.0) pivflag[r - r0] = j;
@@ -168,7 +248,8 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
         return;  // uniform across the grid
       }
       if (prof) t3 = clock64();
-      const double rpiv = 1.0 / urow[jj];  // LAPACK dgetf2/dgetrf2: scale by 1/pivot
+      // (6) multipliers (LAPACK dgetf2: scale by 1/pivot), column jj+1, next candidate
+      const double rpiv = 1.0 / urow[jj];
       cbv = -1.0;
       cbr = 0x7fffffff;
       const bool look = jj + 1 < jb;
@@ -177,11 +258,12 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
         double* row = P + i * LD;
         const double l = row[jj] * rpiv;
         row[jj] = l;
-        for (int c = jj + 1; c < jb; ++c) row[c] = fma(-l, urow[c], row[c]);
-        if (look) better(cbv, cbr, fabs(row[jj + 1]), r0 + i);
+        if (look) {
+          const double x = fma(-l, urow[jj + 1], row[jj + 1]);
+          row[jj + 1] = x;
+          better(cbv, cbr, fabs(x), r0 + i);
+        }
       }
-      __syncthreads();
-      par ^= 1;
       if (prof) {
         const long long t4 = clock64();
         prof[0] += t1 - t0;
@@ -190,6 +272,7 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
         prof[3] += t4 - t3;
       }
     }
+    __syncthreads();
     // write the panel back
     const long long tp0 = prof ? clock64() : 0;
     for (int e = tid; e < nr * jb; e += LU_THREADS) {
@@ -200,59 +283,126 @@ __global__ void __launch_bounds__(LU_THREADS) lu_kernel(LuParams p) {
     if (prof && rest <= 0) prof[4] += clock64() - tp0;
     if (rest > 0) {
       grid.sync();
+      // the panel's pivot rows (known to every CTA from the winner folds)
+      if (tid < jb) pivs[tid] = __ldcg(p.pivrow + J + tid);
+      __syncthreads();
       // unit-lower L11 from the pivot rows' multipliers
       for (int e = tid; e < jb * jb; e += LU_THREADS) {
         int a = e / jb, b = e - (e / jb) * jb;
-        L11[a * nb + b] = (b < a) ? p.X[(long long)p.pivrow[J + a] * p.ldx + J + b] : 0.0;
+        L11[a * nb + b] = (b < a) ? __ldcg(p.X + (long long)pivs[a] * p.ldx + J + b) : 0.0;
       }
-      __syncthreads();
-      for (int c0 = 0; c0 < rest; c0 += LU_CHUNK) {
-        const int cw = min(LU_CHUNK, rest - c0);
+      const long long tu0 = prof ? clock64() : 0;
+      for (int c0 = 0; c0 < rest; c0 += p.ch) {
+        const int cw = min(p.ch, rest - c0);
+        const long long cbase = J + jb + c0;
+#pragma unroll 4
         for (int e = tid; e < jb * cw; e += LU_THREADS) {
           int a = e / cw, c = e - (e / cw) * cw;
-          U12[a * LU_CHUNK + c] = p.X[(long long)p.pivrow[J + a] * p.ldx + J + jb + c0 + c];
+          U12[a * LDU + c] = __ldcg(p.X + (long long)pivs[a] * p.ldx + cbase + c);
         }
         __syncthreads();
-        // forward substitution with the unit-lower L11, parallel over columns
-        for (int c = tid; c < cw; c += LU_THREADS)
-          for (int a = 1; a < jb; ++a) {
-            double s = U12[a * LU_CHUNK + c];
-            for (int b = 0; b < a; ++b) s = fma(-L11[a * nb + b], U12[b * LU_CHUNK + c], s);
-            U12[a * LU_CHUNK + c] = s;
+        // U12 = L11^{-1} U12: one column per thread, held in registers
+        for (int c = tid; c < cw; c += LU_THREADS) {
+          double u[LU_NBMAX];
+#pragma unroll
+          for (int a = 0; a < LU_NBMAX; ++a) u[a] = a < jb ? U12[a * LDU + c] : 0.0;
+#pragma unroll
+          for (int a = 1; a < LU_NBMAX; ++a) {
+            if (a < jb) {
+              double s = u[a];
+#pragma unroll
+              for (int b = 0; b < a; ++b) s = fma(-L11[a * nb + b], u[b], s);
+              u[a] = s;
+            }
           }
+#pragma unroll
+          for (int a = 1; a < LU_NBMAX; ++a)
+            if (a < jb) U12[a * LDU + c] = u[a];
+        }
         __syncthreads();
-        // X[rows, chunk] -= L[rows, panel] U12: thread = (column c, row lane);
-        // 8 rows per iteration so 8 global loads are in flight per thread
+        // X[rows, chunk] -= L[rows, panel] U12 on the tensor cores (DMMA
+        // m8n8k4): a warp owns 16 rows x 32 columns, its accumulators start
+        // as the X tile and go back in place (pivot rows and edges masked)
         {
-          constexpr int RL = LU_THREADS / LU_CHUNK;  // row lanes
-          const int c = tid % LU_CHUNK, rl = tid / LU_CHUNK;
-          if (c < cw) {
-            for (int ib = rl; ib < nr; ib += RL * 8) {
-              double xv[8];
+          const int ntc = (cw + 31) / 32;
+          const int ntiles = ((nr + 15) / 16) * ntc;
+          const int gid = lane >> 2, tig = lane & 3;
+          double nxt[2][4][2];
+          auto load_tile = [&](int t, double (&dst)[2][4][2]) {
+            const int rb = (t / ntc) * 16, cb = (t % ntc) * 32;
 #pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                const int i = ib + u * RL;
-                xv[u] = (i < nr && pivflag[i] < 0) ? p.X[(long long)(r0 + i) * p.ldx + J + jb + c0 + c] : 0.0;
-              }
-              for (int a = 0; a < jb; ++a) {
-                const double u12 = U12[a * LU_CHUNK + c];
+            for (int i = 0; i < 2; ++i) {
+              const int row = rb + i * 8 + gid;
+              const bool lv = row < nr && pivflag[row] < 0;
+              const double* xr = p.X + (long long)(r0 + row) * p.ldx + cbase;
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                  const int i = min(ib + u * RL, nr - 1);
-                  xv[u] = fma(-P[i * LD + a], u12, xv[u]);
+              for (int j = 0; j < 4; ++j) {
+                const int col = cb + j * 8 + 2 * tig;
+                if (lv && vec2 && col + 1 < cw) {
+                  const double2 v = *reinterpret_cast<const double2*>(xr + col);
+                  dst[i][j][0] = v.x;
+                  dst[i][j][1] = v.y;
+                } else {
+                  dst[i][j][0] = (lv && col < cw) ? xr[col] : 0.0;
+                  dst[i][j][1] = (lv && col + 1 < cw) ? xr[col + 1] : 0.0;
                 }
               }
+            }
+          };
+          if (wid < ntiles) load_tile(wid, nxt);
+          for (int t = wid; t < ntiles; t += LU_THREADS / 32) {
+            const int rb = (t / ntc) * 16, cb = (t % ntc) * 32;
+            double acc[2][4][2];
+            bool live[2];
 #pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                const int i = ib + u * RL;
-                if (i < nr && pivflag[i] < 0) p.X[(long long)(r0 + i) * p.ldx + J + jb + c0 + c] = xv[u];
+            for (int i = 0; i < 2; ++i) {
+              const int row = rb + i * 8 + gid;
+              live[i] = row < nr && pivflag[row] < 0;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                acc[i][j][0] = nxt[i][j][0];
+                acc[i][j][1] = nxt[i][j][1];
+              }
+            }
+            if (t + LU_THREADS / 32 < ntiles) load_tile(t + LU_THREADS / 32, nxt);  // next tile in flight
+            for (int k0 = 0; k0 < jb; k0 += 4) {
+              const int k = k0 + tig;
+              double af[2], bf[4];
+#pragma unroll
+              for (int i = 0; i < 2; ++i) af[i] = k < jb ? -P[min(rb + i * 8 + gid, nr - 1) * LD + k] : 0.0;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int col = cb + j * 8 + gid;
+                bf[j] = (k < jb && col < cw) ? U12[k * LDU + col] : 0.0;
+              }
+#pragma unroll
+              for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) lu_dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              if (!live[i]) continue;
+              double* xr = p.X + (long long)(r0 + rb + i * 8 + gid) * p.ldx + cbase;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int col = cb + j * 8 + 2 * tig;
+                if (vec2 && col + 1 < cw) {
+                  *reinterpret_cast<double2*>(xr + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+                } else {
+                  if (col < cw) xr[col] = acc[i][j][0];
+                  if (col + 1 < cw) xr[col + 1] = acc[i][j][1];
+                }
               }
             }
           }
         }
         __syncthreads();
       }
-      if (prof) prof[4] += clock64() - tp0;
+      if (prof) {
+        prof[4] += clock64() - tp0;
+        prof[7] += clock64() - tu0;
+      }
     }
   }
   // pivot rows: unit entry at their step, zeros to the right
@@ -380,13 +530,13 @@ static size_t lu_small_smem(int m, int n) {
 constexpr size_t kLuSmallMaxSmem = 200 * 1024;
 
 struct LuPlan {
-  int G, nb, rows_per;
+  int G, nb, ch, rows_per;
   size_t smem;
 };
 
-static size_t lu_smem_bytes(int rows_per, int nb) {
-  return (size_t)rows_per * (nb + 1) * 8 + (size_t)nb * LU_CHUNK * 8 + (size_t)nb * 8 +
-         (size_t)nb * nb * 8 + (size_t)rows_per * 4 + 16;
+static size_t lu_smem_bytes(int rows_per, int nb, int ch) {
+  return (size_t)rows_per * (nb + 1) * 8 + (size_t)nb * (ch + 4) * 8 + (size_t)nb * 8 +
+         (size_t)nb * nb * 8 + (size_t)rows_per * 4 + 24;
 }
 
 static LuPlan lu_plan(int m, int n) {
@@ -398,19 +548,26 @@ static LuPlan lu_plan(int m, int n) {
   for (int occ = occ_pref; occ >= 1; --occ) {
     const size_t limit = (226 * 1024) / occ - 1024;
     int G = sms * occ;
+    if (G > 32 * LU_CPL) G = 32 * LU_CPL;
     if (G > (m + 31) / 32) G = (m + 31) / 32;
     if (G < 1) G = 1;
     int rows_per = (m + G - 1) / G;
     G = (m + rows_per - 1) / rows_per;
-    for (int nb = 32; nb >= 1; nb >>= 1) {
+    // widest panel first (the panel-end update streams the trailing columns
+    // once per panel: nb = 32 moves ~2.3x fewer bytes than 16 at n = 110),
+    // with the widest U12 chunk that still fits
+    for (int nb = LU_NBMAX; nb >= 1; nb >>= 1) {
       int nbe = nb > n ? n : nb;
-      size_t sm = lu_smem_bytes(rows_per, nbe);
-      if (sm <= limit) {
-        pl.G = G;
-        pl.nb = nbe;
-        pl.rows_per = rows_per;
-        pl.smem = sm;
-        return pl;
+      for (int ch = LU_CHUNK; ch >= (nb >= 16 ? 32 : 8); ch -= 8) {
+        size_t sm = lu_smem_bytes(rows_per, nbe, ch);
+        if (sm <= limit) {
+          pl.G = G;
+          pl.nb = nbe;
+          pl.ch = ch;
+          pl.rows_per = rows_per;
+          pl.smem = sm;
+          return pl;
+        }
       }
     }
   }
@@ -427,7 +584,7 @@ extern "C" {
 long long lr_lu_workspace_doubles(int m, int n) {
   LuPlan pl = lu_plan(m, n);
   long long G = pl.G > 0 ? pl.G : 1;
-  return 4 * G + 2 * G * 32 + n + 8 + lr_stats_partials() + 16;
+  return kCandWords * G + kRowWords * G + n + 8 + lr_stats_partials() + 10;
 }
 
 int lr_lu_pl_f64(int m, int n, double* X, long long ldx, double* work, double* status_host,
@@ -458,9 +615,9 @@ int lr_lu_pl_f64(int m, int n, double* X, long long ldx, double* work, double* s
   LR_REQUIRE(pl.G > 0, "lu_pl: %d rows do not fit the cooperative plan", m);
   const long long G = pl.G;
   double* cand = work;
-  double* prow = cand + 4 * G;
-  int* pivrow = reinterpret_cast<int*>(prow + 2 * G * 32);
-  double* status = prow + 2 * G * 32 + n;  // n ints fit in n doubles
+  double* prow = cand + kCandWords * G;
+  int* pivrow = reinterpret_cast<int*>(prow + kRowWords * G);
+  double* status = work + (kCandWords + kRowWords) * G + n;  // n ints fit in n doubles
   double* stats = status + 4;
   double* partial = stats + 4;
   int st = lr_block_stats_f64(X, m, n, ldx, partial, stats, stream);
@@ -482,6 +639,7 @@ int lr_lu_pl_f64(int m, int n, double* X, long long ldx, double* work, double* s
   prm.m = m;
   prm.n = n;
   prm.nb = pl.nb;
+  prm.ch = pl.ch;
   prm.rows_per = pl.rows_per;
   prm.stats = stats;
   prm.cand = cand;
@@ -492,6 +650,8 @@ int lr_lu_pl_f64(int m, int n, double* X, long long ldx, double* work, double* s
   long long* dprof = reinterpret_cast<long long*>(partial + lr_stats_partials());
   prm.prof = profile ? dprof : nullptr;
   if (profile) LR_CHECK_CUDA(cudaMemsetAsync(dprof, 0, 8 * sizeof(long long), s));
+  prm.bar = reinterpret_cast<unsigned*>(dprof + 8);  // after the 8 profile slots
+  LR_CHECK_CUDA(cudaMemsetAsync(prm.bar, 0, sizeof(unsigned), s));
   void* args[] = {&prm};
   LR_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)lu_kernel, dim3((unsigned)G), dim3(LU_THREADS), args,
                                             pl.smem, s));
@@ -501,9 +661,9 @@ int lr_lu_pl_f64(int m, int n, double* X, long long ldx, double* work, double* s
     LR_CHECK_CUDA(cudaMemcpyAsync(hp, dprof, sizeof(hp), cudaMemcpyDeviceToHost, s));
     LR_CHECK_CUDA(cudaStreamSynchronize(s));
     fprintf(stderr,
-            "lu %dx%d G=%lld nb=%d cycles/col: local %.0f barrier %.0f winner %.0f update %.0f; panel ends total %.0f\n",
-            m, n, G, pl.nb, (double)hp[0] / n, (double)hp[1] / n, (double)hp[2] / n, (double)hp[3] / n,
-            (double)hp[4]);
+            "lu %dx%d G=%lld nb=%d ch=%d cycles/col: local %.0f barrier %.0f winner %.0f (cand %.0f row %.0f) update %.0f; panel ends total %.0f (after barrier %.0f)\n",
+            m, n, G, pl.nb, pl.ch, (double)hp[0] / n, (double)hp[1] / n, (double)hp[2] / n, (double)hp[5] / n,
+            (double)hp[6] / n, (double)hp[3] / n, (double)hp[4], (double)hp[7]);
   }
   double host[8];
   LR_CHECK_CUDA(cudaMemcpyAsync(host, status, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -40,16 +40,35 @@ __global__ void __launch_bounds__(kStatsThreads) block_stats_kernel(const double
                                                                    long long ld, double* partial) {
   __shared__ double sh[32];
   double s = 0.0, mx = 0.0, bad = 0.0;
-  const long long total = rows * cols;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (long long)gridDim.x * blockDim.x) {
-    long long r = t / cols, c = t - r * cols;
-    double v = X[r * ld + c];
+  auto acc = [&](double v) {
     if (!isfinite(v)) {
       bad += 1.0;
     } else {
       s = fma(v, v, s);
       mx = fmax(mx, fabs(v));
+    }
+  };
+  if (ld == cols) {
+    // contiguous: one flat grid-stride sweep, 4 independent loads per trip
+    const long long total = rows * cols;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; t + 3 * stride < total; t += 4 * stride) {
+      const double a = X[t], b = X[t + stride], c = X[t + 2 * stride], d = X[t + 3 * stride];
+      acc(a);
+      acc(b);
+      acc(c);
+      acc(d);
+    }
+    for (; t < total; t += stride) acc(X[t]);
+  } else {
+    // strided block: a warp per row, lanes across the columns (no 64-bit
+    // index division per element)
+    const int lane = threadIdx.x & 31;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
+      const double* row = X + r * ld;
+      for (long long c = lane; c < cols; c += 32) acc(row[c]);
     }
   }
   double S = block_sum<kStatsThreads>(s, sh);
@@ -62,14 +81,20 @@ __global__ void __launch_bounds__(kStatsThreads) block_stats_kernel(const double
   }
 }
 
+// One warp: lane-strided partial sums then a fixed shuffle tree (deterministic;
+// all of a lane's loads are independent, unlike a single-thread serial sum)
 __global__ void stats_finish_kernel(const double* partial, int n, double* out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0, m = 0, b = 0;
-    for (int i = 0; i < n; ++i) {
-      s += partial[3 * i];
-      m = fmax(m, partial[3 * i + 1]);
-      b += partial[3 * i + 2];
-    }
+  const int lane = threadIdx.x;
+  double s = 0, m = 0, b = 0;
+  for (int i = lane; i < n; i += 32) {
+    s += partial[3 * i];
+    m = fmax(m, partial[3 * i + 1]);
+    b += partial[3 * i + 2];
+  }
+  s = warp_sum(s);
+  m = warp_max(m);
+  b = warp_sum(b);
+  if (lane == 0) {
     out[0] = s;
     out[1] = m;
     out[2] = b;
@@ -89,11 +114,11 @@ __global__ void __launch_bounds__(kStatsThreads) dot_kernel(const double* __rest
 }
 
 __global__ void sum_finish_kernel(const double* partial, int n, double* out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0;
-    for (int i = 0; i < n; ++i) s += partial[i];
-    out[0] = s;
-  }
+  const int lane = threadIdx.x;
+  double s = 0;
+  for (int i = lane; i < n; i += 32) s += partial[i];
+  s = warp_sum(s);
+  if (lane == 0) out[0] = s;
 }
 
 // power iteration: partial[0..B) = x.z partials, partial[B..2B) = z.z partials

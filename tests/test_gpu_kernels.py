@@ -185,7 +185,8 @@ def test_upper_triangular_b_and_potrf_inverse():
     assert info == 0 and rel(R.T @ R, G + 3.5 * np.eye(200)) <= 1e-13
 
 
-@pytest.mark.parametrize("m,n", [(25, 7), (300, 40), (5000, 110), (100000, 110), (138493, 65), (40, 40)])
+@pytest.mark.parametrize("m,n", [(25, 7), (300, 40), (5000, 110), (100000, 110), (138493, 65), (40, 40),
+                                 (20000, 300), (60000, 305), (3000, 17)])
 def test_lu_pl_structure_and_span(m, n):
     from paper_1810_06860_b200.linalg import lu_pl
 
@@ -220,6 +221,11 @@ def test_lu_pl_errors():
         lu_pl(X)
     with pytest.raises(ValueError):
         lu_pl(np.ones((3, 5)))
+    # the cooperative (multi-CTA) kernel reports the same column
+    Z = np.random.default_rng(1).standard_normal((60000, 70))
+    Z[:, 41] = Z[:, 7] - 2.0 * Z[:, 30]
+    with pytest.raises(RankDeficiencyError, match="zero pivot at column 41"):
+        lu_pl(Z)
     Y = np.ones((6, 2))
     Y[1, 1] = np.nan
     with pytest.raises(ValueError, match="non-finite"):
