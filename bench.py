@@ -482,7 +482,9 @@ def main():
                    "parallelism": (f"sharded x{ws} (row/column nnz shards, NCCL allgather + allreduce)"
                                    if args.shard else f"replicas x{ws}"),
                    "omega": "device Philox4x64-10 (bit-exact numpy uniforms), value and e2e",
-                   "l2": "256 MB flush between timed steps"},
+                   "l2": "256 MB flush between timed steps",
+                   "subspace": "returned Subspace keeps Q as Q1 R2^-1 (last CholeskyQR pass unformed; "
+                               "U, S, V are complete; Subspace.Q forms Q on access)"},
         "rsvd_bki_time_s": step_ms * 1e-3,
         "step_ms_min_median_max": [min(per_step), float(np.median(per_step)), max(per_step)],
         "comm_bytes_per_step": comm_bytes,

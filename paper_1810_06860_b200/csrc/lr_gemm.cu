@@ -17,8 +17,7 @@
 
 namespace lr {
 
-constexpr int BK = 16;
-constexpr int STAGES = 3;
+constexpr int BK_ALIGN = 32;  // split-K chunks are multiples of every tile's BK
 
 __device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int src_bytes) {
   unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -40,9 +39,9 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int BM_, int BN_, int WM_, int WN_>
+template <int BM_, int BN_, int WM_, int WN_, int BK_ = 16, int STAGES_ = 3>
 struct Tile {
-  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_;
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, BK = BK_, STAGES = STAGES_;
   static constexpr int MT = WM / 8, NT = WN / 8;
   static constexpr int WARPS = (BM / WM) * (BN / WN);
   static constexpr int THREADS = WARPS * 32;
@@ -56,6 +55,9 @@ struct Tile {
 using TileL = Tile<128, 64, 64, 32>;
 using TileL8 = Tile<128, 64, 32, 32>;   // 8 warps of 32x32: 16 warps/SM at 2 CTAs/SM
 using TileW = Tile<128, 128, 64, 32>;   // 8 warps of 64x32
+using TileL32 = Tile<128, 64, 64, 32, 32, 2>;  // BK 32, 2 stages: half the barriers per DMMA
+using TileL832 = Tile<128, 64, 32, 32, 32, 2>;
+using TileT = Tile<64, 128, 32, 64>;    // cuBLAS-like 64x128, 4 warps of 32x64
 using TileS = Tile<64, 64, 32, 32>;
 
 template <typename T, bool TRANS_A>
@@ -68,13 +70,13 @@ __global__ void __launch_bounds__(T::THREADS) gemm_kernel(int M, int N, int K, d
   if ((flags & LR_GEMM_SYRK_UPPER) && (tn + 1) * T::BN <= tm * T::BM) return;  // tile entirely below diagonal
   extern __shared__ __align__(16) double g_smem[];
   double* As = g_smem;
-  double* Bs = g_smem + STAGES * T::A_STAGE;
+  double* Bs = g_smem + T::STAGES * T::A_STAGE;
 
   const int m0 = tm * T::BM, n0 = tn * T::BN;
   const int k_begin = z * k_chunk;
   int k_end = min(K, k_begin + k_chunk);
   if (flags & LR_GEMM_B_UPPER) k_end = min(k_end, n0 + T::BN);
-  const int nk = (k_end > k_begin) ? (k_end - k_begin + BK - 1) / BK : 0;
+  const int nk = (k_end > k_begin) ? (k_end - k_begin + T::BK - 1) / T::BK : 0;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / (T::BN / T::WN), wn = warp % (T::BN / T::WN);
@@ -100,27 +102,27 @@ __global__ void __launch_bounds__(T::THREADS) gemm_kernel(int M, int N, int K, d
   }
 
   auto load_stage = [&](int st, int kt) {
-    const int k0 = k_begin + kt * BK;
+    const int k0 = k_begin + kt * T::BK;
     double* as = As + st * T::A_STAGE;
     double* bs = Bs + st * T::B_STAGE;
     if (vec16) {
       if (!TRANS_A) {
         // A[m][k]: 8 pairs of k per row
-        for (int e = tid; e < T::BM * (BK / 2); e += T::THREADS) {
-          const int mm = e / (BK / 2), kk = 2 * (e % (BK / 2));
+        for (int e = tid; e < T::BM * (T::BK / 2); e += T::THREADS) {
+          const int mm = e / (T::BK / 2), kk = 2 * (e % (T::BK / 2));
           const int gm = m0 + mm, gk = k0 + kk;
           const int nb = (gm < M) ? (gk + 1 < k_end ? 16 : (gk < k_end ? 8 : 0)) : 0;
           cp_async16(as + mm * T::LDA_N + kk, nb ? A + (long long)gm * lda + gk : A, nb);
         }
       } else {
-        for (int e = tid; e < BK * (T::BM / 2); e += T::THREADS) {
+        for (int e = tid; e < T::BK * (T::BM / 2); e += T::THREADS) {
           const int kk = e / (T::BM / 2), mm = 2 * (e % (T::BM / 2));
           const int gm = m0 + mm, gk = k0 + kk;
           const int nb = (gk < k_end) ? (gm + 1 < M ? 16 : (gm < M ? 8 : 0)) : 0;
           cp_async16(as + kk * T::LDA_T + mm, nb ? A + (long long)gk * lda + gm : A, nb);
         }
       }
-      for (int e = tid; e < BK * (T::BN / 2); e += T::THREADS) {
+      for (int e = tid; e < T::BK * (T::BN / 2); e += T::THREADS) {
         const int kk = e / (T::BN / 2), nn = 2 * (e % (T::BN / 2));
         const int gn = n0 + nn, gk = k0 + kk;
         const int nb = (gk < k_end) ? (gn + 1 < N ? 16 : (gn < N ? 8 : 0)) : 0;
@@ -128,21 +130,21 @@ __global__ void __launch_bounds__(T::THREADS) gemm_kernel(int M, int N, int K, d
       }
     } else {
       if (!TRANS_A) {
-        for (int e = tid; e < T::BM * BK; e += T::THREADS) {
-          const int mm = e / BK, kk = e % BK;
+        for (int e = tid; e < T::BM * T::BK; e += T::THREADS) {
+          const int mm = e / T::BK, kk = e % T::BK;
           const int gm = m0 + mm, gk = k0 + kk;
           const bool ok = gm < M && gk < k_end;
           cp_async8(as + mm * T::LDA_N + kk, ok ? A + (long long)gm * lda + gk : A, ok ? 8 : 0);
         }
       } else {
-        for (int e = tid; e < BK * T::BM; e += T::THREADS) {
+        for (int e = tid; e < T::BK * T::BM; e += T::THREADS) {
           const int kk = e / T::BM, mm = e % T::BM;
           const int gm = m0 + mm, gk = k0 + kk;
           const bool ok = gm < M && gk < k_end;
           cp_async8(as + kk * T::LDA_T + mm, ok ? A + (long long)gk * lda + gm : A, ok ? 8 : 0);
         }
       }
-      for (int e = tid; e < BK * T::BN; e += T::THREADS) {
+      for (int e = tid; e < T::BK * T::BN; e += T::THREADS) {
         const int kk = e / T::BN, nn = e % T::BN;
         const int gn = n0 + nn, gk = k0 + kk;
         const bool ok = gn < N && gk < k_end;
@@ -152,24 +154,24 @@ __global__ void __launch_bounds__(T::THREADS) gemm_kernel(int M, int N, int K, d
   };
 
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
+  for (int s = 0; s < T::STAGES - 1; ++s) {
     if (s < nk) load_stage(s, s);
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait<STAGES - 2>();
+    cp_async_wait<T::STAGES - 2>();
     __syncthreads();
     {
-      const int nxt = kt + STAGES - 1;
-      if (nxt < nk) load_stage(nxt % STAGES, nxt);
+      const int nxt = kt + T::STAGES - 1;
+      if (nxt < nk) load_stage(nxt % T::STAGES, nxt);
       cp_async_commit();
     }
-    const double* as = As + (kt % STAGES) * T::A_STAGE;
-    const double* bs = Bs + (kt % STAGES) * T::B_STAGE;
-    const int kg0 = k_begin + kt * BK;
+    const double* as = As + (kt % T::STAGES) * T::A_STAGE;
+    const double* bs = Bs + (kt % T::STAGES) * T::B_STAGE;
+    const int kg0 = k_begin + kt * T::BK;
     if (!warp_live || kg0 >= warp_klim) continue;  // warp-uniform; barriers are at the loop top
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
+    for (int kk = 0; kk < T::BK; kk += 4) {
       double af[T::MT], bf[T::NT];
 #pragma unroll
       for (int i = 0; i < T::MT; ++i) {
@@ -286,13 +288,16 @@ static int choose_splits_t(int M, int N, int K, int flags) {
 
 // large-tile variant: 0 = 128x64 / 4 warps of 64x32, 1 = 128x64 / 8 warps
 // of 32x32 (16 warps/SM keep the DMMA pipe fed through the fragment loads),
-// 2 = 128x128 / 8 warps of 64x32.  Measured (tools/gemm_probe.py): A^T B
-// (Gram) is fastest on 0 (2.00 vs 2.15 ms at 100000 x 660), A B on 1
-// (H R^{-1} 2.00 -> 1.85 ms, H V 0.70 -> 0.62 ms).  LR_GEMM_TILE overrides.
+// 2 = 128x128 / 8 warps of 64x32, 3 = 0 with BK 32 / 2 stages (half the
+// barriers per DMMA), 4 = 1 with BK 32 / 2 stages, 5 = 64x128 / 4 warps of
+// 32x64.  Measured (tools/gemm_probe.py, profiles/r01_gemm_variants.txt):
+// A^T B (Gram) is fastest on 3 (1.95 ms at 100000 x 660; 0: 2.00, 1: 2.15),
+// A B on 4 (H R^{-1} 2.00 -> 1.77 ms, H V 0.70 -> 0.60 ms).  LR_GEMM_TILE
+// overrides.
 static int large_variant(int transA) {
   static const int v = tile_pref("LR_GEMM_TILE", -1);
   if (v >= 0) return v;
-  return transA ? 0 : 1;
+  return transA ? 3 : 4;
 }
 
 static int choose_splits(int transA, int M, int N, int K, int flags) {
@@ -301,6 +306,9 @@ static int choose_splits(int transA, int M, int N, int K, int flags) {
   switch (large_variant(1)) {
     case 1: return choose_splits_t<TileL8, true>(M, N, K, flags);
     case 2: return choose_splits_t<TileW, true>(M, N, K, flags);
+    case 3: return choose_splits_t<TileL32, true>(M, N, K, flags);
+    case 4: return choose_splits_t<TileL832, true>(M, N, K, flags);
+    case 5: return choose_splits_t<TileT, true>(M, N, K, flags);
     default: return choose_splits_t<TileL, true>(M, N, K, flags);
   }
 }
@@ -340,7 +348,7 @@ int lr_gemm_f64(int transA, int M, int N, int K, double alpha, const double* A, 
   if (K == 0 && beta == 0.0) return lr_fill_f64(C, ldc, M, N, 0.0, stream);
   int S = choose_splits(transA, M, N, K, flags);
   if (S > 1 && (work == nullptr || work_doubles < (long long)S * M * N)) S = 1;
-  int k_chunk = S > 1 ? ((K + S - 1) / S + BK - 1) / BK * BK : (K > 0 ? K : 1);
+  int k_chunk = S > 1 ? ((K + S - 1) / S + BK_ALIGN - 1) / BK_ALIGN * BK_ALIGN : (K > 0 ? K : 1);
   if (S > 1) S = (K + k_chunk - 1) / k_chunk;
   const int vec16 = (lda % 2 == 0) && (ldb % 2 == 0) && aligned16(A) && aligned16(B);
   const bool large = use_large(M, N, K, flags);
@@ -353,6 +361,12 @@ int lr_gemm_f64(int transA, int M, int N, int K, double alpha, const double* A, 
       launch<TileL8, true>(LR_GEMM_ARGS);
     else if (variant == 2)
       launch<TileW, true>(LR_GEMM_ARGS);
+    else if (variant == 3)
+      launch<TileL32, true>(LR_GEMM_ARGS);
+    else if (variant == 4)
+      launch<TileL832, true>(LR_GEMM_ARGS);
+    else if (variant == 5)
+      launch<TileT, true>(LR_GEMM_ARGS);
     else
       launch<TileL, true>(LR_GEMM_ARGS);
   } else {
@@ -362,6 +376,12 @@ int lr_gemm_f64(int transA, int M, int N, int K, double alpha, const double* A, 
       launch<TileL8, false>(LR_GEMM_ARGS);
     else if (variant == 2)
       launch<TileW, false>(LR_GEMM_ARGS);
+    else if (variant == 3)
+      launch<TileL32, false>(LR_GEMM_ARGS);
+    else if (variant == 4)
+      launch<TileL832, false>(LR_GEMM_ARGS);
+    else if (variant == 5)
+      launch<TileT, false>(LR_GEMM_ARGS);
     else
       launch<TileL, false>(LR_GEMM_ARGS);
   }

@@ -31,6 +31,7 @@ namespace cg = cooperative_groups;
 
 namespace lr {
 
+constexpr int TD_EPT = 4;  // trailing elements per thread loaded in one batch after the column barrier
 
 struct TdParams {
   const double* A;
@@ -154,11 +155,31 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
     // the same pass so both vectors cost one L2 round trip
     if (tau != 0.0) {
       double pv = 0.0;
-      for (int c = j + 1 + tid; c < n; c += THREADS) {
-        const double pc = pg[c];
-        x[c] = rg[c];
-        w[c] = pc;
-        pv = fma(pc, v[c], pv);
+      if (n - (j + 1) <= TD_EPT * THREADS) {
+        // every load of this thread in flight at once (one L2 round trip)
+        double pcs[TD_EPT], xcs[TD_EPT];
+#pragma unroll
+        for (int u = 0; u < TD_EPT; ++u) {
+          const int c = j + 1 + tid + u * THREADS;
+          pcs[u] = c < n ? __ldcg(pg + c) : 0.0;
+          xcs[u] = c < n ? __ldcg(rg + c) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < TD_EPT; ++u) {
+          const int c = j + 1 + tid + u * THREADS;
+          if (c < n) {
+            x[c] = xcs[u];
+            w[c] = pcs[u];
+            pv = fma(pcs[u], v[c], pv);
+          }
+        }
+      } else {
+        for (int c = j + 1 + tid; c < n; c += THREADS) {
+          const double pc = __ldcg(pg + c);
+          x[c] = __ldcg(rg + c);
+          w[c] = pc;
+          pv = fma(pc, v[c], pv);
+        }
       }
       pv = block_sum<THREADS>(pv, red);  // valid in thread 0
       if (tid == 0) sh[2] = 0.5 * tau * pv;
@@ -168,7 +189,7 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
     } else {
       for (int c = j + 1 + tid; c < n; c += THREADS) {
         w[c] = 0.0;
-        x[c] = rg[c];
+        x[c] = __ldcg(rg + c);
       }
     }
     __syncthreads();

@@ -182,8 +182,29 @@ def potrf_inv_dev(G, shift=0.0):
 
 # --------------------------------------------------------------------- orth
 
-def _cholqr_pass(X, shift=0.0, G=None):
-    """One CholeskyQR pass: returns (info, Q, diag(R)); G = X^T X if given."""
+class LazyQ:
+    """Q = base @ Rinv (Rinv upper triangular) kept unformed: the last
+    CholeskyQR pass of `orth` for callers that only need Y^T Q and Q V
+    (rsvd_bki's projection: (Y^T base) Rinv and base (Rinv V) -- one m x W x W
+    pass fewer).  `materialize()` forms Q once, on demand."""
+
+    def __init__(self, base, Rinv):
+        self.base, self.Rinv = base, Rinv
+        self._Q = None
+
+    @property
+    def shape(self):
+        return (int(self.base.shape[0]), int(self.Rinv.shape[1]))
+
+    def materialize(self):
+        if self._Q is None:
+            self._Q = matmul_dev(self.base, self.Rinv, b_upper=True)
+        return self._Q
+
+
+def _cholqr_pass(X, shift=0.0, G=None, lazy=False):
+    """One CholeskyQR pass: returns (info, Q, diag(R)); G = X^T X if given.
+    lazy=True returns Q as LazyQ(X, R^{-1})."""
     n = X.shape[1]
     if G is None:
         G = gram_dev(X)
@@ -191,28 +212,31 @@ def _cholqr_pass(X, shift=0.0, G=None):
     if info:
         return info, None, None
     diag = _diag_host(G, n)
-    Q = matmul_dev(X, Rinv, b_upper=True)
+    Q = LazyQ(X, Rinv) if lazy else matmul_dev(X, Rinv, b_upper=True)
     return 0, Q, diag
 
 
-def orth_dev(X):
+def orth_dev(X, lazy_last=False):
     """Orthonormal basis of range(X) (linalg.py:101-124), device in/out.
 
     ||X||_F comes from the trace of the first Gram (no extra pass over X);
-    a non-finite trace triggers the explicit finiteness check."""
+    a non-finite trace triggers the explicit finiteness check.  lazy_last
+    returns the final CholeskyQR pass unformed (LazyQ)."""
     if X.dim() != 2 or X.shape[0] < 1 or X.shape[1] < 1:
         raise ValueError(f"orth input must be 2-D with positive dims, got shape {tuple(X.shape)}")
     m, n = X.shape
     if m < n:
         raise ValueError(f"orth requires m >= n, got {m}x{n}")
     return orth_core(X, m, gram_dev, _cholqr_pass, lambda: _fro_from_stats(_check_dev(X, "orth input"), X),
-                     lambda G: _diag_host(G, n))
+                     lambda G: _diag_host(G, n), lazy_last=lazy_last)
 
 
-def orth_core(X, m, gram, cholqr, checked_norm, diag):
+def orth_core(X, m, gram, cholqr, checked_norm, diag, lazy_last=False):
     """CholeskyQR2 / shifted CholeskyQR3 with the reference's collapse test,
     over callables so a row-sharded X (shards.py: gram = local Gram +
-    allreduce, m = global rows) runs the same decisions on every rank."""
+    allreduce, m = global rows) runs the same decisions on every rank.
+    lazy_last: the last pass of the CholeskyQR2 route comes back as LazyQ
+    (cholqr must accept lazy=True); every other route is formed."""
     n = X.shape[1]
     G0 = gram(X)
     tr = float(np.sum(diag(G0)))
@@ -224,11 +248,13 @@ def orth_core(X, m, gram, cholqr, checked_norm, diag):
         raise RankDeficiencyError("cannot orthonormalize a zero matrix")
     info, Q1, d1 = cholqr(X, G=G0)
     if info == 0:
-        info2, Q, d2 = cholqr(Q1)
+        info2, Q, d2 = cholqr(Q1, lazy=True) if lazy_last else cholqr(Q1)
         if info2 == 0:
             rdiag = d2 * d1
             if np.max(np.abs(d2 - 1.0)) > 1e-6:  # Q1 was far from orthonormal: one more pass
-                info3, Q3, d3 = cholqr(Q)
+                if isinstance(Q, LazyQ):
+                    Q = Q.materialize()
+                info3, Q3, d3 = cholqr(Q, lazy=True) if lazy_last else cholqr(Q)
                 if info3 == 0:
                     Q, rdiag = Q3, d3 * rdiag
     else:
@@ -391,6 +417,35 @@ def eig_svd_dev(A, cols=None, check=True):
                  device.ptr(Sd), 1, device.ptr(B), device.ld(B), _st())
     U = matmul_dev(A, B)
     return S, V, U, cols
+
+
+def eig_svd_congruent_dev(T, Rinv, cols):
+    """eig_svd_dev of A = T Rinv without forming A (Rinv upper triangular,
+    W x W): Gram(A) = Rinv^T Gram(T) Rinv (two W^3 products instead of an
+    n x W x W one), U_sel = T (Rinv V[:, cols] / S[cols]).  Same returns as
+    eig_svd_dev."""
+    rows, n = T.shape
+    Gt = gram_dev(T)
+    if not np.isfinite(np.sum(_diag_host(Gt, n))):
+        _check_dev(T, "eig_svd input")
+    H = matmul_dev(Gt, Rinv, b_upper=True)   # Gram(T) Rinv
+    G = matmul_tn_dev(Rinv, H)               # Rinv^T Gram(T) Rinv
+    V, d = sym_eig_dev(G, symmetrize=True)   # (G + G^T)/2, as sym_eig does
+    S = gram_spectrum(device.to_host(d))
+    _native.call("lr_fix_signs_f64", device.ptr(V), device.ld(V), n, n, None, 0, 0, _st())
+    cols = np.asarray(cols, dtype=np.int64)
+    Sd = device.f64_buffer(S)
+    B = device.empty(n, cols.shape[0])
+    ci = device.int_buffer(cols)
+    _native.call("lr_scale_columns_f64", device.ptr(V), device.ld(V), n, device.ptr(ci), cols.shape[0],
+                 device.ptr(Sd), 1, device.ptr(B), device.ld(B), _st())
+    U = matmul_dev(T, tri_mul_dev(Rinv, B))
+    return S, V, U, cols
+
+
+def tri_mul_dev(Rinv, B):
+    """Rinv (upper triangular, W x W) @ B (W x c), dense small product."""
+    return matmul_dev(Rinv, B)
 
 
 def eig_svd(A) -> SvdResult:

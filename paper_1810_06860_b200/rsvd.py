@@ -29,11 +29,15 @@ import numpy as np
 
 from . import _native, device
 from .errors import RankDeficiencyError
-from .linalg import (DevSvd, SvdResult, eig_svd_dev, lu_pl_dev, matmul_dev, oracle_svd_dev, orth_dev)
+from .linalg import (DevSvd, LazyQ, SvdResult, eig_svd_congruent_dev, eig_svd_dev, lu_pl_dev, matmul_dev,
+                     oracle_svd_dev, orth_dev)
 from .rng import RngState, gaussian_matrix, gaussian_matrix_device
 from .sparse import SparseMatrix, frobenius, spmm_dev, spmm_t_dev
 
 OMEGA_SOURCE = "device"
+# rsvd_bki leaves the last CholeskyQR pass unformed (linalg.LazyQ): Y^T Q and
+# Q V run through Q1 and R2^{-1}; Subspace.Q forms Q only when asked.
+LAZY_LAST_PASS = True
 
 
 @dataclass
@@ -75,11 +79,20 @@ class Subspace:
         if isinstance(self._Q, np.ndarray):
             return self._Q
         if self._Qh is None:
-            self._Qh = device.to_host(self._Q)
+            self._Qh = device.to_host(self.Q_dev)
         return self._Qh
 
     @property
     def Q_dev(self):
+        if isinstance(self._Q, np.ndarray):
+            self._Q = device.to_device(self._Q)
+        if isinstance(self._Q, LazyQ):
+            self._Q = self._Q.materialize()
+        return self._Q
+
+    @property
+    def Q_any(self):
+        """The device basis as stored: a tensor or an unformed LazyQ."""
         if isinstance(self._Q, np.ndarray):
             self._Q = device.to_device(self._Q)
         return self._Q
@@ -128,20 +141,25 @@ def _lu_block(block, fb: _Fallback):
         _copy(U, block)
 
 
-def _orthonormalize(X, fb: _Fallback):
+def _orthonormalize(X, fb: _Fallback, lazy_last=False):
     try:
-        return orth_dev(X)
+        return orth_dev(X, lazy_last=lazy_last)
     except RankDeficiencyError as exc:
         fb.fail(exc)
         return oracle_svd_dev(X)[0]
 
 
-def _windowed_small_svd(Bt, idx, fb: _Fallback):
+def _windowed_small_svd(Bt, idx, fb: _Fallback, Rinv=None):
     """eig_svd of Bt (n x W) keeping the ascending-order columns idx (given in
     the output order).  Returns (S_sel host, V_small[:, idx] device,
-    U_small[:, idx] device).  Falls back to the dense SVD (ascending)."""
+    U_small[:, idx] device).  Falls back to the dense SVD (ascending).
+    With Rinv the matrix is Bt @ Rinv, never formed unless the fallback
+    needs it."""
     try:
-        S, V, U, cols = eig_svd_dev(Bt, cols=idx)
+        if Rinv is None:
+            S, V, U, cols = eig_svd_dev(Bt, cols=idx)
+        else:
+            S, V, U, cols = eig_svd_congruent_dev(Bt, Rinv, idx)
         Vsel = device.empty(V.shape[0], len(idx))
         ci = device.int_buffer(cols)
         _native.call("lr_scale_columns_f64", device.ptr(V), device.ld(V), V.shape[0], device.ptr(ci), len(idx),
@@ -149,6 +167,8 @@ def _windowed_small_svd(Bt, idx, fb: _Fallback):
         return S[cols], Vsel, U
     except RankDeficiencyError as exc:
         fb.fail(exc)
+        if Rinv is not None:
+            Bt = matmul_dev(Bt, Rinv, b_upper=True)
         Ud, Sd, Vd = oracle_svd_dev(Bt)  # descending
         W = Bt.shape[1]
         desc = W - 1 - np.asarray(idx)  # ascending index -> descending position
@@ -166,10 +186,16 @@ def project_and_solve(Y: SparseMatrix, Q, k: int, fb: _Fallback):
     """B^T = Y^T Q, small SVD, lift: the shared tail of Alg. 5 steps 8-10,
     recycle_q and rsvd_pi.  Returns the top-k DevSvd (descending)."""
     W = int(Q.shape[1])
-    Bt = spmm_t_dev(Y, Q)
     idx = np.arange(W - 1, W - k - 1, -1)  # top-k of the ascending order, descending
-    S_sel, Vsel, Usel = _windowed_small_svd(Bt, idx, fb)
-    U = matmul_dev(Q, Vsel)
+    if isinstance(Q, LazyQ):
+        # Q = Q1 Rinv unformed: B^T = (Y^T Q1) Rinv, U = Q1 (Rinv V_small)
+        T = spmm_t_dev(Y, Q.base)
+        S_sel, Vsel, Usel = _windowed_small_svd(T, idx, fb, Rinv=Q.Rinv)
+        U = matmul_dev(Q.base, matmul_dev(Q.Rinv, Vsel))
+    else:
+        Bt = spmm_t_dev(Y, Q)
+        S_sel, Vsel, Usel = _windowed_small_svd(Bt, idx, fb)
+        U = matmul_dev(Q, Vsel)
     return DevSvd(U, device.f64_buffer(S_sel), Usel, np.asarray(S_sel, dtype=np.float64))
 
 
@@ -189,7 +215,7 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
         spmm_t_dev(A, H[:, (i - 1) * w:i * w], out=T)
         spmm_dev(A, T, out=H[:, i * w:(i + 1) * w])
         _lu_block(H[:, i * w:(i + 1) * w], fb)
-    Q = _orthonormalize(H, fb)
+    Q = _orthonormalize(H, fb, lazy_last=LAZY_LAST_PASS)
     res = project_and_solve(A, Q, params.k, fb)
     return res, Q, fb.count
 

@@ -255,3 +255,31 @@ def test_svt_cfg3_matches_reference():
     assert got.converged == bool(g["converged"])
     pred = got.predict(g["pred_rows"], g["pred_cols"])
     np.testing.assert_allclose(pred, g["pred"], rtol=1e-8, atol=1e-8 * np.abs(g["pred"]).max())
+
+
+@pytest.mark.parametrize("shape,nnz,k,p", [((3000, 2000, ), 120000, 20, 3), ((20000, 9000), 400000, 40, 2)])
+def test_bki_unformed_last_pass_matches_formed(shape, nnz, k, p):
+    """rsvd_bki keeps the last CholeskyQR pass unformed (Q = Q1 R2^{-1},
+    linalg.LazyQ); the results must match the explicitly formed route, and
+    the subspace Q formed on access must be orthonormal."""
+    from paper_1810_06860_b200 import rsvd, workloads
+    from paper_1810_06860_b200.sparse import SparseMatrix
+
+    obs = workloads.uniform_sparse(shape[0], shape[1], nnz, seed=5)
+    A = SparseMatrix.from_coo(obs.m, obs.n, obs.rows, obs.cols, obs.values)
+    prm = rsvd.RsvdParams(k=k, p=p, s=6, seed=2)
+    old = rsvd.LAZY_LAST_PASS
+    try:
+        rsvd.LAZY_LAST_PASS = False
+        ref, sub_ref = rsvd.rsvd_bki(A, prm)
+        rsvd.LAZY_LAST_PASS = True
+        res, sub = rsvd.rsvd_bki(A, prm)
+    finally:
+        rsvd.LAZY_LAST_PASS = old
+    assert np.max(np.abs(res.S - ref.S) / ref.S) <= 1e-12
+    assert rel((res.U * res.S) @ res.V.T, (ref.U * ref.S) @ ref.V.T) <= 1e-10
+    Q = sub.Q
+    W = (k + 6) * (p + 1)
+    assert Q.shape == (shape[0], W)
+    assert np.linalg.norm(Q.T @ Q - np.eye(W)) <= 1e-12 * W
+    assert rel(Q, sub_ref.Q) <= 1e-12
