@@ -230,16 +230,39 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
 }
 
 // Sturm count: number of eigenvalues of T strictly below x
+// Sturm count (number of eigenvalues of T strictly below x) from the
+// leading-minor sequence p_i = det(T_i - x I) = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2}:
+// a sign change p_{i-1} -> p_i is a negative pivot q_i = p_i / p_{i-1} of
+// LDL^T(T - x I) -- the count dstebz takes from q_i = d_i - x - e^2/q_{i-1}.
+// The division-free form puts ONE fma on the loop-carried chain (the
+// e^2 p_{i-2} product and d_i - x are off it) instead of a ~125-cycle ddiv;
+// T is scaled by 1/||T|| and the pair (p_{i-1}, p_i) is rescaled by a power
+// of two every 8 steps (signs and ratios exact), so nothing over- or
+// underflows.  An exact zero takes the sign opposite to its predecessor (a
+// negative pivot), as a |q| < pivmin pivot does in the division form.
 __device__ __forceinline__ int sturm_count(const double* __restrict__ d, const double* __restrict__ e2, int n,
-                                           double x, double pivmin) {
-  int cnt = 0;
-  double q = d[0] - x;
-  if (fabs(q) < pivmin) q = -pivmin;
-  cnt += q < 0.0;
+                                           double x, double inv_t) {
+  const double inv_t2 = inv_t * inv_t;
+  double pm = 1.0;
+  double p = (d[0] - x) * inv_t;
+  if (p == 0.0) p = -1e-290;
+  int cnt = p < 0.0;
   for (int i = 1; i < n; ++i) {
-    q = d[i] - x - e2[i - 1] / q;
-    if (fabs(q) < pivmin) q = -pivmin;
-    cnt += q < 0.0;
+    const double a = (d[i] - x) * inv_t;
+    const double t = (e2[i - 1] * inv_t2) * pm;
+    double pn = fma(a, p, -t);
+    if (pn == 0.0) pn = (p < 0.0) ? 1e-290 : -1e-290;
+    cnt += (pn < 0.0) != (p < 0.0);
+    pm = p;
+    p = pn;
+    if ((i & 7) == 0) {
+      const long long ep = (__double_as_longlong(p) >> 52) & 0x7ff;
+      const long long eq = (__double_as_longlong(pm) >> 52) & 0x7ff;
+      const long long e = ep > eq ? ep : eq;                 // biased exponent of the larger
+      const double sc = __longlong_as_double((2046 - e) << 52);  // 2^(1023 - (e - 1023)), exact
+      p *= sc;
+      pm *= sc;
+    }
   }
   return cnt;
 }
@@ -279,6 +302,7 @@ __global__ void bisect_kernel(const double* __restrict__ d, const double* __rest
   if (k >= n) return;
   double lo = bounds[0], hi = bounds[1];
   const double pivmin = bounds[2];
+  const double inv_t = bounds[3] > 0.0 ? 1.0 / bounds[3] : 1.0;
   // absolute floor: the reduction already perturbs eigenvalues by O(eps*||T||)
   const double abs_floor = 1e-3 * 2.220446049250313e-16 * bounds[3];
   for (int it = 0; it < 40; ++it) {
@@ -287,7 +311,7 @@ __global__ void bisect_kernel(const double* __restrict__ d, const double* __rest
         width <= abs_floor)
       break;
     const double x = lo + width * (double)(lane + 1) / 33.0;
-    const int c = sturm_count(d, e2, n, x, pivmin);
+    const int c = sturm_count(d, e2, n, x, inv_t);
     // largest x with count <= k is the new lo, smallest with count > k the new hi
     const unsigned le = __ballot_sync(0xffffffffu, c <= k);
     double nlo = lo, nhi = hi;
