@@ -60,6 +60,15 @@ int lr_spmm_f64(const int* ptr, const int* idx, const double* val, int rows,
                 const double* X, long long ldx, int w, double* Y, long long ldy,
                 double* scratch, void* stream);
 
+/* fp32 mode (north_star: "optional fp32 path", singular values within 1e-4):
+ * the same SpMM over fp32 values and fp32 dense blocks (float2 per lane and
+ * column pair: half the gathered bytes of the fp64 kernel), w >= 2.  The
+ * dense linear algebra of the fp32 mode stays fp64 (rsvd.py converts the
+ * product blocks with lr_convert_*). */
+int lr_spmm_f32(const int* ptr, const int* idx, const float* val, int rows, const int* items, int n_items,
+                const int* splits, int n_splits, const float* X, long long ldx, int w, float* Y, long long ldy,
+                float* scratch, void* stream);
+
 /* x_e = sum_t U[i,t]*S[t]*V[j,t] for every stored (i,j), CSR order.
  * Replaces `project_pattern` / `_project_entries` (sparse.py:173-191). */
 int lr_sddmm_f64(const int* ptr, const int* idx, int rows, const int* items, int n_items,
@@ -188,6 +197,11 @@ int lr_gaussian_f64(unsigned long long seed, int rows, int cols, double* omega, 
 /* ------------------------------------------------------------- utilities */
 int lr_copy2d_f64(const double* src, long long lds, double* dst, long long ldd, long long rows,
                   long long cols, int reverse_cols, void* stream);
+/* Precision conversion of strided row-major blocks (round to nearest). */
+int lr_convert_f64_to_f32(const double* src, long long lds, float* dst, long long ldd, long long rows,
+                          long long cols, void* stream);
+int lr_convert_f32_to_f64(const float* src, long long lds, double* dst, long long ldd, long long rows,
+                          long long cols, void* stream);
 int lr_fill_f64(double* dst, long long ld, long long rows, long long cols, double v, void* stream);
 /* dst (cols x rows) = src^T */
 int lr_transpose_f64(const double* src, long long lds, long long rows, long long cols, double* dst,

@@ -32,6 +32,7 @@ SIGNATURES = {
     "lr_sm_count": (_I, []),
     "lr_launch_count": (_LL, []),
     "lr_spmm_f64": (_I, [_P, _P, _P, _I, _P, _I, _P, _I, _P, _LL, _I, _P, _LL, _P, _P]),
+    "lr_spmm_f32": (_I, [_P, _P, _P, _I, _P, _I, _P, _I, _P, _LL, _I, _P, _LL, _P, _P]),
     "lr_csr_transpose_workspace_ints": (_LL, [_I, _I]),
     "lr_csr_transpose_i32": (_I, [_I, _I, _LL, _P, _P, _P, _P, _P, _P, _P, _LL, _P]),
     "lr_sddmm_f64": (_I, [_P, _P, _I, _P, _I, _P, _LL, _P, _P, _LL, _I, _P, _P]),
@@ -57,6 +58,8 @@ SIGNATURES = {
     "lr_fix_signs_f64": (_I, [_P, _LL, _I, _I, _P, _LL, _I, _P]),
     "lr_scale_columns_f64": (_I, [_P, _LL, _I, _P, _I, _P, _I, _P, _LL, _P]),
     "lr_gaussian_f64": (_I, [_ULL, _I, _I, _P, _LL, _P]),
+    "lr_convert_f64_to_f32": (_I, [_P, _LL, _P, _LL, _LL, _LL, _P]),
+    "lr_convert_f32_to_f64": (_I, [_P, _LL, _P, _LL, _LL, _LL, _P]),
     "lr_copy2d_f64": (_I, [_P, _LL, _P, _LL, _LL, _LL, _I, _P]),
     "lr_fill_f64": (_I, [_P, _LL, _LL, _LL, _D, _P]),
     "lr_transpose_f64": (_I, [_P, _LL, _LL, _LL, _P, _LL, _P]),

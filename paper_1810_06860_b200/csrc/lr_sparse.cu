@@ -37,22 +37,39 @@ __device__ __forceinline__ Item load_item(const int* __restrict__ items, const i
 }
 
 // ------------------------------------------------------------------- SpMM
+// Scalar traits: the fp64 path moves double2 (16 B) per lane and column
+// pair, the optional fp32 path (north_star "fp32 mode") float2 (8 B), so
+// every gathered row costs half the L2 bytes.
+template <typename Sc>
+struct Vec2T;
+template <>
+struct Vec2T<double> {
+  using type = double2;
+  static __device__ __forceinline__ double2 make(double a, double b) { return make_double2(a, b); }
+};
+template <>
+struct Vec2T<float> {
+  using type = float2;
+  static __device__ __forceinline__ float2 make(float a, float b) { return make_float2(a, b); }
+};
+
 // A group of G lanes owns one item; lane g covers column pairs
 // c = 2*(g + G*t), t < T, of a column tile of width 2*G*T starting at c0.
 // VEC2: double2 loads/stores (requires 16B-aligned rows); tail columns scalar.
 // Q: stored entries per lane kept in flight (4; 8 for one-pair-per-lane
 // narrow products, whose gathers are too small to cover the L2 latency)
-template <int G, int T, bool VEC2, int Q = 4>
 #ifndef LR_SPMM_MINB
 #define LR_SPMM_MINB 4
 #endif
+template <int G, int T, bool VEC2, int Q = 4, typename Sc = double>
 __global__ void __launch_bounds__(256, LR_SPMM_MINB) spmm_kernel(const int* __restrict__ ptr,
                                                    const int* __restrict__ idx,
-                                                   const double* __restrict__ val,
+                                                   const Sc* __restrict__ val,
                                                    const int* __restrict__ items, int n_items,
-                                                   const double* __restrict__ X, long long ldx, int w,
-                                                   double* __restrict__ Y, long long ldy,
-                                                   double* __restrict__ scratch, int n_tiles) {
+                                                   const Sc* __restrict__ X, long long ldx, int w,
+                                                   Sc* __restrict__ Y, long long ldy,
+                                                   Sc* __restrict__ scratch, int n_tiles) {
+  using V2 = typename Vec2T<Sc>::type;
   constexpr int GROUPS = 32 / G;
   constexpr int TILE = 2 * G * T;  // columns per tile
   const int lane = threadIdx.x & 31;
@@ -69,33 +86,33 @@ __global__ void __launch_bounds__(256, LR_SPMM_MINB) spmm_kernel(const int* __re
     Item it{0, 0, 0, -1};
     if (active) it = load_item(items, ptr, item_i);
     const int c0 = tile * TILE;
-    double2 acc[T];
+    V2 acc[T];
 #pragma unroll
-    for (int t = 0; t < T; ++t) acc[t] = make_double2(0.0, 0.0);
+    for (int t = 0; t < T; ++t) acc[t] = Vec2T<Sc>::make(Sc(0), Sc(0));
 
     if (active) {
       int e = it.beg;
       // process Q entries per step for memory-level parallelism
       for (; e + Q <= it.end; e += Q) {
         int cj[Q];
-        double vj[Q];
+        Sc vj[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
           cj[q] = __ldg(idx + e + q);
           vj[q] = __ldg(val + e + q);
         }
-        double2 xv[Q][T];
+        V2 xv[Q][T];
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-          const double* xr = X + (long long)cj[q] * ldx + c0;
+          const Sc* xr = X + (long long)cj[q] * ldx + c0;
 #pragma unroll
           for (int t = 0; t < T; ++t) {
             const int c = 2 * (g + G * t);
             if (VEC2 && c0 + c + 1 < w) {
-              xv[q][t] = __ldg(reinterpret_cast<const double2*>(xr + c));
+              xv[q][t] = __ldg(reinterpret_cast<const V2*>(xr + c));
             } else {
-              xv[q][t].x = (c0 + c < w) ? __ldg(xr + c) : 0.0;
-              xv[q][t].y = (c0 + c + 1 < w) ? __ldg(xr + c + 1) : 0.0;
+              xv[q][t].x = (c0 + c < w) ? __ldg(xr + c) : Sc(0);
+              xv[q][t].y = (c0 + c + 1 < w) ? __ldg(xr + c + 1) : Sc(0);
             }
           }
         }
@@ -109,30 +126,30 @@ __global__ void __launch_bounds__(256, LR_SPMM_MINB) spmm_kernel(const int* __re
       }
       for (; e < it.end; ++e) {
         const int cj = __ldg(idx + e);
-        const double vj = __ldg(val + e);
-        const double* xr = X + (long long)cj * ldx + c0;
+        const Sc vj = __ldg(val + e);
+        const Sc* xr = X + (long long)cj * ldx + c0;
 #pragma unroll
         for (int t = 0; t < T; ++t) {
           const int c = 2 * (g + G * t);
-          double2 xv;
+          V2 xv;
           if (VEC2 && c0 + c + 1 < w) {
-            xv = __ldg(reinterpret_cast<const double2*>(xr + c));
+            xv = __ldg(reinterpret_cast<const V2*>(xr + c));
           } else {
-            xv.x = (c0 + c < w) ? __ldg(xr + c) : 0.0;
-            xv.y = (c0 + c + 1 < w) ? __ldg(xr + c + 1) : 0.0;
+            xv.x = (c0 + c < w) ? __ldg(xr + c) : Sc(0);
+            xv.y = (c0 + c + 1 < w) ? __ldg(xr + c + 1) : Sc(0);
           }
           acc[t].x = fma(vj, xv.x, acc[t].x);
           acc[t].y = fma(vj, xv.y, acc[t].y);
         }
       }
-      double* dst = (it.slot >= 0) ? (scratch + (long long)it.slot * w + c0)
+      Sc* dst = (it.slot >= 0) ? (scratch + (long long)it.slot * w + c0)
                                    : (Y + (long long)it.row * ldy + c0);
       const bool dst_vec = VEC2 && (it.slot < 0 || (w % 2 == 0));
 #pragma unroll
       for (int t = 0; t < T; ++t) {
         const int c = 2 * (g + G * t);
         if (dst_vec && c0 + c + 1 < w) {
-          *reinterpret_cast<double2*>(dst + c) = acc[t];
+          *reinterpret_cast<V2*>(dst + c) = acc[t];
         } else {
           if (c0 + c < w) dst[c] = acc[t].x;
           if (c0 + c + 1 < w) dst[c + 1] = acc[t].y;
@@ -143,15 +160,16 @@ __global__ void __launch_bounds__(256, LR_SPMM_MINB) spmm_kernel(const int* __re
 }
 
 // sum partial rows of split items, in slot order
+template <typename Sc>
 __global__ void spmm_split_reduce_kernel(const int* __restrict__ splits, int n_splits,
-                                         const double* __restrict__ scratch, int w,
-                                         double* __restrict__ Y, long long ldy) {
+                                         const Sc* __restrict__ scratch, int w,
+                                         Sc* __restrict__ Y, long long ldy) {
   const long long total = (long long)n_splits * w;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
     const int s = (int)(t / w), c = (int)(t - (long long)s * w);
     const int4 sp = reinterpret_cast<const int4*>(splits)[s];
-    double acc = 0.0;
+    Sc acc = Sc(0);
     for (int k = sp.y; k < sp.z; ++k) acc += scratch[(long long)k * w + c];
     Y[(long long)sp.x * ldy + c] = acc;
   }
@@ -370,10 +388,10 @@ __global__ void pattern_axpy_kernel(double* __restrict__ y_csr, double* __restri
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-template <int G, int T, bool V2, int Q = 4>
-static void launch_spmm_t(const int* ptr, const int* idx, const double* val, const int* items,
-                          int n_items, const double* X, long long ldx, int w, double* Y,
-                          long long ldy, double* scratch, cudaStream_t s) {
+template <int G, int T, bool V2, int Q = 4, typename Sc = double>
+static void launch_spmm_t(const int* ptr, const int* idx, const Sc* val, const int* items,
+                          int n_items, const Sc* X, long long ldx, int w, Sc* Y,
+                          long long ldy, Sc* scratch, cudaStream_t s) {
   constexpr int TILE = 2 * G * T;
   const int n_tiles = (w + TILE - 1) / TILE;
   constexpr int GROUPS = 32 / G;
@@ -382,18 +400,18 @@ static void launch_spmm_t(const int* ptr, const int* idx, const double* val, con
   long long cap = (long long)sm_count() * 16;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  spmm_kernel<G, T, V2, Q><<<(int)blocks, 256, 0, s>>>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy,
-                                                       scratch, n_tiles);
+  spmm_kernel<G, T, V2, Q, Sc><<<(int)blocks, 256, 0, s>>>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy,
+                                                           scratch, n_tiles);
 }
 
 // (G, T) per width: G lanes per item, T column pairs per lane.  Narrow
 // products use few lanes and several pairs per lane so a warp keeps 4-16
 // items (gathers) in flight and no lane idles on padding columns;
 // LR_SPMM_GT="G,T" overrides for experiments.
-template <bool V2>
-static void dispatch_spmm(const int* ptr, const int* idx, const double* val, const int* items,
-                          int n_items, const double* X, long long ldx, int w, double* Y,
-                          long long ldy, double* scratch, cudaStream_t s) {
+template <bool V2, typename Sc = double>
+static void dispatch_spmm(const int* ptr, const int* idx, const Sc* val, const int* items,
+                          int n_items, const Sc* X, long long ldx, int w, Sc* Y,
+                          long long ldy, Sc* scratch, cudaStream_t s) {
   const int pairs = (w + 1) / 2;
   static const char* env = getenv("LR_SPMM_GT");
   int G = 0, T = 0;
@@ -414,9 +432,9 @@ static void dispatch_spmm(const int* ptr, const int* idx, const double* val, con
   if (G == g && T == t) {                                                                               \
     if constexpr (t == 1) {                                                                             \
       if (Qv == 8)                                                                                      \
-        return launch_spmm_t<g, t, V2, 8>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s); \
+        return launch_spmm_t<g, t, V2, 8, Sc>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s); \
     }                                                                                                   \
-    return launch_spmm_t<g, t, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);        \
+    return launch_spmm_t<g, t, V2, 4, Sc>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);        \
   }
   LR_SPMM_CASE(1, 1) LR_SPMM_CASE(2, 1) LR_SPMM_CASE(4, 1) LR_SPMM_CASE(8, 1) LR_SPMM_CASE(16, 1)
   LR_SPMM_CASE(32, 1) LR_SPMM_CASE(32, 2) LR_SPMM_CASE(32, 3)
@@ -424,7 +442,47 @@ static void dispatch_spmm(const int* ptr, const int* idx, const double* val, con
   LR_SPMM_CASE(4, 4) LR_SPMM_CASE(8, 2) LR_SPMM_CASE(8, 3) LR_SPMM_CASE(8, 4) LR_SPMM_CASE(16, 2)
   LR_SPMM_CASE(16, 3)
 #undef LR_SPMM_CASE
-  launch_spmm_t<32, 3, V2>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+  launch_spmm_t<32, 3, V2, 4, Sc>(ptr, idx, val, items, n_items, X, ldx, w, Y, ldy, scratch, s);
+}
+
+static bool aligned_bytes(const void* p, unsigned a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
+
+// Column-chunked SpMM over a row-compressed pattern, w >= 2 (shared by the
+// fp64 and fp32 entry points)
+template <typename Sc>
+static int spmm_cols(const int* ptr, const int* idx, const Sc* val, const int* items, int n_items,
+                     const int* splits, int n_splits, const Sc* X, long long ldx, int w, Sc* Y, long long ldy,
+                     Sc* scratch, cudaStream_t s) {
+  // Products wider than kChunkCols run as column chunks: each chunk's slice
+  // of X stays L2-resident while every stored entry gathers from it (the
+  // W-column Y^T Q of BKI at cfg2 is 528 MB), and the <= 128-column tiles run
+  // at higher occupancy than the 192-column one even when X fits in L2
+  // (cfg4 CSR w = 132: 2.64 ms chunked vs 4.04 ms whole, tools/spmm_cfg4_probe.py).
+  constexpr int kChunkCols = 128;
+  constexpr unsigned kVecBytes = 2 * sizeof(Sc);
+  const int n_chunks = (w + kChunkCols - 1) / kChunkCols;
+  const int cw_even = (((w + n_chunks - 1) / n_chunks) + 1) & ~1;
+  for (int c0 = 0; c0 < w; c0 += cw_even) {
+    const int cw = (w - c0 < cw_even) ? (w - c0) : cw_even;
+    const Sc* Xc = X + c0;
+    Sc* Yc = Y + c0;
+    const bool v2 = (ldx % 2 == 0) && (ldy % 2 == 0) && aligned_bytes(Xc, kVecBytes) &&
+                    aligned_bytes(Yc, kVecBytes) &&
+                    (scratch == nullptr || (aligned_bytes(scratch, kVecBytes) && cw % 2 == 0));
+    if (v2)
+      dispatch_spmm<true, Sc>(ptr, idx, val, items, n_items, Xc, ldx, cw, Yc, ldy, scratch, s);
+    else
+      dispatch_spmm<false, Sc>(ptr, idx, val, items, n_items, Xc, ldx, cw, Yc, ldy, scratch, s);
+    LR_CHECK_LAUNCH();
+    if (n_splits > 0) {
+      long long total = (long long)n_splits * cw;
+      long long blocks = (total + 255) / 256;
+      if (blocks > sm_count() * 8) blocks = sm_count() * 8;
+      spmm_split_reduce_kernel<Sc><<<(int)blocks, 256, 0, s>>>(splits, n_splits, scratch, cw, Yc, ldy);
+      LR_CHECK_LAUNCH();
+    }
+  }
+  return LR_OK;
 }
 
 }  // namespace lr
@@ -454,39 +512,24 @@ int lr_spmm_f64(const int* ptr, const int* idx, const double* val, int rows, con
     if (n_splits > 0) {
       long long rb = ((long long)n_splits + 255) / 256;
       if (rb > sm_count() * 8) rb = sm_count() * 8;
-      spmm_split_reduce_kernel<<<(int)rb, 256, 0, s>>>(splits, n_splits, scratch, 1, Y, ldy);
+      spmm_split_reduce_kernel<double><<<(int)rb, 256, 0, s>>>(splits, n_splits, scratch, 1, Y, ldy);
       LR_CHECK_LAUNCH();
     }
     return LR_OK;
   }
-  // Products wider than kChunkCols run as column chunks: each chunk's slice
-  // of X stays L2-resident while every stored entry gathers from it (the
-  // W-column Y^T Q of BKI at cfg2 is 528 MB), and the <= 128-column tiles run
-  // at higher occupancy than the 192-column one even when X fits in L2
-  // (cfg4 CSR w = 132: 2.64 ms chunked vs 4.04 ms whole, tools/spmm_cfg4_probe.py).
-  constexpr int kChunkCols = 128;
-  const int n_chunks = (w + kChunkCols - 1) / kChunkCols;
-  const int cw_even = (((w + n_chunks - 1) / n_chunks) + 1) & ~1;
-  for (int c0 = 0; c0 < w; c0 += cw_even) {
-    const int cw = (w - c0 < cw_even) ? (w - c0) : cw_even;
-    const double* Xc = X + c0;
-    double* Yc = Y + c0;
-    const bool v2 = (ldx % 2 == 0) && (ldy % 2 == 0) && aligned16(Xc) && aligned16(Yc) &&
-                    (scratch == nullptr || (aligned16(scratch) && cw % 2 == 0));
-    if (v2)
-      dispatch_spmm<true>(ptr, idx, val, items, n_items, Xc, ldx, cw, Yc, ldy, scratch, s);
-    else
-      dispatch_spmm<false>(ptr, idx, val, items, n_items, Xc, ldx, cw, Yc, ldy, scratch, s);
-    LR_CHECK_LAUNCH();
-    if (n_splits > 0) {
-      long long total = (long long)n_splits * cw;
-      long long blocks = (total + 255) / 256;
-      if (blocks > sm_count() * 8) blocks = sm_count() * 8;
-      spmm_split_reduce_kernel<<<(int)blocks, 256, 0, s>>>(splits, n_splits, scratch, cw, Yc, ldy);
-      LR_CHECK_LAUNCH();
-    }
-  }
-  return LR_OK;
+  return spmm_cols<double>(ptr, idx, val, items, n_items, splits, n_splits, X, ldx, w, Y, ldy, scratch, s);
+}
+
+int lr_spmm_f32(const int* ptr, const int* idx, const float* val, int rows, const int* items, int n_items,
+                const int* splits, int n_splits, const float* X, long long ldx, int w, float* Y, long long ldy,
+                float* scratch, void* stream) {
+  LR_REQUIRE(w >= 2 && ldx >= w && ldy >= w, "spmm_f32: bad widths (w=%d ldx=%lld ldy=%lld; w >= 2)", w, ldx,
+             ldy);
+  if (rows == 0) return LR_OK;
+  if (!items) n_items = rows;
+  LR_REQUIRE(n_splits == 0 || scratch, "spmm_f32: split schedule needs scratch");
+  return spmm_cols<float>(ptr, idx, val, items, n_items, splits, n_splits, X, ldx, w, Y, ldy, scratch,
+                          as_stream(stream));
 }
 
 static int launch_sddmm(bool fused, const int* ptr, const int* idx, int rows, const int* items,

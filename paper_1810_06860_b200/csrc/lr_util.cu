@@ -189,6 +189,27 @@ __global__ void copy2d_kernel(const double* __restrict__ src, long long lds, dou
   }
 }
 
+// precision conversion of a strided block: a warp per row, lanes across the
+// columns (no per-element index division); fp64 -> fp32 rounds to nearest
+template <typename Src, typename Dst>
+__global__ void convert2d_kernel(const Src* __restrict__ src, long long lds, Dst* __restrict__ dst, long long ldd,
+                                 long long rows, long long cols) {
+  if (rows == 1 || (lds == cols && ldd == cols)) {  // contiguous: one flat grid-stride sweep
+    const long long total = rows * cols;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x)
+      dst[t] = static_cast<Dst>(src[t]);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
+    const Src* s = src + r * lds;
+    Dst* d = dst + r * ldd;
+    for (long long c = lane; c < cols; c += 32) d[c] = static_cast<Dst>(s[c]);
+  }
+}
+
 __global__ void fill_kernel(double* dst, long long ld, long long rows, long long cols, double v) {
   const long long total = rows * cols;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
@@ -336,6 +357,30 @@ int lr_copy2d_f64(const double* src, long long lds, double* dst, long long ldd, 
   if (rows * cols == 0) return LR_OK;
   copy2d_kernel<<<grid_for(rows * cols, 256), 256, 0, as_stream(stream)>>>(src, lds, dst, ldd, rows,
                                                                           cols, reverse_cols);
+  LR_CHECK_LAUNCH();
+  return LR_OK;
+}
+
+static int convert_grid(long long rows, long long cols) {
+  long long b = rows == 1 ? (cols + 255) / 256 : (rows + 7) / 8;  // flat, or 8 warps (rows) per block
+  const long long cap = (long long)sm_count() * 16;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+int lr_convert_f64_to_f32(const double* src, long long lds, float* dst, long long ldd, long long rows,
+                          long long cols, void* stream) {
+  LR_REQUIRE(rows >= 0 && cols >= 0 && lds >= cols && ldd >= cols, "convert: bad shape");
+  if (rows * cols == 0) return LR_OK;
+  convert2d_kernel<double, float><<<convert_grid(rows, cols), 256, 0, as_stream(stream)>>>(src, lds, dst, ldd, rows, cols);
+  LR_CHECK_LAUNCH();
+  return LR_OK;
+}
+
+int lr_convert_f32_to_f64(const float* src, long long lds, double* dst, long long ldd, long long rows,
+                          long long cols, void* stream) {
+  LR_REQUIRE(rows >= 0 && cols >= 0 && lds >= cols && ldd >= cols, "convert: bad shape");
+  if (rows * cols == 0) return LR_OK;
+  convert2d_kernel<float, double><<<convert_grid(rows, cols), 256, 0, as_stream(stream)>>>(src, lds, dst, ldd, rows, cols);
   LR_CHECK_LAUNCH();
   return LR_OK;
 }

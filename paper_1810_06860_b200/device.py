@@ -56,6 +56,37 @@ def empty(rows: int, cols: int) -> torch.Tensor:
     return base[:rows, :cols]
 
 
+def empty32(rows: int, cols: int) -> torch.Tensor:
+    """fp32 row-major block (fp32 mode), even leading dimension (8-byte
+    aligned rows for the float2 SpMM path)."""
+    dev = require_cuda()
+    base = torch.empty((max(rows, 1), padded_ld(cols)), dtype=torch.float32, device=dev)
+    return base[:rows, :cols]
+
+
+def to_f32(x, out=None) -> torch.Tensor:
+    """fp64 device block -> fp32 device block (lr_convert_f64_to_f32)."""
+    from . import _native
+
+    rows, cols = (int(x.shape[0]), int(x.shape[1])) if x.dim() == 2 else (1, int(x.shape[0]))
+    if out is None:
+        out = empty32(rows, cols) if x.dim() == 2 else torch.empty(cols, dtype=torch.float32, device=x.device)
+    _native.call("lr_convert_f64_to_f32", ptr(x), ld(x) if x.dim() == 2 else cols, ptr(out),
+                 ld(out) if out.dim() == 2 else cols, rows, cols, stream())
+    return out
+
+
+def to_f64(x, out=None) -> torch.Tensor:
+    """fp32 device block -> fp64 device block (lr_convert_f32_to_f64)."""
+    from . import _native
+
+    rows, cols = int(x.shape[0]), int(x.shape[1])
+    if out is None:
+        out = empty(rows, cols)
+    _native.call("lr_convert_f32_to_f64", ptr(x), ld(x), ptr(out), ld(out), rows, cols, stream())
+    return out
+
+
 def zeros(rows: int, cols: int) -> torch.Tensor:
     t = empty(rows, cols)
     if rows and cols:

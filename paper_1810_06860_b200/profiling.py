@@ -21,8 +21,11 @@ import torch
 
 
 def spmm_model(meta):
+    """fp64: value 8 B + index 4 B per entry; fp32 mode (bytes_per_value 4):
+    value 4 B + index 4 B and 4 B per dense element."""
     nnz, r, c, w = meta["nnz"], meta["rows"], meta["cols"], meta["w"]
-    return 12 * nnz + 4 * (r + 1) + 8 * c * w + 8 * r * w, 2 * nnz * w
+    b = meta.get("bytes_per_value", 8)
+    return (b + 4) * nnz + 4 * (r + 1) + b * c * w + b * r * w, 2 * nnz * w
 
 
 def svt_model(meta):
@@ -38,7 +41,8 @@ def gemm_model(meta):
     return 8 * (M * K + K * N + M * N), flops
 
 
-MODELS = {"lr_spmm_f64": ("hbm", spmm_model), "lr_svt_step_f64": ("hbm", svt_model),
+MODELS = {"lr_spmm_f64": ("hbm", spmm_model), "lr_spmm_f32": ("hbm", spmm_model),
+          "lr_svt_step_f64": ("hbm", svt_model),
           "lr_gemm_f64": ("tensor", gemm_model)}
 
 

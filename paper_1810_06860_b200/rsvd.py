@@ -32,12 +32,13 @@ from .errors import RankDeficiencyError
 from .linalg import (DevSvd, LazyQ, SvdResult, eig_svd_congruent_dev, eig_svd_dev, lu_pl_dev, matmul_dev,
                      oracle_svd_dev, orth_dev)
 from .rng import RngState, gaussian_matrix, gaussian_matrix_device
-from .sparse import SparseMatrix, frobenius, spmm_dev, spmm_t_dev
+from .sparse import SparseMatrix, frobenius, spmm_dev, spmm_dev32, spmm_t_dev, spmm_t_dev32
 
 OMEGA_SOURCE = "device"
 # rsvd_bki leaves the last CholeskyQR pass unformed (linalg.LazyQ): Y^T Q and
 # Q V run through Q1 and R2^{-1}; Subspace.Q forms Q only when asked.
 LAZY_LAST_PASS = True
+LAZY_MIN_FLOPS = 1 << 30  # m * W^2 below this: form Q (the GEMM is a few microseconds)
 
 
 @dataclass
@@ -182,47 +183,83 @@ def _windowed_small_svd(Bt, idx, fb: _Fallback, Rinv=None):
         return Sd[desc], Vsel, Usel
 
 
-def project_and_solve(Y: SparseMatrix, Q, k: int, fb: _Fallback):
+def _spmm_t_prec(Y: SparseMatrix, X, precision: str):
+    """Y^T X in the requested precision; the fp32 product comes back fp64."""
+    if precision == "fp32" and int(X.shape[1]) >= 2:
+        return device.to_f64(spmm_t_dev32(Y, device.to_f32(X)))
+    return spmm_t_dev(Y, X)
+
+
+def project_and_solve(Y: SparseMatrix, Q, k: int, fb: _Fallback, precision: str = "fp64"):
     """B^T = Y^T Q, small SVD, lift: the shared tail of Alg. 5 steps 8-10,
     recycle_q and rsvd_pi.  Returns the top-k DevSvd (descending)."""
     W = int(Q.shape[1])
     idx = np.arange(W - 1, W - k - 1, -1)  # top-k of the ascending order, descending
     if isinstance(Q, LazyQ):
         # Q = Q1 Rinv unformed: B^T = (Y^T Q1) Rinv, U = Q1 (Rinv V_small)
-        T = spmm_t_dev(Y, Q.base)
+        T = _spmm_t_prec(Y, Q.base, precision)
         S_sel, Vsel, Usel = _windowed_small_svd(T, idx, fb, Rinv=Q.Rinv)
         U = matmul_dev(Q.base, matmul_dev(Q.Rinv, Vsel))
     else:
-        Bt = spmm_t_dev(Y, Q)
+        Bt = _spmm_t_prec(Y, Q, precision)
         S_sel, Vsel, Usel = _windowed_small_svd(Bt, idx, fb)
         U = matmul_dev(Q, Vsel)
     return DevSvd(U, device.f64_buffer(S_sel), Usel, np.asarray(S_sel, dtype=np.float64))
 
 
-def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, omega=None):
-    """Device Alg. 5 -> (DevSvd, Q device, fallbacks)."""
+def _check_precision(precision: str) -> str:
+    if precision not in ("fp64", "fp32"):
+        raise ValueError(f"precision must be 'fp64' or 'fp32', got {precision!r}")
+    return precision
+
+
+def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, omega=None,
+                 precision: str = "fp64"):
+    """Device Alg. 5 -> (DevSvd, Q device, fallbacks).
+
+    precision="fp32" (north_star's optional fp32 mode, singular values within
+    1e-4): the sparse products run on fp32 values and fp32 blocks (half the
+    gathered bytes); LU, CholeskyQR, the eigensolver and the lifts stay fp64
+    on the converted blocks."""
     params.check_against(A, krylov=True)
+    fp32 = _check_precision(precision) == "fp32" and params.k + params.s >= 2
     fb = _Fallback(allow_fallback, "Krylov blocks are near-collinear, reduce p or use a larger matrix")
     w = params.k + params.s
     W = w * (params.p + 1)
     m, n = A.shape
     Om = _omega(params.seed, n, w, omega or OMEGA_SOURCE)
     H = device.empty(m, W)
-    spmm_dev(A, Om, out=H[:, 0:w])
+    if fp32:
+        H32, T32 = device.empty32(m, w), device.empty32(n, w)
+        spmm_dev32(A, device.to_f32(Om), out=H32)
+        device.to_f64(H32, out=H[:, 0:w])
+    else:
+        spmm_dev(A, Om, out=H[:, 0:w])
     _lu_block(H[:, 0:w], fb)
-    T = device.empty(n, w)
+    T = None if fp32 else device.empty(n, w)
     for i in range(1, params.p + 1):
-        spmm_t_dev(A, H[:, (i - 1) * w:i * w], out=T)
-        spmm_dev(A, T, out=H[:, i * w:(i + 1) * w])
+        if fp32:
+            device.to_f32(H[:, (i - 1) * w:i * w], out=H32)
+            spmm_t_dev32(A, H32, out=T32)
+            spmm_dev32(A, T32, out=H32)
+            device.to_f64(H32, out=H[:, i * w:(i + 1) * w])
+        else:
+            spmm_t_dev(A, H[:, (i - 1) * w:i * w], out=T)
+            spmm_dev(A, T, out=H[:, i * w:(i + 1) * w])
         _lu_block(H[:, i * w:(i + 1) * w], fb)
-    Q = _orthonormalize(H, fb, lazy_last=LAZY_LAST_PASS)
-    res = project_and_solve(A, Q, params.k, fb)
+    # small blocks (launch-bound, e.g. cfg1's 1000 x 64): forming Q is cheaper
+    # than the extra small products of the unformed route
+    lazy = LAZY_LAST_PASS and m * W * W >= LAZY_MIN_FLOPS
+    Q = _orthonormalize(H, fb, lazy_last=lazy)
+    res = project_and_solve(A, Q, params.k, fb, "fp32" if fp32 else "fp64")
     return res, Q, fb.count
 
 
-def rsvd_bki(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, *, omega=None):
-    """Rank-k randomized SVD by block Krylov iteration (descending)."""
-    res, Q, nfb = rsvd_bki_dev(A, params, allow_fallback, omega)
+def rsvd_bki(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, *, omega=None,
+             precision: str = "fp64"):
+    """Rank-k randomized SVD by block Krylov iteration (descending).
+    precision="fp32": the optional fp32 mode (sparse products in fp32)."""
+    res, Q, nfb = rsvd_bki_dev(A, params, allow_fallback, omega, precision)
     return res.to_host(), Subspace(Q, "bki", params.p, nfb)
 
 

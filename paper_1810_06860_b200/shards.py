@@ -253,6 +253,7 @@ class DeviceKernels:
                      device.ptr(part), npart, device.ptr(out2), device.stream(),
                      meta={"nnz": A.nnz, "m": A.rows, "n": A.cols, "r": r})
         A._host_stale = True
+        A._dvals32 = None
         return out2
 
     def project(self, A, U, S_dev, V, r):

@@ -339,6 +339,16 @@ class SparseMatrix:
             self._dvals = self.pattern().values(self._data)
         return self._dvals
 
+    def device_values32(self):
+        """(csr, csc) fp32 copies of the device values (fp32 mode), rounded
+        from the fp64 copies once per value state."""
+        vals = self.device_values()
+        cached = getattr(self, "_dvals32", None)
+        if cached is None or cached[0] is not vals:
+            cached = (vals, device.to_f32(vals[0]), device.to_f32(vals[1]))
+            self._dvals32 = cached
+        return cached[1], cached[2]
+
 
 # --------------------------------------------------------------- kernels
 
@@ -356,6 +366,33 @@ def _spmm_side(side: _Side, vals, X, out=None):
                  device.ptr(out), device.ld(out), device.ptr(scratch), device.stream(),
                  meta={"nnz": int(side.idx.numel()), "rows": side.rows, "cols": int(X.shape[0]), "w": w})
     return out
+
+
+def _spmm_side32(side: _Side, vals32, X32, out=None):
+    rows_out = side.rows
+    w = int(X32.shape[1])
+    if out is None:
+        out = device.empty32(rows_out, w)
+    scratch = None
+    if side.n_splits:  # fp32 partial rows fit the fp64 arena buffer
+        scratch = device.arena().get("spmm_scratch", (side.n_slots * max(w, 1) + 3) // 2 + 2)
+    _native.call("lr_spmm_f32", device.ptr(side.ptr), device.ptr(side.idx), device.ptr(vals32), side.rows,
+                 device.ptr(side.items), side.n_items if side.items is not None else side.rows,
+                 device.ptr(side.splits), side.n_splits, device.ptr(X32), device.ld(X32), w,
+                 device.ptr(out), device.ld(out), device.ptr(scratch), device.stream(),
+                 meta={"nnz": int(side.idx.numel()), "rows": side.rows, "cols": int(X32.shape[0]), "w": w,
+                       "bytes_per_value": 4})
+    return out
+
+
+def spmm_dev32(A: SparseMatrix, X32, out=None):
+    """fp32 mode: Y @ X with fp32 values and fp32 blocks (w >= 2)."""
+    return _spmm_side32(A.pattern().csr, A.device_values32()[0], X32, out)
+
+
+def spmm_t_dev32(A: SparseMatrix, H32, out=None):
+    """fp32 mode: Y^T @ H with fp32 values and fp32 blocks (w >= 2)."""
+    return _spmm_side32(A.pattern().csc, A.device_values32()[1], H32, out)
 
 
 def spmm_dev(A: SparseMatrix, X, out=None):
@@ -469,6 +506,7 @@ def update_pattern_values(Y: SparseMatrix, delta_vals) -> SparseMatrix:
     _native.call("lr_pattern_axpy_f64", device.ptr(vc), device.ptr(vt), device.ptr(Y.pattern().inv_perm),
                  device.ptr(d), 1.0, Y.nnz, device.stream())
     Y._host_stale = True
+    Y._dvals32 = None
     return Y
 
 

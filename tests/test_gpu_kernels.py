@@ -371,3 +371,41 @@ def test_device_transpose_matches_host_stable_argsort(case):
     assert np.array_equal(device.to_host(dp.inv_perm)[:A.nnz], inv), name
     vc, vt = A.device_values()
     assert np.array_equal(device.to_host(vt)[:A.nnz], A.data[perm]), name
+
+
+@pytest.mark.parametrize("w", [2, 3, 16, 45, 110, 300])
+def test_spmm_f32_matches_rounded_product(w):
+    """fp32 mode kernel: against the fp64 product of the fp32-rounded inputs,
+    within fp32 accumulation error (long rows and split items included)."""
+    import torch
+
+    from paper_1810_06860_b200 import device
+    from paper_1810_06860_b200.sparse import SparseMatrix, spmm_dev32, spmm_t_dev32
+
+    m, n = 700, 1300
+    i, j, v = rand_pattern(m, n, 20000, seed=w, long_rows=2, long_cols=1)
+    A = SparseMatrix.from_coo(m, n, i, j, v)
+    P = oracle.csr_from_triples(m, n, i, j, v)
+    P32 = oracle.csr_from_triples(m, n, i, j, np.asarray(v, dtype=np.float32).astype(np.float64))
+    rng = np.random.default_rng(200 + w)
+    X = rng.standard_normal((n, w)).astype(np.float32)
+    H = rng.standard_normal((m, w)).astype(np.float32)
+    Y32 = spmm_dev32(A, device.to_f32(device.to_device(X.astype(np.float64))))
+    Yt32 = spmm_t_dev32(A, device.to_f32(device.to_device(H.astype(np.float64))))
+    assert Y32.dtype == torch.float32 and Yt32.dtype == torch.float32
+    ref = oracle.csr_times_dense(P32, X.astype(np.float64))
+    ref_t = oracle.csr_t_times_dense(P32, H.astype(np.float64))
+    got = device.to_host(device.to_f64(Y32))
+    got_t = device.to_host(device.to_f64(Yt32))
+    assert np.linalg.norm(got - ref) <= 2e-6 * np.linalg.norm(ref)
+    assert np.linalg.norm(got_t - ref_t) <= 2e-6 * np.linalg.norm(ref_t)
+
+
+def test_convert_roundtrip_and_rounding():
+    from paper_1810_06860_b200 import device
+
+    x = np.random.default_rng(3).standard_normal((37, 29)) * 1e3
+    d = device.to_device(x)
+    f = device.to_f32(d)
+    back = device.to_host(device.to_f64(f))
+    np.testing.assert_array_equal(back, x.astype(np.float32).astype(np.float64))

@@ -263,19 +263,21 @@ def test_bki_unformed_last_pass_matches_formed(shape, nnz, k, p):
     linalg.LazyQ); the results must match the explicitly formed route, and
     the subspace Q formed on access must be orthonormal."""
     from paper_1810_06860_b200 import rsvd, workloads
+    from paper_1810_06860_b200.linalg import LazyQ
     from paper_1810_06860_b200.sparse import SparseMatrix
 
     obs = workloads.uniform_sparse(shape[0], shape[1], nnz, seed=5)
     A = SparseMatrix.from_coo(obs.m, obs.n, obs.rows, obs.cols, obs.values)
     prm = rsvd.RsvdParams(k=k, p=p, s=6, seed=2)
-    old = rsvd.LAZY_LAST_PASS
+    old = rsvd.LAZY_LAST_PASS, rsvd.LAZY_MIN_FLOPS
     try:
         rsvd.LAZY_LAST_PASS = False
         ref, sub_ref = rsvd.rsvd_bki(A, prm)
-        rsvd.LAZY_LAST_PASS = True
+        rsvd.LAZY_LAST_PASS, rsvd.LAZY_MIN_FLOPS = True, 0
         res, sub = rsvd.rsvd_bki(A, prm)
+        assert isinstance(sub.Q_any, LazyQ)
     finally:
-        rsvd.LAZY_LAST_PASS = old
+        rsvd.LAZY_LAST_PASS, rsvd.LAZY_MIN_FLOPS = old
     assert np.max(np.abs(res.S - ref.S) / ref.S) <= 1e-12
     assert rel((res.U * res.S) @ res.V.T, (ref.U * ref.S) @ ref.V.T) <= 1e-10
     Q = sub.Q
@@ -283,3 +285,22 @@ def test_bki_unformed_last_pass_matches_formed(shape, nnz, k, p):
     assert Q.shape == (shape[0], W)
     assert np.linalg.norm(Q.T @ Q - np.eye(W)) <= 1e-12 * W
     assert rel(Q, sub_ref.Q) <= 1e-12
+
+
+def test_bki_fp32_mode_singular_values_within_1e4():
+    """north_star's optional fp32 mode: singular values within 1e-4 relative
+    of the fp64 CPU oracle (same seeded Omega)."""
+    from paper_1810_06860_b200 import rsvd, workloads
+    from paper_1810_06860_b200.sparse import SparseMatrix
+
+    obs = workloads.uniform_sparse(6000, 4000, 240000, seed=9)
+    A = SparseMatrix.from_coo(obs.m, obs.n, obs.rows, obs.cols, obs.values)
+    prm = rsvd.RsvdParams(k=30, p=3, s=8, seed=4)
+    res, _ = rsvd.rsvd_bki(A, prm, precision="fp32", omega="host")
+    P = oracle.csr_from_triples(obs.m, obs.n, obs.rows, obs.cols, obs.values)
+    ref, _ = oracle.sketch_bki(P, oracle.SketchParams(k=30, p=3, s=8, seed=4))
+    assert np.max(np.abs(res.S - ref.S) / ref.S) <= 1e-4
+    res64, _ = rsvd.rsvd_bki(A, prm, omega="host")
+    assert np.max(np.abs(res64.S - ref.S) / ref.S) <= 1e-10
+    with pytest.raises(ValueError, match="precision"):
+        rsvd.rsvd_bki(A, prm, precision="fp16")
