@@ -463,9 +463,18 @@ def main():
     kernels = kernel_table(summary, step_ms * PROF_STEPS, PROF_STEPS, hbm_peak, fp64_peak)
     dominant = next((k for k in kernels if "bound" in k), None)
     roofline = None
+    traffic = {}
+    tpath = os.path.join(ROOT, "profiles", "r01i_ncu_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath))
     if dominant:
         roofline = {"bound": dominant["bound"], "achieved": dominant["achieved"], "peak": dominant["peak"],
-                    "unit": dominant["unit"], "frac": dominant["frac"], "traffic": None,
+                    "unit": dominant["unit"], "frac": dominant["frac"],
+                    "traffic": (traffic.get(dominant["call"]) or {}).get("traffic_bytes"),
+                    "traffic_note": ("dram bytes of the call's largest launch from one ncu --set full capture "
+                                     "(profiles/r01i_ncu_traffic.json: " +
+                                     str((traffic.get(dominant["call"]) or {}).get("launch")) + ", algorithmic " +
+                                     str((traffic.get(dominant["call"]) or {}).get("algorithmic_bytes")) + " B)"),
                     "kernel": dominant["call"], "share_of_step": dominant["share"],
                     "peak_source": ("MEASURED_PEAKS.json hbm_gbs (measured)" if dominant["bound"] == "hbm"
                                     else "fp64 cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json "
