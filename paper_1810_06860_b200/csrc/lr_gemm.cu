@@ -278,7 +278,10 @@ static int choose_splits_t(int M, int N, int K, int flags) {
   if (!TA) return 1;
   long long tiles = (flags & LR_GEMM_SYRK_UPPER) ? upper_tiles<T>(M, N)
                                                  : (long long)((M + T::BM - 1) / T::BM) * ((N + T::BN - 1) / T::BN);
-  const long long cap = (long long)sm_count() * occupancy<T, TA>();
+  // waves of split-K work: > 1 lets the block scheduler even out SMs that
+  // drew short (diagonal, pruned) tiles (LR_GEMM_WAVES, experiments)
+  static const int waves = tile_pref("LR_GEMM_WAVES", 1);
+  const long long cap = (long long)sm_count() * occupancy<T, TA>() * waves;
   long long s = tiles >= cap ? 1 : cap / tiles;
   const long long smax = (K + 511) / 512;
   if (s > smax) s = smax;

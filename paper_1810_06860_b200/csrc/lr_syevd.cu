@@ -331,6 +331,17 @@ __global__ void bisect_kernel(const double* __restrict__ d, const double* __rest
   if (lane == 0) w[k] = 0.5 * (lo + hi);
 }
 
+// 1/x to within an ulp: MUFU.RCP64H seed refined by two Newton steps (x is a
+// clamped pivot: never zero, never denormal)
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // inverse iteration, one thread per eigenvalue; scratch laid out [i * n + k]
 // (coalesced across the warp).  Values that the recurrences carry stay in
 // registers; only independent loads touch memory.
@@ -360,7 +371,7 @@ __global__ void inviter_kernel(const double* __restrict__ d, const double* __res
     const double b_next = (i + 2 < n) ? e[i + 1] : 0.0;
     const bool keep = fabs(a) >= fabs(c);  // no interchange
     const double piv = keep ? ((a == 0.0) ? tiny : a) : c;
-    const double rp = 1.0 / piv;
+    const double rp = fast_rcp(piv);  // on the carried chain: MUFU + 2 Newton steps, not a ~125-cycle DDIV
     const double l = (keep ? c : a) * rp;
     Dg[IX(i)] = (fabs(piv) < tiny) ? clamp_rcp(piv) : rp;
     U1[IX(i)] = keep ? b : a_next;

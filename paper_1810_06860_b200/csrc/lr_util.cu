@@ -66,7 +66,18 @@ __global__ void __launch_bounds__(kStatsThreads) block_stats_kernel(const double
     // index division per element)
     const int lane = threadIdx.x & 31;
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
+    long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    for (; r + 3 * nw < rows; r += 4 * nw) {  // four rows' loads in flight
+      const double* r0 = X + r * ld;
+      for (long long c = lane; c < cols; c += 32) {
+        const double a = r0[c], b = r0[nw * ld + c], d = r0[2 * nw * ld + c], e = r0[3 * nw * ld + c];
+        acc(a);
+        acc(b);
+        acc(d);
+        acc(e);
+      }
+    }
+    for (; r < rows; r += nw) {
       const double* row = X + r * ld;
       for (long long c = lane; c < cols; c += 32) acc(row[c]);
     }

@@ -8,7 +8,7 @@ A = ObservationSet(o.m, o.n, o.rows, o.cols, o.values, o.split).train_matrix()
 A.pattern(); A.device_values()
 rng = np.random.default_rng(0)
 print(f"cfg4 train nnz {A.nnz}, rows {A.rows}, cols {A.cols}, csr items {A.pattern().csr.n_items}, csc items {A.pattern().csc.n_items}")
-for w in (11, 16, 22, 33, 45, 66, 89, 132, 264):
+for w in tuple(int(x) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else "11,16,22,33,45,66,89,132,264".split(","))):
     X = device.to_device(rng.standard_normal((A.cols, w)))
     H = device.to_device(rng.standard_normal((A.rows, w)))
     res = []
