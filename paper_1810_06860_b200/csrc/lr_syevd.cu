@@ -31,7 +31,9 @@ namespace cg = cooperative_groups;
 
 namespace lr {
 
-constexpr int TD_EPT = 4;  // trailing elements per thread loaded in one batch after the column barrier
+constexpr int TD_EPT = 4;
+constexpr int kPvSlots = 2 * 512;  // p.v partial slots (2 x G, G <= SM count)
+constexpr int TD_PPL = 8;   // p.v partials per lane: G <= 256  // trailing elements per thread loaded in one batch after the column barrier
 
 struct TdParams {
   const double* A;
@@ -43,6 +45,7 @@ struct TdParams {
   double* Vr;    // n x n: row j holds reflector j at columns j+1..n-1 (v[j+1] = 1)
   double* vbuf;  // 2 x n
   double* pbuf;  // 2 x n
+  double* pvbuf;  // 2 x G per-CTA partials of p.v
   double* rows_global;  // n x (n+1) working rows when they do not fit shared memory, else null
   long long* prof;      // optional per-phase clocks of CTA 0 (LR_SYEVD_TIMING)
 };
@@ -136,6 +139,7 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
     // (a) my slice of p, (b) the owner publishes row j+1
     if (tau != 0.0) {
       const int lane = tid & 31, wp = tid >> 5;
+      double wpv = 0.0;  // this warp's share of p.v (rows in order)
       for (int i = wp; i < nr; i += THREADS / 32) {
         const int r = r0 + i;
         if (r <= j) continue;
@@ -143,7 +147,18 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
         double s = 0.0;
         for (int c = j + 1 + lane; c < n; c += 32) s = fma(row[c], v[c], s);
         s = warp_sum(s);
-        if (lane == 0) pg[r] = tau * s;
+        const double pr = tau * s;
+        if (lane == 0) pg[r] = pr;
+        wpv = fma(pr, v[r], wpv);
+      }
+      // CTA partial of p.v published with p: the post-barrier phase sums the
+      // G partials per warp instead of a block reduction over p
+      if (lane == 0) red[wp] = wpv;
+      __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int q = 0; q < THREADS / 32; ++q) t += red[q];
+        P.pvbuf[par * gridDim.x + blockIdx.x] = t;
       }
     }
     if (j + 1 >= r0 && j + 1 < r1)
@@ -153,27 +168,40 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
     if (prof) tp[2] = clock64();
     // (c) w = p - (tau/2)(p.v) v  (every CTA, full length); row j+1 copy in
     // the same pass so both vectors cost one L2 round trip
-    if (tau != 0.0) {
+    if (tau != 0.0 && n - (j + 1) <= TD_EPT * THREADS && (int)gridDim.x <= 32 * TD_PPL) {
+      // every load of this thread in flight at once (one L2 round trip): its
+      // p and row elements and a lane's share of the G partials of p.v,
+      // which every warp folds in the same fixed order (bit-identical K in
+      // every thread of every CTA, no block reduction)
+      const int lane = tid & 31;
+      double pcs[TD_EPT], xcs[TD_EPT], pps[TD_PPL];
+#pragma unroll
+      for (int u = 0; u < TD_EPT; ++u) {
+        const int c = j + 1 + tid + u * THREADS;
+        pcs[u] = c < n ? __ldcg(pg + c) : 0.0;
+        xcs[u] = c < n ? __ldcg(rg + c) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < TD_PPL; ++u) {
+        const int q = lane + 32 * u;
+        pps[u] = q < (int)gridDim.x ? __ldcg(P.pvbuf + par * gridDim.x + q) : 0.0;
+      }
       double pv = 0.0;
-      if (n - (j + 1) <= TD_EPT * THREADS) {
-        // every load of this thread in flight at once (one L2 round trip)
-        double pcs[TD_EPT], xcs[TD_EPT];
 #pragma unroll
-        for (int u = 0; u < TD_EPT; ++u) {
-          const int c = j + 1 + tid + u * THREADS;
-          pcs[u] = c < n ? __ldcg(pg + c) : 0.0;
-          xcs[u] = c < n ? __ldcg(rg + c) : 0.0;
-        }
+      for (int u = 0; u < TD_PPL; ++u) pv += pps[u];
+      pv = warp_sum(pv);
+      const double K = 0.5 * tau * pv;
 #pragma unroll
-        for (int u = 0; u < TD_EPT; ++u) {
-          const int c = j + 1 + tid + u * THREADS;
-          if (c < n) {
-            x[c] = xcs[u];
-            w[c] = pcs[u];
-            pv = fma(pcs[u], v[c], pv);
-          }
+      for (int u = 0; u < TD_EPT; ++u) {
+        const int c = j + 1 + tid + u * THREADS;
+        if (c < n) {
+          x[c] = xcs[u];
+          w[c] = pcs[u] - K * v[c];
         }
-      } else {
+      }
+    } else if (tau != 0.0) {
+      double pv = 0.0;
+      {
         for (int c = j + 1 + tid; c < n; c += THREADS) {
           const double pc = __ldcg(pg + c);
           x[c] = __ldcg(rg + c);
@@ -669,7 +697,7 @@ long long lr_syevd_workspace_doubles(int n) {
   // d, e, tau, e2, w, bounds | Vr | vbuf, pbuf | Z, U1, U2, Lm, Dg | Pv (ints) | clusters | global rows
   // | WY T factors (one kWY x kWY block per 32 reflectors)
   return 6 * N + 8 + N * N + 4 * N + 5 * N * N + N * N / 2 + N + N + 64 + N * (N + 1) +
-         ((N + kWY - 1) / kWY + 1) * kWY * kWY;
+         ((N + kWY - 1) / kWY + 1) * kWY * kWY + kPvSlots;
 }
 
 int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V, long long ldv, double* work,
@@ -725,6 +753,8 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
   P.Vr = Vr;
   P.vbuf = vbuf;
   P.pbuf = pbuf;
+  // per-CTA p.v partials (2 x G), after the WY T factors
+  P.pvbuf = reinterpret_cast<double*>(clus) + N + 64 + N * (N + 1) + ((N + kWY - 1) / kWY + 1) * kWY * kWY;
   P.rows_global = pl.global_rows ? reinterpret_cast<double*>(clus) + N + 64 : nullptr;
   static const bool timing_env = getenv("LR_SYEVD_TIMING") != nullptr;
   // phase clocks borrow the eigenvalue buffer w (written only after the reduction)
