@@ -232,7 +232,7 @@ def test_lu_pl_errors():
         lu_pl(Y)
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 11, 50, 96, 97, 130, 260, 400])
+@pytest.mark.parametrize("n", [1, 2, 3, 11, 50, 96, 97, 130, 260, 400, 700, 1400])
 def test_sym_eig_matches_numpy(n):
     from paper_1810_06860_b200.linalg import sym_eig
 
