@@ -143,6 +143,67 @@ def to_host(t) -> np.ndarray:
     return out
 
 
+_SIDE = {}
+
+
+def side_stream() -> torch.cuda.Stream:
+    """A second stream for copies that overlap the compute stream."""
+    dev = require_cuda()
+    st = _SIDE.get(dev.index)
+    if st is None:
+        st = _SIDE[dev.index] = torch.cuda.Stream(device=dev)
+    return st
+
+
+class PendingHost:
+    """A device->host copy in flight on the side stream (to_host_async)."""
+
+    def __init__(self, host: torch.Tensor, done: torch.cuda.Event):
+        self.host, self.done = host, done
+
+    def result(self) -> np.ndarray:
+        self.done.synchronize()
+        out = self.host.numpy()
+        TRAFFIC["d2h"] += out.nbytes
+        return out
+
+
+def to_host_async(t) -> PendingHost:
+    """Start copying device tensor t into pinned host memory on the side
+    stream, ordered after the work already queued on the compute stream, so
+    the transfer overlaps whatever the compute stream does next."""
+    t = t.detach()
+    cur = torch.cuda.current_stream()
+    side = side_stream()
+    ready = torch.cuda.Event()
+    ready.record(cur)
+    host = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    with torch.cuda.stream(side):
+        side.wait_event(ready)
+        host.copy_(t, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(side)
+    t.record_stream(side)  # the allocator must not recycle t before the copy ran
+    return PendingHost(host, done)
+
+
+def f64_upload_async(a: np.ndarray):
+    """(device tensor, event): an H2D copy of host float64 data started on the
+    side stream (asynchronous when a is page-locked).  The consumer waits on
+    the event on its own stream before use."""
+    h = np.ascontiguousarray(a, dtype=np.float64)
+    TRAFFIC["h2d"] += h.nbytes
+    dev = require_cuda()
+    side = side_stream()
+    out = torch.empty(h.shape, dtype=torch.float64, device=dev)
+    with torch.cuda.stream(side):
+        out.copy_(torch.from_numpy(h), non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(side)
+    out.record_stream(side)
+    return out, done
+
+
 _NP_TO_TORCH = {np.dtype(np.float64): torch.float64, np.dtype(np.int64): torch.int64,
                 np.dtype(np.int32): torch.int32, np.dtype(np.uint8): torch.uint8}
 

@@ -83,9 +83,11 @@ class DevSvd:
     S: object
     V: object
     S_host: np.ndarray
+    V_pending: object = None  # device.PendingHost of V started before U was lifted
 
     def to_host(self) -> SvdResult:
-        return SvdResult(device.to_host(self.U), self.S_host.copy(), device.to_host(self.V), "descending")
+        V = self.V_pending.result() if self.V_pending is not None else device.to_host(self.V)
+        return SvdResult(device.to_host(self.U), self.S_host.copy(), V, "descending")
 
 
 # ------------------------------------------------------------------ helpers

@@ -190,21 +190,25 @@ def _spmm_t_prec(Y: SparseMatrix, X, precision: str):
     return spmm_t_dev(Y, X)
 
 
-def project_and_solve(Y: SparseMatrix, Q, k: int, fb: _Fallback, precision: str = "fp64"):
+def project_and_solve(Y: SparseMatrix, Q, k: int, fb: _Fallback, precision: str = "fp64",
+                      download: bool = False):
     """B^T = Y^T Q, small SVD, lift: the shared tail of Alg. 5 steps 8-10,
-    recycle_q and rsvd_pi.  Returns the top-k DevSvd (descending)."""
+    recycle_q and rsvd_pi.  Returns the top-k DevSvd (descending).
+    download: V's device->host copy starts (side stream) before U is lifted."""
     W = int(Q.shape[1])
     idx = np.arange(W - 1, W - k - 1, -1)  # top-k of the ascending order, descending
     if isinstance(Q, LazyQ):
         # Q = Q1 Rinv unformed: B^T = (Y^T Q1) Rinv, U = Q1 (Rinv V_small)
         T = _spmm_t_prec(Y, Q.base, precision)
         S_sel, Vsel, Usel = _windowed_small_svd(T, idx, fb, Rinv=Q.Rinv)
+        pend = device.to_host_async(Usel) if download else None
         U = matmul_dev(Q.base, matmul_dev(Q.Rinv, Vsel))
     else:
         Bt = _spmm_t_prec(Y, Q, precision)
         S_sel, Vsel, Usel = _windowed_small_svd(Bt, idx, fb)
+        pend = device.to_host_async(Usel) if download else None
         U = matmul_dev(Q, Vsel)
-    return DevSvd(U, device.f64_buffer(S_sel), Usel, np.asarray(S_sel, dtype=np.float64))
+    return DevSvd(U, device.f64_buffer(S_sel), Usel, np.asarray(S_sel, dtype=np.float64), pend)
 
 
 def _check_precision(precision: str) -> str:
@@ -214,7 +218,7 @@ def _check_precision(precision: str) -> str:
 
 
 def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, omega=None,
-                 precision: str = "fp64"):
+                 precision: str = "fp64", download: bool = False):
     """Device Alg. 5 -> (DevSvd, Q device, fallbacks).
 
     precision="fp32" (north_star's optional fp32 mode, singular values within
@@ -251,7 +255,7 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
     # than the extra small products of the unformed route
     lazy = LAZY_LAST_PASS and m * W * W >= LAZY_MIN_FLOPS
     Q = _orthonormalize(H, fb, lazy_last=lazy)
-    res = project_and_solve(A, Q, params.k, fb, "fp32" if fp32 else "fp64")
+    res = project_and_solve(A, Q, params.k, fb, "fp32" if fp32 else "fp64", download=download)
     return res, Q, fb.count
 
 
@@ -259,7 +263,7 @@ def rsvd_bki(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, 
              precision: str = "fp64"):
     """Rank-k randomized SVD by block Krylov iteration (descending).
     precision="fp32": the optional fp32 mode (sparse products in fp32)."""
-    res, Q, nfb = rsvd_bki_dev(A, params, allow_fallback, omega, precision)
+    res, Q, nfb = rsvd_bki_dev(A, params, allow_fallback, omega, precision, download=True)
     return res.to_host(), Subspace(Q, "bki", params.p, nfb)
 
 

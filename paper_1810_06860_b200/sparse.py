@@ -23,6 +23,7 @@ the data lives, not in what is computed:
 from __future__ import annotations
 
 import numpy as np
+import torch
 
 from . import _native, device
 from .errors import DataError
@@ -168,11 +169,16 @@ class DevicePattern:
     CSR arrays are uploaded; the transpose index is built on the device and
     just the n+1 CSC offsets come back for the host-side work schedule."""
 
-    def __init__(self, A: "SparseMatrix"):
+    def __init__(self, A: "SparseMatrix", prefetch_values=None):
         self.shape = (A.rows, A.cols)
         self.nnz = A.nnz
         hp = A._host_prep()
         self.csr = _Side(hp.csr)
+        # the values' upload (side stream) overlaps the device transpose below
+        self._prefetch = None
+        if prefetch_values is not None and self.nnz:
+            vc, done = device.f64_upload_async(prefetch_values)
+            self._prefetch = (prefetch_values, vc, done)
         t_ptr, t_idx, self.perm, self.inv_perm = _device_transpose(self.csr, A.rows, A.cols, A.nnz)
         if hp.csc_sched is None:  # first upload of this pattern: offsets come back once
             hp.csc_sched = _schedule(device.to_host(t_ptr).astype(np.int64))
@@ -180,7 +186,13 @@ class DevicePattern:
 
     def values(self, host_vals: np.ndarray):
         """(csr, csc) device value copies of host values in CSR order."""
-        vc = device.f64_buffer(host_vals)
+        pre = self._prefetch
+        if pre is not None and pre[0] is host_vals:
+            self._prefetch = None
+            vc = pre[1]
+            torch.cuda.current_stream().wait_event(pre[2])
+        else:
+            vc = device.f64_buffer(host_vals)
         vt = device.vector(self.nnz)
         if self.nnz:
             _native.call("lr_gather_f64", device.ptr(vc), device.ptr(self.perm), device.ptr(vt),
@@ -305,7 +317,10 @@ class SparseMatrix:
 
     def pattern(self) -> DevicePattern:
         if self._pattern is None:
-            self._pattern = DevicePattern(self)
+            # first device use: the values ride along (uploaded while the
+            # transpose index is built) unless they are already resident
+            pre = self._data if (self._dvals is None and not self._host_stale) else None
+            self._pattern = DevicePattern(self, prefetch_values=pre)
         return self._pattern
 
     def pin_memory(self) -> "SparseMatrix":
