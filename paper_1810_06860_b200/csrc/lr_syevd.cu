@@ -575,6 +575,11 @@ __global__ void __launch_bounds__(256) build_T_kernel(const double* __restrict__
 // thread owns one row c and all kTC columns.  ~2.6x fewer shared-memory
 // wavefronts per FMA than one output per thread.
 constexpr int kWyRedWarps = 4;
+__device__ __forceinline__ void wy_cp_async8(double* smem, const double* gmem) {
+  const unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gmem));
+}
+
 template <int kTC>
 __global__ void __launch_bounds__(256) wy_apply_kernel(double* __restrict__ Z, int n, const double* __restrict__ Vr,
                                                      const double* __restrict__ T, int nrefl, double* __restrict__ V,
@@ -596,11 +601,16 @@ __global__ void __launch_bounds__(256) wy_apply_kernel(double* __restrict__ Z, i
     const int J = b * kWY;
     const int bsb = min(kWY, nrefl - J);
     if (vb) {
-      const int L = n - J - 1;
-      for (int e = tid; e < bsb * L; e += 256) {
-        const int q = e / L, c = J + 1 + (e - (e / L) * L);
-        vb[q * LDV + c] = Vr[(long long)(J + q) * n + c];
+      // stage the block's reflector rows with asynchronous 8-byte copies: every
+      // copy of the thread in flight at once, one wait (the plain load/store
+      // loop paid an L2 round trip per few elements)
+      for (int q = 0; q < bsb; ++q) {
+        const double* src = Vr + (long long)(J + q) * n;
+        double* dst = vb + q * LDV;
+        for (int c = J + 1 + tid; c < n; c += 256) wy_cp_async8(dst + c, src + c);
       }
+      asm volatile("cp.async.commit_group;\n" ::);
+      asm volatile("cp.async.wait_group 0;\n" ::);
     }
     __syncthreads();
     // (1) partials of Y[k][:] over a quarter of the reflector length
