@@ -28,6 +28,13 @@ for rep in range(2):
     print(f"rsvd_bki k=300 p=3 (W=1220): {t6 - t5:.3f} s  S[0]={res.S_host[0]:.6e} S[299]={res.S_host[299]:.6e}", flush=True)
 S = res.S_host
 U = res.U
+for rep in range(2):
+    torch.cuda.synchronize(); t5 = time.perf_counter()
+    r32, _, _ = rsvd_bki_dev(A, p, precision="fp32")
+    torch.cuda.synchronize(); t6 = time.perf_counter()
+    print(f"rsvd_bki fp32 mode k=300 p=3 (W=1220): {t6 - t5:.3f} s  max rel S diff vs fp64 "
+          f"{np.max(np.abs(r32.S_host - S) / S):.2e}", flush=True)
+del r32
 G = (U.T @ U).cpu().numpy()
 print("descending:", bool(np.all(np.diff(S) <= 0)), " ||U^T U - I|| =", np.abs(G - np.eye(G.shape[0])).max(),
       " peak mem GB:", torch.cuda.max_memory_allocated() / 1e9, flush=True)
