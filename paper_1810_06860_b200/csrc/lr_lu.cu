@@ -85,7 +85,7 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 // owner's.  (A barrier-free exchange of self-validating tagged words was
 // measured slower: 1.02 vs 0.89 ms at 100000 x 110 -- every CTA polling
 // every candidate costs more than one counter.)
-__global__ void __launch_bounds__(LU_THREADS, 2) lu_kernel(LuParams p) {
+__global__ void __launch_bounds__(LU_THREADS, (512 / LU_THREADS) > 0 ? (512 / LU_THREADS) : 1) lu_kernel(LuParams p) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double lu_smem[];
   const int nb = p.nb, LD = nb + 1;
