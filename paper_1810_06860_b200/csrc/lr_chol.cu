@@ -393,7 +393,9 @@ __global__ void __launch_bounds__(CB_THREADS) chol_coop_kernel(int n, double* A,
           for (int e = threadIdx.x; e < CB * CB; e += CB_THREADS) dst[e] = pk[e >> 5][e & 31];
         }
         if (t == 0) {  // CTA 0: next diagonal block
+          if (3 * J + 64 < 126) CB_STAMP(3 * J + 64);
           const int bad = cb_factor(tt, pl, rowbuf, K, n);
+          if (3 * J + 65 < 126) CB_STAMP(3 * J + 65);
           if (bad) {
             if (threadIdx.x == 0) atomicExch(info, bad);
           } else {
@@ -497,6 +499,9 @@ static int potrf_coop(int n, double* A, long long lda, double shift, double* Rin
     LR_CHECK_CUDA(cudaStreamSynchronize(s));
     fprintf(stderr, "potrf_coop n=%d G=%d:", n, G);
     for (int k = 1; k < 4 + 2 * nb; ++k)
+      if (trace[k]) fprintf(stderr, " %d:%.1f", k, (trace[k] - trace[0]) * 1e-3);
+    fprintf(stderr, "\n  CTA0 diag tile updated / factored:");
+    for (int k = 64; k < 126; ++k)
       if (trace[k]) fprintf(stderr, " %d:%.1f", k, (trace[k] - trace[0]) * 1e-3);
     fprintf(stderr, " end:%.1f us\n", (trace[120] - trace[0]) * 1e-3);
     for (int k = 0; k < 128; ++k) trace[k] = 0;

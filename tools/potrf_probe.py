@@ -4,7 +4,7 @@ sys.path.insert(0, '.')
 from paper_1810_06860_b200 import _native, device
 
 lib = _native.load()
-for n in (110, 330, 660, 1220, 2048):
+for n in tuple(int(a) for a in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["110", "330", "660", "1220", "2048"])):
     X = np.random.default_rng(n).standard_normal((4 * n, n))
     G0 = device.to_device(X.T @ X)
     G = device.empty(n, n)
