@@ -101,7 +101,66 @@ __global__ void __launch_bounds__(T::THREADS) gemm_kernel(int M, int N, int K, d
     warp_klim = (flags & LR_GEMM_B_UPPER) ? min(k_end, cbase + T::WN) : k_end;
   }
 
+  // Lean 16-byte path: every (row, pair) a thread copies is fixed for the
+  // whole k loop, so offsets and the M/N edge predicates are computed once
+  // and a stage is NA + NB fully unrolled cp.async with one k-bound test
+  // each (the generic loop below re-derived indices per element per stage).
+  constexpr int A_PAIRS = TRANS_A ? T::BM / 2 : T::BK / 2;  // 16-byte chunks per A smem row
+  constexpr int A_ROWS = TRANS_A ? T::BK : T::BM;
+  constexpr int NA = A_ROWS * A_PAIRS / T::THREADS;          // chunks per thread
+  constexpr int A_STRIDE = T::THREADS / A_PAIRS;              // rows between a thread's chunks
+  constexpr int B_PAIRS = T::BN / 2;
+  constexpr int NB = T::BK * B_PAIRS / T::THREADS;
+  constexpr int B_STRIDE = T::THREADS / B_PAIRS;
+  static_assert(NA * T::THREADS == A_ROWS * A_PAIRS && NB * T::THREADS == T::BK * B_PAIRS, "tile/threads");
+  const int a_row0 = tid / A_PAIRS, a_col = 2 * (tid % A_PAIRS);
+  const int b_row0 = tid / B_PAIRS, b_col = 2 * (tid % B_PAIRS);
+  int a_bytes_mn = 16;  // TRANS_A: M edge of this thread's column pair (fixed)
+  if (TRANS_A) a_bytes_mn = (m0 + a_col + 1 < M) ? 16 : (m0 + a_col < M ? 8 : 0);
+  const int b_bytes_n = (n0 + b_col + 1 < N) ? 16 : (n0 + b_col < N ? 8 : 0);
+  unsigned a_row_ok = 0;  // !TRANS_A: M edge per chunk row (fixed)
+  if (!TRANS_A) {
+#pragma unroll
+    for (int i = 0; i < NA; ++i)
+      if (m0 + a_row0 + i * A_STRIDE < M) a_row_ok |= 1u << i;
+  }
+  auto load_stage_fast = [&](int st, int kt) {
+    const int k0 = k_begin + kt * T::BK;
+    double* as = As + st * T::A_STAGE;
+    double* bs = Bs + st * T::B_STAGE;
+    if (TRANS_A) {
+      const double* src = A + (long long)(k0 + a_row0) * lda + m0 + a_col;
+#pragma unroll
+      for (int i = 0; i < NA; ++i) {
+        const int kk = a_row0 + i * A_STRIDE;
+        const int nb = (k0 + kk < k_end) ? a_bytes_mn : 0;
+        cp_async16(as + kk * T::LDA_T + a_col, nb ? src + (long long)i * A_STRIDE * lda : A, nb);
+      }
+    } else {
+      const int gk = k0 + a_col;
+      const int kb = (gk + 1 < k_end) ? 16 : (gk < k_end ? 8 : 0);
+      const double* src = A + (long long)(m0 + a_row0) * lda + gk;
+#pragma unroll
+      for (int i = 0; i < NA; ++i) {
+        const int mm = a_row0 + i * A_STRIDE;
+        const int nb = (a_row_ok >> i) & 1 ? kb : 0;
+        cp_async16(as + mm * T::LDA_N + a_col, nb ? src + (long long)i * A_STRIDE * lda : A, nb);
+      }
+    }
+    const double* bsrc = B + (long long)(k0 + b_row0) * ldb + n0 + b_col;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const int kk = b_row0 + i * B_STRIDE;
+      const int nb = (k0 + kk < k_end) ? b_bytes_n : 0;
+      cp_async16(bs + kk * T::LDB + b_col, nb ? bsrc + (long long)i * B_STRIDE * ldb : B, nb);
+    }
+  };
+
   auto load_stage = [&](int st, int kt) {
+    if (vec16) {
+      load_stage_fast(st, kt);
+      return;
+    }
     const int k0 = k_begin + kt * T::BK;
     double* as = As + st * T::A_STAGE;
     double* bs = Bs + st * T::B_STAGE;
