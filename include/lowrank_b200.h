@@ -145,6 +145,10 @@ int lr_gemm_f64(int transA, int M, int N, int K, double alpha, const double* A, 
 long long lr_potrf_workspace_doubles(int n);
 int lr_potrf_inv_f64(int n, double* A, long long lda, double shift, double* Rinv, long long ldr,
                      double* work, int* info_host, void* stream);
+/* Asynchronous variant: info (0, or the 1-based failing column) to device
+ * memory *info_dev, no host synchronisation. */
+int lr_potrf_inv_async_f64(int n, double* A, long long lda, double shift, double* Rinv, long long ldr,
+                           double* work, int* info_dev, void* stream);
 
 /* Partial-pivoting LU of a tall m x n block (m >= n), in place, returning
  * P^T L like scipy.linalg.lu(X, permute_l=True) as used by `lu_pl`
@@ -156,6 +160,11 @@ int lr_potrf_inv_f64(int n, double* A, long long lda, double shift, double* Rinv
 long long lr_lu_workspace_doubles(int m, int n);
 int lr_lu_pl_f64(int m, int n, double* X, long long ldx, double* work, double* status_host,
                  void* stream);
+/* Asynchronous variant (no host synchronisation): {code, pivot, tol} go to
+ * device memory status_dev[0..2] with the codes above (-1 ok, -2 zero
+ * matrix, -3 non-finite, j >= 0 zero pivot at column j); the caller checks
+ * several calls' statuses with one read (rsvd.py's speculative BKI). */
+int lr_lu_pl_async_f64(int m, int n, double* X, long long ldx, double* work, double* status_dev, void* stream);
 
 /* Symmetric eigendecomposition by parallel (block-)Jacobi: eigenvalues
  * ascending in d, orthonormal eigenvectors in V (n x n, ldv).  A (n x n) is

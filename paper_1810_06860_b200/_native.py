@@ -49,8 +49,10 @@ SIGNATURES = {
     "lr_gemm_f64": (_I, [_I, _I, _I, _I, _D, _P, _LL, _P, _LL, _D, _P, _LL, _I, _P, _LL, _P]),
     "lr_potrf_workspace_doubles": (_LL, [_I]),
     "lr_potrf_inv_f64": (_I, [_I, _P, _LL, _D, _P, _LL, _P, _P, _P]),
+    "lr_potrf_inv_async_f64": (_I, [_I, _P, _LL, _D, _P, _LL, _P, _P, _P]),
     "lr_lu_workspace_doubles": (_LL, [_I, _I]),
     "lr_lu_pl_f64": (_I, [_I, _I, _P, _LL, _P, _P, _P]),
+    "lr_lu_pl_async_f64": (_I, [_I, _I, _P, _LL, _P, _P, _P]),
     "lr_syevj_workspace_doubles": (_LL, [_I]),
     "lr_syevj_f64": (_I, [_I, _P, _LL, _P, _P, _LL, _I, _P, _P, _P]),
     "lr_syevd_workspace_doubles": (_LL, [_I]),

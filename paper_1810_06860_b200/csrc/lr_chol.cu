@@ -467,7 +467,7 @@ long long lr_potrf_workspace_doubles(int n) {
 }
 
 static int potrf_coop(int n, double* A, long long lda, double shift, double* Rinv, long long ldr,
-                      double* work, int* info_host, cudaStream_t s) {
+                      double* work, int* info_host, int* info_dev, cudaStream_t s) {
   const int nb = (n + CB - 1) / CB;
   const size_t smem = (size_t)kCoopSmemDoubles * sizeof(double);
   static bool attr = false;
@@ -491,6 +491,7 @@ static int potrf_coop(int n, double* A, long long lda, double shift, double* Rin
   LR_CHECK_CUDA(cudaLaunchCooperativeKernel((const void*)chol_coop_kernel, dim3((unsigned)G), dim3(CB_THREADS),
                                             args, smem, s));
   LR_CHECK_LAUNCH();
+  if (info_dev) LR_CHECK_CUDA(cudaMemcpyAsync(info_dev, info, sizeof(int), cudaMemcpyDeviceToDevice, s));
   if (info_host) {
     LR_CHECK_CUDA(cudaMemcpyAsync(info_host, info, sizeof(int), cudaMemcpyDeviceToHost, s));
     LR_CHECK_CUDA(cudaStreamSynchronize(s));
@@ -509,12 +510,27 @@ static int potrf_coop(int n, double* A, long long lda, double shift, double* Rin
   return LR_OK;
 }
 
+static int potrf_impl(int n, double* A, long long lda, double shift, double* Rinv, long long ldr, double* work,
+                      int* info_host, int* info_dev, void* stream);
+
 int lr_potrf_inv_f64(int n, double* A, long long lda, double shift, double* Rinv, long long ldr,
                      double* work, int* info_host, void* stream) {
+  return potrf_impl(n, A, lda, shift, Rinv, ldr, work, info_host, nullptr, stream);
+}
+
+int lr_potrf_inv_async_f64(int n, double* A, long long lda, double shift, double* Rinv, long long ldr,
+                           double* work, int* info_dev, void* stream) {
+  LR_REQUIRE(info_dev != nullptr, "potrf_async: info_dev is required");
+  return potrf_impl(n, A, lda, shift, Rinv, ldr, work, nullptr, info_dev, stream);
+}
+
+static int potrf_impl(int n, double* A, long long lda, double shift, double* Rinv, long long ldr, double* work,
+                      int* info_host, int* info_dev, void* stream) {
   LR_REQUIRE(n >= 1 && lda >= n && ldr >= n, "potrf: bad shape");
   cudaStream_t s = as_stream(stream);
   static const bool blocked_only = getenv("LR_POTRF_BLOCKED") != nullptr;
-  if (n <= kCoopMaxN && !blocked_only) return potrf_coop(n, A, lda, shift, Rinv, ldr, work, info_host, s);
+  if (n <= kCoopMaxN && !blocked_only)
+    return potrf_coop(n, A, lda, shift, Rinv, ldr, work, info_host, info_dev, s);
   const long long nblk = (n + CH_NB - 1) / CH_NB;
   double* Dinv = work;
   double* T = work + nblk * CH_NB * CH_NB;  // CH_NB x n
@@ -576,6 +592,7 @@ int lr_potrf_inv_f64(int n, double* A, long long lda, double shift, double* Rinv
       }
     }
   }
+  if (info_dev) LR_CHECK_CUDA(cudaMemcpyAsync(info_dev, info, sizeof(int), cudaMemcpyDeviceToDevice, s));
   if (info_host) {
     LR_CHECK_CUDA(cudaMemcpyAsync(info_host, info, sizeof(int), cudaMemcpyDeviceToHost, s));
     LR_CHECK_CUDA(cudaStreamSynchronize(s));

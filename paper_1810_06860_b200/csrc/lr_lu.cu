@@ -587,8 +587,36 @@ long long lr_lu_workspace_doubles(int m, int n) {
   return kCandWords * G + kRowWords * G + n + 8 + lr_stats_partials() + 10;
 }
 
+// status_dev (async variant): {code, pivot, tol} with the host wrapper's codes
+// (-1 ok, -2 zero matrix, -3 non-finite, j >= 0 first bad column)
+__global__ void lu_status_kernel(const double* status, const double* stats, double* out) {
+  if (threadIdx.x != 0) return;
+  if (stats != nullptr && stats[2] != 0.0) {
+    out[0] = -3.0;
+  } else if (stats != nullptr && stats[1] == 0.0) {
+    out[0] = -2.0;
+  } else {
+    out[0] = status[0];
+    out[1] = status[1];
+    out[2] = status[2];
+  }
+}
+
+static int lu_impl(int m, int n, double* X, long long ldx, double* work, double* status_host, double* status_dev,
+                   void* stream);
+
 int lr_lu_pl_f64(int m, int n, double* X, long long ldx, double* work, double* status_host,
                  void* stream) {
+  return lu_impl(m, n, X, ldx, work, status_host, nullptr, stream);
+}
+
+int lr_lu_pl_async_f64(int m, int n, double* X, long long ldx, double* work, double* status_dev, void* stream) {
+  LR_REQUIRE(status_dev != nullptr, "lu_pl_async: status_dev is required");
+  return lu_impl(m, n, X, ldx, work, nullptr, status_dev, stream);
+}
+
+static int lu_impl(int m, int n, double* X, long long ldx, double* work, double* status_host, double* status_dev,
+                   void* stream) {
   LR_REQUIRE(m >= n && n >= 1, "lu_pl requires m >= n, got %dx%d", m, n);
   LR_REQUIRE(ldx >= n, "lu_pl: ldx < n");
   cudaStream_t s = as_stream(stream);
@@ -603,6 +631,11 @@ int lr_lu_pl_f64(int m, int n, double* X, long long ldx, double* work, double* s
     double* status = work;
     lu_small_kernel<<<1, LUS_THREADS, lu_small_smem(m, n), s>>>(X, ldx, m, n, status);
     LR_CHECK_LAUNCH();
+    if (status_dev) {
+      lu_status_kernel<<<1, 32, 0, s>>>(status, nullptr, status_dev);
+      LR_CHECK_LAUNCH();
+      return LR_OK;
+    }
     double host[4];
     LR_CHECK_CUDA(cudaMemcpyAsync(host, status, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
     LR_CHECK_CUDA(cudaStreamSynchronize(s));
@@ -664,6 +697,11 @@ int lr_lu_pl_f64(int m, int n, double* X, long long ldx, double* work, double* s
             "lu %dx%d G=%lld nb=%d ch=%d cycles/col: local %.0f barrier %.0f winner %.0f (cand %.0f row %.0f) update %.0f; panel ends total %.0f (after barrier %.0f)\n",
             m, n, G, pl.nb, pl.ch, (double)hp[0] / n, (double)hp[1] / n, (double)hp[2] / n, (double)hp[5] / n,
             (double)hp[6] / n, (double)hp[3] / n, (double)hp[4], (double)hp[7]);
+  }
+  if (status_dev) {
+    lu_status_kernel<<<1, 32, 0, s>>>(status, stats, status_dev);
+    LR_CHECK_LAUNCH();
+    return LR_OK;
   }
   double host[8];
   LR_CHECK_CUDA(cudaMemcpyAsync(host, status, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -21,15 +21,36 @@ I32 = torch.int32
 TRAFFIC = {"h2d": 0, "d2h": 0}
 
 
+_READY = False
+_DEVICES = {}
+
+
 def require_cuda() -> torch.device:
-    if not torch.cuda.is_available():
-        raise RuntimeError(
-            "paper_1810_06860_b200 needs a CUDA device (B200, sm_100a); it has no CPU fallback")
-    _native.load()
-    return torch.device("cuda", torch.cuda.current_device())
+    """The current CUDA device; raises without one (no CPU fallback).  The
+    availability check and the library load run once per process."""
+    global _READY
+    if not _READY:
+        if not torch.cuda.is_available():
+            raise RuntimeError(
+                "paper_1810_06860_b200 needs a CUDA device (B200, sm_100a); it has no CPU fallback")
+        _native.load()
+        _READY = True
+    idx = torch._C._cuda_getDevice()
+    dev = _DEVICES.get(idx)
+    if dev is None:
+        dev = _DEVICES[idx] = torch.device("cuda", idx)
+    return dev
+
+
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 
 
 def stream() -> int:
+    """cudaStream_t of torch's current stream on the current device (the raw
+    C accessor: the Python-level current_stream() costs microseconds per
+    native call)."""
+    if _RAW_STREAM is not None:
+        return _RAW_STREAM(torch._C._cuda_getDevice())
     return torch.cuda.current_stream().cuda_stream
 
 

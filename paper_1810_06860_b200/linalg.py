@@ -29,6 +29,7 @@ import ctypes
 from dataclasses import dataclass
 
 import numpy as np
+import torch
 
 from . import _native, device
 from .errors import NumericalError, RankDeficiencyError, SizeCapError
@@ -216,6 +217,51 @@ def _cholqr_pass(X, shift=0.0, G=None, lazy=False):
     diag = _diag_host(G, n)
     Q = LazyQ(X, Rinv) if lazy else matmul_dev(X, Rinv, b_upper=True)
     return 0, Q, diag
+
+
+def orth_speculative_dev(X, lazy_last=False):
+    """The CholeskyQR2 route of orth_dev without host synchronisation.
+
+    Every quantity orth_core decides on -- diag(G0) (its trace is ||X||_F^2),
+    the two Cholesky infos, diag(R1), diag(R2) -- is left in device buffers;
+    returns (Q, probe) where probe is a list of device tensors to read with the
+    caller's single synchronisation, and `orth_speculation_holds` replays
+    orth_core's decisions on them: True iff orth_core would have taken exactly
+    this route (no breakdown, no third pass) and accepted the result, so the
+    returned Q is bit-identical to orth_dev's."""
+    m, n = X.shape
+    diag = device.vector(3 * n)
+    infos = torch.zeros(2, dtype=torch.int32, device=X.device)
+    work = device.arena().get("potrf_work", int(_native.load().lr_potrf_workspace_doubles(n)))
+    G0 = gram_dev(X)
+    _native.call("lr_diag_f64", device.ptr(G0), device.ld(G0), n, device.ptr(diag[0:n]), _st())
+    R1inv = device.empty(n, n)
+    _native.call("lr_potrf_inv_async_f64", n, device.ptr(G0), device.ld(G0), 0.0, device.ptr(R1inv),
+                 device.ld(R1inv), device.ptr(work), device.ptr(infos[0:1]), _st())
+    _native.call("lr_diag_f64", device.ptr(G0), device.ld(G0), n, device.ptr(diag[n:2 * n]), _st())
+    Q1 = matmul_dev(X, R1inv, b_upper=True)
+    G1 = gram_dev(Q1)
+    R2inv = device.empty(n, n)
+    _native.call("lr_potrf_inv_async_f64", n, device.ptr(G1), device.ld(G1), 0.0, device.ptr(R2inv),
+                 device.ld(R2inv), device.ptr(work), device.ptr(infos[1:2]), _st())
+    _native.call("lr_diag_f64", device.ptr(G1), device.ld(G1), n, device.ptr(diag[2 * n:3 * n]), _st())
+    Q = LazyQ(Q1, R2inv) if lazy_last else matmul_dev(Q1, R2inv, b_upper=True)
+    return Q, [diag, infos]
+
+
+def orth_speculation_holds(diag_h, infos_h) -> bool:
+    """orth_core's decisions on the values orth_speculative_dev recorded."""
+    n = diag_h.shape[0] // 3
+    if int(infos_h[0]) != 0 or int(infos_h[1]) != 0:
+        return False
+    tr = float(np.sum(diag_h[0:n]))
+    if not (np.isfinite(tr) and tr < 1e300) or tr <= 0.0:
+        return False
+    scale = float(np.sqrt(tr))
+    d1, d2 = diag_h[n:2 * n], diag_h[2 * n:3 * n]
+    if not np.all(np.isfinite(d2)) or np.max(np.abs(d2 - 1.0)) > 1e-6:
+        return False
+    return not np.any(np.abs(d2 * d1) < ORTH_RANK_TOL * scale)
 
 
 def orth_dev(X, lazy_last=False):

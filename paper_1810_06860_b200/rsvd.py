@@ -30,7 +30,7 @@ import numpy as np
 from . import _native, device
 from .errors import RankDeficiencyError
 from .linalg import (DevSvd, LazyQ, SvdResult, eig_svd_congruent_dev, eig_svd_dev, lu_pl_dev, matmul_dev,
-                     oracle_svd_dev, orth_dev)
+                     oracle_svd_dev, orth_dev, orth_speculation_holds, orth_speculative_dev)
 from .rng import RngState, gaussian_matrix, gaussian_matrix_device
 from .sparse import SparseMatrix, frobenius, spmm_dev, spmm_dev32, spmm_t_dev, spmm_t_dev32
 
@@ -39,6 +39,9 @@ OMEGA_SOURCE = "device"
 # Q V run through Q1 and R2^{-1}; Subspace.Q forms Q only when asked.
 LAZY_LAST_PASS = True
 LAZY_MIN_FLOPS = 1 << 30  # m * W^2 below this: form Q (the GEMM is a few microseconds)
+# rsvd_bki checks LU statuses and orth's decisions with one read after the
+# basis is built, redoing the call on the careful path when one is unusual
+SPECULATIVE = True
 
 
 @dataclass
@@ -142,6 +145,14 @@ def _lu_block(block, fb: _Fallback):
         _copy(U, block)
 
 
+def _lu_block_async(block, status):
+    """LU-normalise a device block in place, its status left on the device."""
+    m, n = block.shape
+    work = device.arena().get("lu_work", int(_native.load().lr_lu_workspace_doubles(m, n)))
+    _native.call("lr_lu_pl_async_f64", m, n, device.ptr(block), device.ld(block), device.ptr(work),
+                 device.ptr(status), device.stream())
+
+
 def _orthonormalize(X, fb: _Fallback, lazy_last=False):
     try:
         return orth_dev(X, lazy_last=lazy_last)
@@ -218,7 +229,7 @@ def _check_precision(precision: str) -> str:
 
 
 def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, omega=None,
-                 precision: str = "fp64", download: bool = False):
+                 precision: str = "fp64", download: bool = False, _speculate: bool = True):
     """Device Alg. 5 -> (DevSvd, Q device, fallbacks).
 
     precision="fp32" (north_star's optional fp32 mode, singular values within
@@ -231,15 +242,30 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
     w = params.k + params.s
     W = w * (params.p + 1)
     m, n = A.shape
+    # Speculation: the LU statuses and orth's decisions stay on the device and
+    # are read with ONE synchronisation after the basis is built; if any of
+    # them is not the common case (a zero pivot, a Cholesky breakdown, a third
+    # CholeskyQR pass, a rank collapse) the call is redone on the careful path
+    # below, which makes every decision as it goes -- so results, errors and
+    # fallbacks are exactly the careful path's.
+    spec = SPECULATIVE and _speculate
+    lu_status = device.vector(4 * (params.p + 1)) if spec else None
     Om = _omega(params.seed, n, w, omega or OMEGA_SOURCE)
     H = device.empty(m, W)
+
+    def normalise(i):
+        if spec:
+            _lu_block_async(H[:, i * w:(i + 1) * w], lu_status[4 * i:4 * i + 3])
+        else:
+            _lu_block(H[:, i * w:(i + 1) * w], fb)
+
     if fp32:
         H32, T32 = device.empty32(m, w), device.empty32(n, w)
         spmm_dev32(A, device.to_f32(Om), out=H32)
         device.to_f64(H32, out=H[:, 0:w])
     else:
         spmm_dev(A, Om, out=H[:, 0:w])
-    _lu_block(H[:, 0:w], fb)
+    normalise(0)
     T = None if fp32 else device.empty(n, w)
     for i in range(1, params.p + 1):
         if fp32:
@@ -250,11 +276,22 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
         else:
             spmm_t_dev(A, H[:, (i - 1) * w:i * w], out=T)
             spmm_dev(A, T, out=H[:, i * w:(i + 1) * w])
-        _lu_block(H[:, i * w:(i + 1) * w], fb)
+        normalise(i)
     # small blocks (launch-bound, e.g. cfg1's 1000 x 64): forming Q is cheaper
     # than the extra small products of the unformed route
     lazy = LAZY_LAST_PASS and m * W * W >= LAZY_MIN_FLOPS
-    Q = _orthonormalize(H, fb, lazy_last=lazy)
+    if spec:
+        Q, probe = orth_speculative_dev(H, lazy_last=lazy)
+        st = device.to_host(lu_status).reshape(-1, 4)[:, :3]
+        diag_h, infos_h = device.to_host(probe[0]), device.to_host(probe[1])
+        if not np.all(st[:, 0] == -1.0):  # an LU decision differed: redo the whole call
+            return rsvd_bki_dev(A, params, allow_fallback, omega, precision, download, _speculate=False)
+        if not orth_speculation_holds(diag_h, infos_h):
+            # the Krylov blocks are exactly the careful path's (H is untouched
+            # by the speculative orth): only the orthonormalisation is redone
+            Q = _orthonormalize(H, fb, lazy_last=lazy)
+    else:
+        Q = _orthonormalize(H, fb, lazy_last=lazy)
     res = project_and_solve(A, Q, params.k, fb, "fp32" if fp32 else "fp64", download=download)
     return res, Q, fb.count
 

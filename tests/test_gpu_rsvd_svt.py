@@ -304,3 +304,43 @@ def test_bki_fp32_mode_singular_values_within_1e4():
     assert np.max(np.abs(res64.S - ref.S) / ref.S) <= 1e-10
     with pytest.raises(ValueError, match="precision"):
         rsvd.rsvd_bki(A, prm, precision="fp16")
+
+
+def test_bki_speculative_matches_careful_path():
+    """rsvd_bki's speculative route (LU statuses and CholeskyQR decisions read
+    with one synchronisation) returns exactly what the careful route returns,
+    also when a decision differs (ill-conditioned Krylov blocks need a third
+    CholeskyQR pass; a rank-deficient matrix trips an LU pivot)."""
+    from paper_1810_06860_b200 import rsvd, workloads
+    from paper_1810_06860_b200.sparse import SparseMatrix
+
+    obs = workloads.uniform_sparse(5000, 3000, 150000, seed=21)
+    cases = [SparseMatrix.from_coo(obs.m, obs.n, obs.rows, obs.cols, obs.values)]
+    # nearly rank-3 matrix: later Krylov blocks are almost collinear
+    rng = np.random.default_rng(3)
+    L, R = rng.standard_normal((400, 3)), rng.standard_normal((300, 3))
+    D = L @ R.T + 1e-9 * rng.standard_normal((400, 300))
+    ii, jj = np.nonzero(np.ones_like(D))
+    cases.append(SparseMatrix.from_coo(400, 300, ii, jj, D[ii, jj]))
+    for A in cases:
+        for fallback in (False, True):
+            prm = rsvd.RsvdParams(k=10, p=3, s=5, seed=7)
+            old = rsvd.SPECULATIVE
+            outs = []
+            for spec in (True, False):
+                rsvd.SPECULATIVE = spec
+                try:
+                    res, sub = rsvd.rsvd_bki(A, prm, allow_fallback=fallback)
+                    outs.append(("ok", res.S, res.U, res.V, sub.Q, sub.fallbacks))
+                except Exception as exc:  # the same error type and text on both routes
+                    outs.append(("err", type(exc).__name__, str(exc)))
+                finally:
+                    rsvd.SPECULATIVE = old
+            a, b = outs
+            assert a[0] == b[0]
+            if a[0] == "err":
+                assert a[1:] == b[1:]
+            else:
+                for x, y in zip(a[1:5], b[1:5]):
+                    np.testing.assert_array_equal(x, y)
+                assert a[5] == b[5]
