@@ -239,16 +239,29 @@ def pinned_copy(a: np.ndarray) -> np.ndarray:
     return out
 
 
-def int_buffer(a: np.ndarray) -> torch.Tensor:
-    h = np.ascontiguousarray(a, dtype=np.int32)
+SMALL_ASYNC_BYTES = 1 << 20  # small uploads go through pinned staging, without a stream sync
+
+
+def _upload(h: np.ndarray, dtype) -> torch.Tensor:
+    """Host array -> device.  Small arrays (the S vectors, column lists of a
+    call) are staged in pinned memory and copied without blocking, so the
+    upload does not synchronise the stream (a pageable .to(cuda) does); the
+    caching host allocator keeps the staging block until the copy ran."""
     TRAFFIC["h2d"] += h.nbytes
-    return torch.from_numpy(h).to(require_cuda())
+    dev = require_cuda()
+    if h.nbytes <= SMALL_ASYNC_BYTES:
+        st = torch.empty(h.shape, dtype=dtype, pin_memory=True)
+        st.numpy()[...] = h
+        return st.to(dev, non_blocking=True)
+    return torch.from_numpy(h).to(dev)
+
+
+def int_buffer(a: np.ndarray) -> torch.Tensor:
+    return _upload(np.ascontiguousarray(a, dtype=np.int32), torch.int32)
 
 
 def f64_buffer(a: np.ndarray) -> torch.Tensor:
-    h = np.ascontiguousarray(a, dtype=np.float64)
-    TRAFFIC["h2d"] += h.nbytes
-    return torch.from_numpy(h).to(require_cuda())
+    return _upload(np.ascontiguousarray(a, dtype=np.float64), torch.float64)
 
 
 class Arena:

@@ -450,10 +450,18 @@ def eig_svd_dev(A, cols=None, check=True):
     if rows < n:
         raise ValueError(f"eig_svd requires m >= n, got {rows}x{n}")
     G = gram_dev(A)
-    if check and not np.isfinite(np.sum(_diag_host(G, n))):
-        _check_dev(A, "eig_svd input")  # raises ValueError on non-finite input
-    V, d = sym_eig_dev(G, symmetrize=False)
-    S = gram_spectrum(device.to_host(d))
+    try:
+        V, d = sym_eig_dev(G, symmetrize=False)
+    except NumericalError:
+        if check:
+            _check_dev(A, "eig_svd input")  # a non-finite input is the reference's ValueError
+        raise
+    dh = device.to_host(d)
+    # a non-finite input shows as non-finite Gram eigenvalues: only then is
+    # the input scanned, for the reference's ValueError (no extra sync before)
+    if check and not np.all(np.isfinite(dh)):
+        _check_dev(A, "eig_svd input")
+    S = gram_spectrum(dh)
     _native.call("lr_fix_signs_f64", device.ptr(V), device.ld(V), n, n, None, 0, 0, _st())
     if cols is None:
         cols = np.arange(n)
@@ -474,12 +482,17 @@ def eig_svd_congruent_dev(T, Rinv, cols):
     eig_svd_dev."""
     rows, n = T.shape
     Gt = gram_dev(T)
-    if not np.isfinite(np.sum(_diag_host(Gt, n))):
-        _check_dev(T, "eig_svd input")
     H = matmul_dev(Gt, Rinv, b_upper=True)   # Gram(T) Rinv
     G = matmul_tn_dev(Rinv, H)               # Rinv^T Gram(T) Rinv
-    V, d = sym_eig_dev(G, symmetrize=True)   # (G + G^T)/2, as sym_eig does
-    S = gram_spectrum(device.to_host(d))
+    try:
+        V, d = sym_eig_dev(G, symmetrize=True)   # (G + G^T)/2, as sym_eig does
+    except NumericalError:
+        _check_dev(T, "eig_svd input")
+        raise
+    dh = device.to_host(d)
+    if not np.all(np.isfinite(dh)):  # non-finite input: the reference's ValueError
+        _check_dev(T, "eig_svd input")
+    S = gram_spectrum(dh)
     _native.call("lr_fix_signs_f64", device.ptr(V), device.ld(V), n, n, None, 0, 0, _st())
     cols = np.asarray(cols, dtype=np.int64)
     Sd = device.f64_buffer(S)
@@ -514,7 +527,12 @@ def _tall_dense_svd_dev(A):
     orthonormal completion from a seeded Gaussian block)."""
     rows, n = A.shape
     G = gram_dev(A)
-    V, d = sym_eig_dev(G, symmetrize=False)
+    try:
+        V, d = sym_eig_dev(G, symmetrize=False)
+    except NumericalError:
+        if check:
+            _check_dev(A, "eig_svd input")  # a non-finite input is the reference's ValueError
+        raise
     dh = device.to_host(d)[::-1].copy()  # descending
     S = np.sqrt(np.maximum(dh, 0.0))
     order = np.arange(n - 1, -1, -1)
