@@ -98,7 +98,9 @@ __device__ __forceinline__ void td_reflector(const double* x, int j, int n, doub
 // after step j-1); after it every CTA forms w, updates its rows, rebuilds
 // row j+1 after step j from the published copy with the same rank-2 formula
 // and derives the next reflector redundantly.
-template <int THREADS>
+// SINGLE (one CTA holds every row, n <= 96): p, the row j+1 copy and the
+// p.v partial stay in shared memory -- no L2 round trip per column.
+template <int THREADS, bool SINGLE = false>
 __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double td_smem[];
@@ -112,9 +114,11 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
   double* v = P.rows_global ? td_smem : td_smem + (size_t)P.rows_per * LD;  // n
   double* w = v + n;                                                       // n
   double* x = w + n;                                                       // n
+  double* psh = x + n;                                // n (SINGLE: p in shared memory)
   __shared__ double red[32];
   __shared__ double sh[4];
   const bool rec = blockIdx.x == 0;
+  auto ldx = [](const double* q) { return SINGLE ? *q : __ldcg(q); };
 
   for (int e = tid; e < nr * n; e += THREADS) {
     const int i = e / n, c = e - (e / n) * n;
@@ -130,8 +134,8 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
 
   for (int j = 0; j + 2 < n; ++j) {
     const int par = j & 1;
-    double* pg = P.pbuf + par * n;
-    double* rg = P.vbuf + (1 - par) * n;  // row j+1 (vbuf[0] held row 0)
+    double* pg = SINGLE ? psh : P.pbuf + par * n;
+    double* rg = SINGLE ? R + (j + 1) * LD : P.vbuf + (1 - par) * n;  // row j+1 (vbuf[0] held row 0)
     const double tau = sh[0];
     long long* prof = (P.prof && blockIdx.x == 0 && tid == 0) ? P.prof : nullptr;
     long long tp[6];
@@ -158,10 +162,13 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
       if (tid == 0) {
         double t = 0.0;
         for (int q = 0; q < THREADS / 32; ++q) t += red[q];
-        P.pvbuf[par * gridDim.x + blockIdx.x] = t;
+        if (SINGLE)
+          sh[3] = t;
+        else
+          P.pvbuf[par * gridDim.x + blockIdx.x] = t;
       }
     }
-    if (j + 1 >= r0 && j + 1 < r1)
+    if (!SINGLE && j + 1 >= r0 && j + 1 < r1)
       for (int c = j + 1 + tid; c < n; c += THREADS) rg[c] = R[(j + 1 - r0) * LD + c];
     if (prof) tp[1] = clock64();
     td_barrier(grid);
@@ -178,18 +185,23 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
 #pragma unroll
       for (int u = 0; u < TD_EPT; ++u) {
         const int c = j + 1 + tid + u * THREADS;
-        pcs[u] = c < n ? __ldcg(pg + c) : 0.0;
-        xcs[u] = c < n ? __ldcg(rg + c) : 0.0;
+        pcs[u] = c < n ? ldx(pg + c) : 0.0;
+        xcs[u] = c < n ? ldx(rg + c) : 0.0;
       }
+      double pv;
+      if (SINGLE) {
+        pv = sh[3];
+      } else {
 #pragma unroll
-      for (int u = 0; u < TD_PPL; ++u) {
-        const int q = lane + 32 * u;
-        pps[u] = q < (int)gridDim.x ? __ldcg(P.pvbuf + par * gridDim.x + q) : 0.0;
+        for (int u = 0; u < TD_PPL; ++u) {
+          const int q = lane + 32 * u;
+          pps[u] = q < (int)gridDim.x ? __ldcg(P.pvbuf + par * gridDim.x + q) : 0.0;
+        }
+        pv = 0.0;
+#pragma unroll
+        for (int u = 0; u < TD_PPL; ++u) pv += pps[u];
+        pv = warp_sum(pv);
       }
-      double pv = 0.0;
-#pragma unroll
-      for (int u = 0; u < TD_PPL; ++u) pv += pps[u];
-      pv = warp_sum(pv);
       const double K = 0.5 * tau * pv;
 #pragma unroll
       for (int u = 0; u < TD_EPT; ++u) {
@@ -203,8 +215,8 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
       double pv = 0.0;
       {
         for (int c = j + 1 + tid; c < n; c += THREADS) {
-          const double pc = __ldcg(pg + c);
-          x[c] = __ldcg(rg + c);
+          const double pc = ldx(pg + c);
+          x[c] = ldx(rg + c);
           w[c] = pc;
           pv = fma(pc, v[c], pv);
         }
@@ -217,7 +229,7 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
     } else {
       for (int c = j + 1 + tid; c < n; c += THREADS) {
         w[c] = 0.0;
-        x[c] = __ldcg(rg + c);
+        x[c] = ldx(rg + c);
       }
     }
     __syncthreads();
@@ -742,14 +754,16 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
   static bool attr = false;
   if (!attr) {
     LR_CHECK_CUDA(cudaFuncSetAttribute(tridiag_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    LR_CHECK_CUDA(cudaFuncSetAttribute(tridiag_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    LR_CHECK_CUDA(cudaFuncSetAttribute(tridiag_kernel<1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       220 * 1024));
     LR_CHECK_CUDA(cudaFuncSetAttribute(wy_apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 214 * 1024));
     LR_CHECK_CUDA(cudaFuncSetAttribute(wy_apply_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 214 * 1024));
     attr = true;
   }
   int occ = 0;
   const bool single = pl.G == 1;
-  const void* tdk = single ? (const void*)tridiag_kernel<1024> : (const void*)tridiag_kernel<256>;
+  const void* tdk = single ? (const void*)tridiag_kernel<1024, true> : (const void*)tridiag_kernel<256>;
+  if (single) pl.smem += (size_t)n * sizeof(double);  // p in shared memory
   LR_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tdk, single ? 1024 : 256, pl.smem));
   LR_REQUIRE((long long)occ * sm_count() >= pl.G, "syevd: cooperative grid %d exceeds residency", pl.G);
   TdParams P;
