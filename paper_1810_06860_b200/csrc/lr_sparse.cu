@@ -458,9 +458,36 @@ static int spmm_cols(const int* ptr, const int* idx, const Sc* val, const int* i
   // W-column Y^T Q of BKI at cfg2 is 528 MB), and the <= 128-column tiles run
   // at higher occupancy than the 192-column one even when X fits in L2
   // (cfg4 CSR w = 132: 2.64 ms chunked vs 4.04 ms whole, tools/spmm_cfg4_probe.py).
-  constexpr int kChunkCols = 128;
+  // Chunk count by a measured cost model: a pass over the entries with a
+  // chunk of pc column pairs costs ~ (cap(pc) + 14) units per stored entry,
+  // cap = the pair slots of dispatch_spmm's (G,T) mapping (1..96), 14 = the
+  // per-pass entry overhead (fit to the cfg4 width sweep: 163 us + 11.4 us
+  // per slot at 18M nnz, tools/spmm_cfg4_probe.py).  Cost = chunks x (cap +
+  // 14); chunks are at most 128 columns.  E.g. w = 132: 3 chunks of 22 pairs
+  // (1.77 -> 1.59 ms at cfg4) instead of 2 of 33; w = 110 stays one chunk.
+  // LR_SPMM_CHUNK forces a fixed chunk width.
+  static const int chunk_env = getenv("LR_SPMM_CHUNK") ? atoi(getenv("LR_SPMM_CHUNK")) : 0;
   constexpr unsigned kVecBytes = 2 * sizeof(Sc);
-  const int n_chunks = (w + kChunkCols - 1) / kChunkCols;
+  const int pairs_all = (w + 1) / 2;
+  auto cap = [](int pc) {
+    return pc <= 1 ? 1 : pc <= 2 ? 2 : pc <= 4 ? 4 : pc <= 8 ? 8 : pc <= 16 ? 16 : pc <= 32 ? 32 : pc <= 64 ? 64 : 96;
+  };
+  int n_chunks = 1;
+  if (chunk_env > 0) {
+    n_chunks = (w + chunk_env - 1) / chunk_env;
+  } else {
+    long long best = -1;
+    for (int c = 1; c <= pairs_all; ++c) {
+      const int pc = (pairs_all + c - 1) / c;
+      if (2 * pc > 128) continue;
+      const long long score = (long long)c * (cap(pc) + 14);
+      if (best < 0 || score < best) {
+        best = score;
+        n_chunks = c;
+      }
+      if (pc <= 8) break;  // narrower chunks only add metadata passes
+    }
+  }
   const int cw_even = (((w + n_chunks - 1) / n_chunks) + 1) & ~1;
   for (int c0 = 0; c0 < w; c0 += cw_even) {
     const int cw = (w - c0 < cw_even) ? (w - c0) : cw_even;
