@@ -694,7 +694,7 @@ static TdPlan td_plan(int n) {
   const int sms = sm_count();
   // CTAs: every CTA re-reads the broadcast vectors each column, so fewer,
   // fatter CTAs cut L2 contention (tunable: LR_TD_ROWS = rows per CTA)
-  static const int rows_pref = getenv("LR_TD_ROWS") ? atoi(getenv("LR_TD_ROWS")) : 4;
+  static const int rows_pref = getenv("LR_TD_ROWS") ? atoi(getenv("LR_TD_ROWS")) : 8;  // swept: tools/td_rows_probe.py
   int G = n <= 96 ? 1 : (n + rows_pref - 1) / rows_pref;
   if (G > sms) G = sms;
   int rows_per = (n + G - 1) / G;
