@@ -7,7 +7,7 @@ python tools/ncu_target.py > gpurun_out/${tag}_target.log 2>&1 || exit 1
 [ -z "$SKIP_LAUNCHES" ] && ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/${tag}_launches.csv \
     python bench.py --steps 2 --warmup 1 --cpu-baseline skip --svt off --e2e-steps 0 > gpurun_out/${tag}_launches.log 2>&1
 # name regex : launches to skip (first matching launch after the skip is captured)
-KERNELS=${KERNELS:-"gemm_kernel<lr::Tile<128, 64, 64, 32, 32, 2>, 1>:0|gemm_kernel<lr::Tile<128, 64, 32, 32, 32, 2>, 0>:0|spmm_kernel<32, 2, 1, 4, double>:0|spmm_kernel<32, 2, 1, 4, float>:0|lu_kernel:0|tridiag_kernel:0|chol_coop_kernel:0|bisect_kernel:0"}
+KERNELS=${KERNELS:-"gemm_kernel:0|spmm_kernel:0|lu_kernel:0|tridiag_kernel:0|chol_coop_kernel:0|bisect_kernel:0"}
 IFS='|' read -ra SPECS <<< "$KERNELS"
 for spec in "${SPECS[@]}"; do
   k=${spec%:*}; skip=${spec##*:}
