@@ -261,6 +261,18 @@ def bench_svt(cpu: bool, peaks=None):
     d = {"iterations": res.iterations, "iterations_per_s": res.iterations / loop, "loop_s": loop, "total_s": total,
          "residual": res.residual, "rank": res.rank, "ks": [t.k for t in res.trace],
          "heldout_mae": completion.mae(res.predict(rt, ct), vt), "note": SVT_CFG4_NOTE}
+    # fp32 mode (SvtParams.precision, north_star's optional fp32 path): same run, sparse products in fp32
+    prm32 = completion.SvtParams(epsilon=0.17, i_reuse=5, q_reuse=10, strategy="reuse-q", seed=0, i_max=20,
+                                 delta=1.0, tau=5.0 * o4.n / 40, precision="fp32")
+    completion.svt_fast(obs4, prm32)
+    torch.cuda.synchronize()
+    res32 = completion.svt_fast(obs4, prm32)
+    torch.cuda.synchronize()
+    loop32 = sum(t.wall_time for t in res32.trace)
+    d["fp32_mode"] = {"iterations": res32.iterations, "iterations_per_s": res32.iterations / loop32,
+                      "residual": res32.residual, "rank": res32.rank,
+                      "residual_rel_diff_vs_fp64": abs(res32.residual - res.residual) / res.residual,
+                      "ks": [t.k for t in res32.trace]}
     if peaks is not None:  # kernel breakdown from a second, profiled run (events around every native call)
         prof = profiling.Profiler()
         _native.PROFILER = prof

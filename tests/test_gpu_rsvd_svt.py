@@ -344,3 +344,26 @@ def test_bki_speculative_matches_careful_path():
                 for x, y in zip(a[1:5], b[1:5]):
                     np.testing.assert_array_equal(x, y)
                 assert a[5] == b[5]
+
+
+def test_svt_fp32_mode_tracks_fp64():
+    """SvtParams(precision="fp32"): the inner SVDs' sparse products in fp32.
+    On cfg1 the loop reaches the fp64 iteration count +-1 with the residual
+    within 1e-4 relative (north_star's fp32 tolerance), and the completed
+    entries agree to 1e-4."""
+    from paper_1810_06860_b200 import completion, workloads
+    from paper_1810_06860_b200.sparse import ObservationSet
+
+    o, _ = workloads.cfg1()
+    ob = ObservationSet(o.m, o.n, o.rows, o.cols, o.values)
+    for eps in (0.05, 1e-3):
+        r64 = completion.svt_reference(ob, completion.SvtParams(seed=0, epsilon=eps), backend="rsvd-bki")
+        r32 = completion.svt_reference(ob, completion.SvtParams(seed=0, epsilon=eps, precision="fp32"),
+                                       backend="rsvd-bki")
+        assert abs(r32.iterations - r64.iterations) <= 1
+        assert abs(r32.residual - r64.residual) <= 1e-4 * r64.residual
+        rows, cols = o.rows[:2000], o.cols[:2000]
+        p64, p32 = r64.predict(rows, cols), r32.predict(rows, cols)
+        assert np.max(np.abs(p32 - p64)) <= 1e-4 * np.max(np.abs(p64))
+    with pytest.raises(ValueError, match="precision"):
+        completion.SvtParams(precision="bf16")
