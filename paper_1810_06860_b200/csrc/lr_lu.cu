@@ -180,8 +180,9 @@ __global__ void __launch_bounds__(LU_THREADS, (512 / LU_THREADS) > 0 ? (512 / LU
           // (2) arrive: the lanes' stores are ordered before thread 0's fence
           __syncwarp();
           if (lane == 0) {
-            __threadfence();
-            atomicAdd(p.bar, 1u);
+            // release-ordered arrive (cumulative over the warp's stores made
+            // visible to lane 0 by the __syncwarp): no separate full fence
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(p.bar) : "memory");
           }
         }
       }
