@@ -31,7 +31,7 @@ namespace cg = cooperative_groups;
 
 namespace lr {
 
-constexpr int TD_EPT = 4;
+constexpr int TD_NMAX_FAST = 2048;  // n up to which the post-barrier loads are one batch per thread
 constexpr int kPvSlots = 2 * 512;  // p.v partial slots (2 x G, G <= SM count)
 constexpr int TD_PPL = 8;   // p.v partials per lane: G <= 256  // trailing elements per thread loaded in one batch after the column barrier
 
@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
   __shared__ double sh[4];
   const bool rec = blockIdx.x == 0;
   auto ldx = [](const double* q) { return SINGLE ? *q : __ldcg(q); };
+  constexpr int EPT = (TD_NMAX_FAST + THREADS - 1) / THREADS;  // 8 at 256 threads, 2 at 1024
 
   for (int e = tid; e < nr * n; e += THREADS) {
     const int i = e / n, c = e - (e / n) * n;
@@ -175,15 +176,15 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
     if (prof) tp[2] = clock64();
     // (c) w = p - (tau/2)(p.v) v  (every CTA, full length); row j+1 copy in
     // the same pass so both vectors cost one L2 round trip
-    if (tau != 0.0 && n - (j + 1) <= TD_EPT * THREADS && (int)gridDim.x <= 32 * TD_PPL) {
+    if (tau != 0.0 && n - (j + 1) <= EPT * THREADS && (int)gridDim.x <= 32 * TD_PPL) {
       // every load of this thread in flight at once (one L2 round trip): its
       // p and row elements and a lane's share of the G partials of p.v,
       // which every warp folds in the same fixed order (bit-identical K in
       // every thread of every CTA, no block reduction)
       const int lane = tid & 31;
-      double pcs[TD_EPT], xcs[TD_EPT], pps[TD_PPL];
+      double pcs[EPT], xcs[EPT], pps[TD_PPL];
 #pragma unroll
-      for (int u = 0; u < TD_EPT; ++u) {
+      for (int u = 0; u < EPT; ++u) {
         const int c = j + 1 + tid + u * THREADS;
         pcs[u] = c < n ? ldx(pg + c) : 0.0;
         xcs[u] = c < n ? ldx(rg + c) : 0.0;
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
       }
       const double K = 0.5 * tau * pv;
 #pragma unroll
-      for (int u = 0; u < TD_EPT; ++u) {
+      for (int u = 0; u < EPT; ++u) {
         const int c = j + 1 + tid + u * THREADS;
         if (c < n) {
           x[c] = xcs[u];
