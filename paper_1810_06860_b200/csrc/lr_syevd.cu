@@ -235,25 +235,81 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
     }
     __syncthreads();
     if (prof) tp[3] = clock64();
-    // (d) rank-2 update of my rows; (e) row j+1 after step j from the copy
+    // (d) rank-2 update of my rows; (e) row j+1 after step j from the copy,
+    // with this thread's share of the next reflector's ||x[j+3:]||^2
+    const int lane = tid & 31, wp = tid >> 5;
+    double ssp = 0.0;
     if (tau != 0.0) {
-      const int lane = tid & 31, wp = tid >> 5;
       for (int i = max(0, j + 1 - r0) + wp; i < nr; i += THREADS / 32) {  // warp per row
         const int r = r0 + i;
         const double vr = v[r], wr = w[r];
         double* row = R + i * LD;
         for (int c = j + 1 + lane; c < n; c += 32) row[c] -= __dadd_rn(__dmul_rn(vr, w[c]), __dmul_rn(wr, v[c]));
       }
-      for (int c = j + 1 + tid; c < n; c += THREADS)
-        x[c] -= __dadd_rn(__dmul_rn(v[j + 1], w[c]), __dmul_rn(w[j + 1], v[c]));
+      for (int c = j + 1 + tid; c < n; c += THREADS) {
+        const double xc = x[c] - __dadd_rn(__dmul_rn(v[j + 1], w[c]), __dmul_rn(w[j + 1], v[c]));
+        x[c] = xc;
+        if (c >= j + 3) ssp = fma(xc, xc, ssp);
+      }
+    } else {
+      for (int c = j + 3 + tid; c < n; c += THREADS) ssp = fma(x[c], x[c], ssp);
     }
+    // one barrier closes the update and all-reduces ||x[j+3:]||^2 (every
+    // thread folds the warp partials in the same order: bit-identical
+    // reflectors in every thread of every CTA, no broadcast round)
+    if (THREADS > 256) {  // 32-warp CTA: the block reduction of td_reflector is cheaper than 32-way folds
+      __syncthreads();
+      if (prof) tp[4] = clock64();
+      if (j + 3 < n) {
+        td_reflector<THREADS>(x, j + 1, n, v, red, sh, P, rec);
+      } else if (rec && tid == 0) {  // j + 1 == n - 2: the last 2 x 2 block
+        P.d[n - 2] = x[n - 2];
+        P.e[n - 2] = x[n - 1];
+        sh[0] = 0.0;
+      }
+      __syncthreads();
+      if (prof) {
+        tp[5] = clock64();
+        for (int q = 0; q < 5; ++q) prof[q] += tp[q + 1] - tp[q];
+      }
+      continue;
+    }
+    ssp = warp_sum(ssp);
+    if (lane == 0) red[wp] = ssp;
     __syncthreads();
     if (prof) tp[4] = clock64();
     if (j + 3 < n) {
-      td_reflector<THREADS>(x, j + 1, n, v, red, sh, P, rec);
-    } else if (rec && tid == 0) {  // j + 1 == n - 2: the last 2 x 2 block
-      P.d[n - 2] = x[n - 2];
-      P.e[n - 2] = x[n - 1];
+      double ss = 0.0;
+#pragma unroll
+      for (int q = 0; q < THREADS / 32; ++q) ss += red[q];
+      // dlarfg on x[j+2:] for column j+1, as td_reflector
+      const int jr = j + 1;
+      const double alpha = x[jr + 1];
+      double tau1 = 0.0, beta = alpha, scal = 0.0;
+      if (ss != 0.0) {
+        const double nrm = sqrt(alpha * alpha + ss);
+        beta = (alpha >= 0.0) ? -nrm : nrm;
+        tau1 = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      if (tid == 0) {
+        sh[0] = tau1;
+        if (rec) {
+          P.d[jr] = x[jr];
+          P.e[jr] = beta;
+          P.tau[jr] = tau1;
+        }
+      }
+      for (int c = jr + 1 + tid; c < n; c += THREADS) {
+        const double vc = (c == jr + 1) ? 1.0 : (tau1 == 0.0 ? 0.0 : x[c] * scal);
+        v[c] = vc;
+        if (rec) P.Vr[(long long)jr * n + c] = vc;
+      }
+    } else if (tid == 0) {  // j + 1 == n - 2: the last 2 x 2 block
+      if (rec) {
+        P.d[n - 2] = x[n - 2];
+        P.e[n - 2] = x[n - 1];
+      }
       sh[0] = 0.0;
     }
     __syncthreads();
