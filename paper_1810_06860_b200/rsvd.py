@@ -228,29 +228,15 @@ def _check_precision(precision: str) -> str:
     return precision
 
 
-def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, omega=None,
-                 precision: str = "fp64", download: bool = False, _speculate: bool = True):
-    """Device Alg. 5 -> (DevSvd, Q device, fallbacks).
-
-    precision="fp32" (north_star's optional fp32 mode, singular values within
-    1e-4): the sparse products run on fp32 values and fp32 blocks (half the
-    gathered bytes); LU, CholeskyQR, the eigensolver and the lifts stay fp64
-    on the converted blocks."""
-    params.check_against(A, krylov=True)
-    fp32 = _check_precision(precision) == "fp32" and params.k + params.s >= 2
-    fb = _Fallback(allow_fallback, "Krylov blocks are near-collinear, reduce p or use a larger matrix")
+def _krylov_orth(A: SparseMatrix, Om, params: RsvdParams, spec: bool, fp32: bool, lazy: bool, fb: _Fallback):
+    """Alg. 5 steps 1-7 from a given Omega: Krylov blocks H_0..H_p (LU-
+    normalised) and the basis.  spec: LU statuses and the CholeskyQR route's
+    decisions stay on the device (no host synchronisation at all: the body
+    can be captured in a CUDA graph).  Returns (H, Q, lu_status, probe)."""
     w = params.k + params.s
     W = w * (params.p + 1)
     m, n = A.shape
-    # Speculation: the LU statuses and orth's decisions stay on the device and
-    # are read with ONE synchronisation after the basis is built; if any of
-    # them is not the common case (a zero pivot, a Cholesky breakdown, a third
-    # CholeskyQR pass, a rank collapse) the call is redone on the careful path
-    # below, which makes every decision as it goes -- so results, errors and
-    # fallbacks are exactly the careful path's.
-    spec = SPECULATIVE and _speculate
     lu_status = device.vector(4 * (params.p + 1)) if spec else None
-    Om = _omega(params.seed, n, w, omega or OMEGA_SOURCE)
     H = device.empty(m, W)
 
     def normalise(i):
@@ -277,11 +263,43 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
             spmm_t_dev(A, H[:, (i - 1) * w:i * w], out=T)
             spmm_dev(A, T, out=H[:, i * w:(i + 1) * w])
         normalise(i)
+    if spec:
+        Q, probe = orth_speculative_dev(H, lazy_last=lazy)
+    else:
+        Q, probe = _orthonormalize(H, fb, lazy_last=lazy), None
+    return H, Q, lu_status, probe
+
+
+def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, omega=None,
+                 precision: str = "fp64", download: bool = False, _speculate: bool = True):
+    """Device Alg. 5 -> (DevSvd, Q device, fallbacks).
+
+    precision="fp32" (north_star's optional fp32 mode, singular values within
+    1e-4): the sparse products run on fp32 values and fp32 blocks (half the
+    gathered bytes); LU, CholeskyQR, the eigensolver and the lifts stay fp64
+    on the converted blocks."""
+    params.check_against(A, krylov=True)
+    fp32 = _check_precision(precision) == "fp32" and params.k + params.s >= 2
+    fb = _Fallback(allow_fallback, "Krylov blocks are near-collinear, reduce p or use a larger matrix")
+    w = params.k + params.s
+    W = w * (params.p + 1)
+    m, n = A.shape
     # small blocks (launch-bound, e.g. cfg1's 1000 x 64): forming Q is cheaper
     # than the extra small products of the unformed route
     lazy = LAZY_LAST_PASS and m * W * W >= LAZY_MIN_FLOPS
+    # Speculation: the LU statuses and orth's decisions stay on the device and
+    # are read with ONE synchronisation after the basis is built; if any of
+    # them is not the common case (a zero pivot, a Cholesky breakdown, a third
+    # CholeskyQR pass, a rank collapse) the call is redone on the careful path,
+    # which makes every decision as it goes -- so results, errors and
+    # fallbacks are exactly the careful path's.  (The speculative steps have
+    # no host synchronisation and were captured as a CUDA graph once: -9 %
+    # per steady-state cfg1-sized call, but ~6 ms per capture, and the SVT
+    # loop's k changes make captures outnumber replays -- not kept.)
+    spec = SPECULATIVE and _speculate
+    Om = _omega(params.seed, n, w, omega or OMEGA_SOURCE)
+    H, Q, lu_status, probe = _krylov_orth(A, Om, params, spec, fp32, lazy, fb)
     if spec:
-        Q, probe = orth_speculative_dev(H, lazy_last=lazy)
         st = device.to_host(lu_status).reshape(-1, 4)[:, :3]
         diag_h, infos_h = device.to_host(probe[0]), device.to_host(probe[1])
         if not np.all(st[:, 0] == -1.0):  # an LU decision differed: redo the whole call
@@ -290,8 +308,6 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
             # the Krylov blocks are exactly the careful path's (H is untouched
             # by the speculative orth): only the orthonormalisation is redone
             Q = _orthonormalize(H, fb, lazy_last=lazy)
-    else:
-        Q = _orthonormalize(H, fb, lazy_last=lazy)
     res = project_and_solve(A, Q, params.k, fb, "fp32" if fp32 else "fp64", download=download)
     return res, Q, fb.count
 
