@@ -344,6 +344,7 @@ __device__ __forceinline__ int sturm_count(const double* __restrict__ d, const d
   double p = (d[0] - x) * inv_t;
   if (p == 0.0) p = -1e-290;
   int cnt = p < 0.0;
+#pragma unroll 4
   for (int i = 1; i < n; ++i) {
     const double a = (d[i] - x) * inv_t;
     const double t = (e2[i - 1] * inv_t2) * pm;
@@ -392,8 +393,18 @@ __global__ void tri_prep_kernel(const double* d, const double* e, int n, double*
 }
 
 // one warp per eigenvalue index k (k-th smallest)
-__global__ void bisect_kernel(const double* __restrict__ d, const double* __restrict__ e2, int n,
+__global__ void bisect_kernel(const double* __restrict__ dg, const double* __restrict__ e2g, int n,
                               const double* __restrict__ bounds, double* __restrict__ w) {
+  // d and e^2 staged in shared memory once per block: the Sturm recurrence
+  // then reads them at shared-memory latency, off the carried chain
+  extern __shared__ double bis_smem[];
+  double* d = bis_smem;
+  double* e2 = bis_smem + n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    d[i] = dg[i];
+    if (i + 1 < n) e2[i] = e2g[i];
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (k >= n) return;
@@ -864,7 +875,16 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
   // 2. eigenvalues (ascending) by multisection
   tri_prep_kernel<<<1, 256, 0, s>>>(d, e, n, e2, bounds);
   LR_CHECK_LAUNCH();
-  bisect_kernel<<<(n * 32 + 255) / 256, 256, 0, s>>>(d, e2, n, bounds, w);
+  {
+    const size_t bsm = 2 * (size_t)n * sizeof(double);
+    LR_REQUIRE(bsm <= 200 * 1024, "syevd: n = %d exceeds the bisection staging limit", n);
+    static bool battr = false;
+    if (!battr) {
+      LR_CHECK_CUDA(cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      battr = true;
+    }
+    bisect_kernel<<<(n * 32 + 255) / 256, 256, bsm, s>>>(d, e2, n, bounds, w);
+  }
   LR_CHECK_LAUNCH();
   if (timing) cudaEventRecord(ev[2], s);
   // 3. eigenvectors of T
