@@ -178,6 +178,39 @@ __device__ __forceinline__ void cb_store(double* __restrict__ A, long long lda, 
 }
 
 // out = D^T X (D upper: D^T lower -> k <= i), 32 x 32; thread owns row i, 4 cols
+// three tiles at once: every global load of the thread is issued before any
+// shared store (one L2 round trip instead of one per tile); null src -> skip
+__device__ __forceinline__ void cb_load3(const double* A0, long long ld0, int n0, int I0, int K0, double (*t0)[CB_LD],
+                                         const double* A1, long long ld1, int n1, int I1, int K1, double (*t1)[CB_LD],
+                                         const double* A2, long long ld2, int n2, int I2, int K2,
+                                         double (*t2)[CB_LD]) {
+  constexpr int PER = CB * CB / CB_THREADS;
+  double v0[PER], v1[PER], v2[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int e = threadIdx.x + u * CB_THREADS, i = e >> 5, c = e & 31;
+    {
+      const int gi = I0 * CB + i, gc = K0 * CB + c;
+      v0[u] = (gi < n0 && gc < n0) ? A0[(long long)gi * ld0 + gc] : 0.0;
+    }
+    if (A1) {
+      const int gi = I1 * CB + i, gc = K1 * CB + c;
+      v1[u] = (gi < n1 && gc < n1) ? A1[(long long)gi * ld1 + gc] : 0.0;
+    }
+    {
+      const int gi = I2 * CB + i, gc = K2 * CB + c;
+      v2[u] = (gi < n2 && gc < n2) ? A2[(long long)gi * ld2 + gc] : 0.0;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int e = threadIdx.x + u * CB_THREADS, i = e >> 5, c = e & 31;
+    t0[i][c] = v0[u];
+    if (A1) t1[i][c] = v1[u];
+    t2[i][c] = v2[u];
+  }
+}
+
 __device__ __forceinline__ void cb_dtx(const double (*D)[CB_LD], const double (*X)[CB_LD], double (*out)[CB_LD]) {
   const int i = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 4;
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -378,10 +411,8 @@ __global__ void __launch_bounds__(CB_THREADS) chol_coop_kernel(int n, double* A,
       if (t < Tc) {
         int K, L;
         cb_tile_of(t, J, nb, K, L);
-        // all four operand tiles in flight at once (one L2 round trip per tile)
-        cb_load(A, lda, n, J, K, ld);
-        if (K != L) cb_load(A, lda, n, J, L, al);
-        cb_load(A, lda, n, K, L, tt);
+        // the operand tiles in flight at once (one L2 round trip)
+        cb_load3(A, lda, n, J, K, ld, K != L ? A : nullptr, lda, n, J, L, al, A, lda, n, K, L, tt);
         __syncthreads();
         cb_dtx(dinv, ld, pk);
         if (K != L) cb_dtx(dinv, al, pl);
@@ -409,9 +440,7 @@ __global__ void __launch_bounds__(CB_THREADS) chol_coop_kernel(int n, double* A,
       } else if (t < Tc + Ti) {
         const int u = t - Tc;
         const int K = J + 1 + u / (J + 1), L = u % (J + 1);
-        cb_load(A, lda, n, J, K, ld);
-        cb_load(Acc, np, np, J, L, al);
-        cb_load(Acc, np, np, K, L, tt);
+        cb_load3(A, lda, n, J, K, ld, Acc, np, np, J, L, al, Acc, np, np, K, L, tt);
         __syncthreads();
         cb_dtx(dinv, ld, pk);   // R_JK
         cb_dtx(dinv, al, pl);   // W_JL
