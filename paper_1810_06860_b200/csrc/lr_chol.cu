@@ -252,6 +252,16 @@ __device__ __forceinline__ void cb_sub_ptq(const double (*P)[CB_LD], const doubl
 // carry no block barriers (a __syncthreads per step made this 25x slower).
 // Returns the 1-based global column of a non-positive pivot, 0 if fine;
 // called by ALL threads (warp 0 computes), result block-uniform.
+__device__ __forceinline__ double cb_rsqrt(double d) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  // Newton: y <- y (1.5 - 0.5 d y^2), twice (the seed has ~2^-22 relative error)
+  const double hd = 0.5 * d;
+  y = y * fma(-hd * y, y, 1.5);
+  y = y * fma(-hd * y, y, 1.5);
+  return y;
+}
+
 __device__ int cb_factor(double (*t)[CB_LD], double (*x)[CB_LD], double* rowbuf, int J, int n) {
   __shared__ int s_bad;
   __syncthreads();
@@ -273,9 +283,11 @@ __device__ int cb_factor(double (*t)[CB_LD], double (*x)[CB_LD], double* rowbuf,
         bad = J * CB + j + 1;
         break;
       }
-      // LAPACK dpotf2 scales the row by 1/R_jj; sqrt and rsqrt issue in parallel
-      const double r = sqrt(d);
-      const double ri = rsqrt(d);
+      // LAPACK dpotf2 scales the row by 1/R_jj.  1/sqrt(d) from the MUFU
+      // seed and two Newton steps (the library sqrt / rsqrt sit on this
+      // column-to-column chain for ~100+ cycles each); R_jj = d / sqrt(d)
+      const double ri = cb_rsqrt(d);
+      const double r = d * ri;
       double v = (lane == j) ? r : a[j] * ri;  // R[j][lane]
       if (lane < j) v = 0.0;
       if (lane == j) rinv_lane = ri;
