@@ -35,6 +35,27 @@ constexpr int TD_NMAX_FAST = 2048;  // n up to which the post-barrier loads are 
 constexpr int kPvSlots = 2 * 512;  // p.v partial slots (2 x G, G <= SM count)
 constexpr int TD_PPL = 8;   // p.v partials per lane: G <= 256  // trailing elements per thread loaded in one batch after the column barrier
 
+// 1/x to within an ulp: MUFU.RCP64H seed refined by two Newton steps (x is a
+// clamped pivot: never zero, never denormal)
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// 1/sqrt(x) for x > 0: MUFU.RSQ64H seed and two Newton steps
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
 struct TdParams {
   const double* A;
   long long lda;
@@ -70,10 +91,11 @@ __device__ __forceinline__ void td_reflector(const double* x, int j, int n, doub
     const double alpha = x[j + 1];
     double tau = 0.0, beta = alpha, scal = 0.0;
     if (ss != 0.0) {
-      const double nrm = sqrt(alpha * alpha + ss);
+      const double x2 = alpha * alpha + ss;
+      const double nrm = x2 * fast_rsqrt(x2);
       beta = (alpha >= 0.0) ? -nrm : nrm;
-      tau = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
+      tau = (beta - alpha) * fast_rcp(beta);
+      scal = fast_rcp(alpha - beta);
     }
     sh[0] = tau;
     sh[1] = scal;
@@ -287,10 +309,13 @@ __global__ void __launch_bounds__(THREADS) tridiag_kernel(TdParams P) {
       const double alpha = x[jr + 1];
       double tau1 = 0.0, beta = alpha, scal = 0.0;
       if (ss != 0.0) {
-        const double nrm = sqrt(alpha * alpha + ss);
+        // on the column-to-column chain: MUFU seeds + Newton instead of the
+        // library sqrt and two divisions
+        const double x2 = alpha * alpha + ss;
+        const double nrm = x2 * fast_rsqrt(x2);
         beta = (alpha >= 0.0) ? -nrm : nrm;
-        tau1 = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
+        tau1 = (beta - alpha) * fast_rcp(beta);
+        scal = fast_rcp(alpha - beta);
       }
       if (tid == 0) {
         sh[0] = tau1;
@@ -439,16 +464,6 @@ __global__ void bisect_kernel(const double* __restrict__ dg, const double* __res
   if (lane == 0) w[k] = 0.5 * (lo + hi);
 }
 
-// 1/x to within an ulp: MUFU.RCP64H seed refined by two Newton steps (x is a
-// clamped pivot: never zero, never denormal)
-__device__ __forceinline__ double fast_rcp(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
 
 // inverse iteration, one thread per eigenvalue; scratch laid out [i * n + k]
 // (coalesced across the warp).  Values that the recurrences carry stay in
