@@ -49,6 +49,18 @@ struct LuParams {
   long long* prof;      // optional per-phase clock totals of CTA 0 (LR_LU_PROFILE)
 };
 
+// 1/x on the column chain: MUFU seed + two Newton steps (within an ulp of
+// the IEEE quotient; pivots are nonzero and far from the denormal range,
+// |pivot| >= 1e-14 max|X| or the factorization stops)
+__device__ __forceinline__ double lu_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 __device__ __forceinline__ void better(double& v, int& r, double v2, int r2) {
   if (v2 > v || (v2 == v && r2 < r)) {
     v = v2;
@@ -250,7 +262,7 @@ __global__ void __launch_bounds__(LU_THREADS, (512 / LU_THREADS) > 0 ? (512 / LU
       }
       if (prof) t3 = clock64();
       // (6) multipliers (LAPACK dgetf2: scale by 1/pivot), column jj+1, next candidate
-      const double rpiv = 1.0 / urow[jj];
+      const double rpiv = lu_rcp(urow[jj]);
       cbv = -1.0;
       cbr = 0x7fffffff;
       const bool look = jj + 1 < jb;
@@ -486,7 +498,7 @@ __global__ void __launch_bounds__(LUS_THREADS) lu_small_kernel(double* X, long l
         s_bad = !(v >= tol) || v == 0.0;
         if (!s_bad) {
           pivflag[r] = j;
-          s_rpiv = 1.0 / P[r * LD + j];  // LAPACK dgetf2: scale by 1/pivot
+          s_rpiv = lu_rcp(P[r * LD + j]);  // LAPACK dgetf2: scale by 1/pivot
         }
       }
     }
