@@ -156,11 +156,17 @@ __global__ void __launch_bounds__(kStatsThreads) power_dots_kernel(const double*
 
 // state = {prev, curr, done, iters, zero_hit, zn}
 __global__ void power_scalar_kernel(const double* partial, int nb, double tol, double* state) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int lane = threadIdx.x;
+  if (lane >= 32 || blockIdx.x != 0) return;
   if (state[2] != 0.0) return;
   double lam = 0, zz = 0;
-  for (int i = 0; i < nb; ++i) lam += partial[i];
-  for (int i = 0; i < nb; ++i) zz += partial[nb + i];
+  for (int i = lane; i < nb; i += 32) {  // one warp, fixed-order folds
+    lam += partial[i];
+    zz += partial[nb + i];
+  }
+  lam = warp_sum(lam);
+  zz = warp_sum(zz);
+  if (lane != 0) return;
   double zn = sqrt(zz);
   state[0] = state[1];
   state[1] = sqrt(fmax(lam, 0.0));
