@@ -1,0 +1,138 @@
+"""Host-side logic that runs without a GPU: argument validation with the
+reference's error types (completion.py:44-88, rsvd.py RsvdParams,
+sparse.py:84-104 / :200-246), the SpMM work-item schedule, the Gram-spectrum
+rank checks (linalg.py:190-198), and the loud failure of the product path
+when no CUDA device is present (no CPU fallback)."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1810_06860_b200 import completion, linalg, rsvd, sparse, workloads
+from paper_1810_06860_b200.errors import DataError, RankDeficiencyError
+from paper_1810_06860_b200.sparse import SparseMatrix
+
+
+@pytest.mark.parametrize("kw", [dict(tau=0.0), dict(delta=-1.0), dict(l=0), dict(epsilon=1.0), dict(epsilon=0.0),
+                                dict(i_max=0), dict(i_reuse=0), dict(q_reuse=-1), dict(strategy="nope"),
+                                dict(p0=0), dict(p_min=0), dict(s=-1), dict(precision="bf16")])
+def test_svt_params_reject(kw):
+    with pytest.raises(ValueError):
+        completion.SvtParams(**kw)
+
+
+def test_svt_params_defaults():
+    p = completion.SvtParams()
+    assert (p.l, p.epsilon, p.i_max, p.i_reuse, p.q_reuse, p.strategy, p.p0, p.p_min, p.s) == \
+        (5, 0.05, 500, 100, 10, "none", 3, 1, 5)
+    assert p.tau is None and p.delta is None and p.precision == "fp64"
+    assert completion.SvtParams(precision="fp32").precision == "fp32"
+
+
+@pytest.mark.parametrize("kw", [dict(k=0, p=1), dict(k=3, p=-1), dict(k=3, p=1, s=-1)])
+def test_rsvd_params_reject(kw):
+    with pytest.raises(ValueError):
+        rsvd.RsvdParams(**kw)
+
+
+def test_rsvd_params_width_check():
+    A = SparseMatrix.from_coo(20, 12, [0, 1], [0, 1], [1.0, 2.0])
+    rsvd.RsvdParams(k=2, p=1, s=1).check_against(A, krylov=True)  # (2+1)*2 = 6 <= 12
+    with pytest.raises(ValueError, match="sketch width"):
+        rsvd.RsvdParams(k=3, p=2, s=2).check_against(A, krylov=True)  # 15 > 12
+    rsvd.RsvdParams(k=3, p=2, s=2).check_against(A, krylov=False)  # 5 <= 12
+
+
+def test_sparse_validation():
+    with pytest.raises(DataError):
+        SparseMatrix(0, 3, [0], [], [])
+    with pytest.raises(DataError):
+        SparseMatrix(2, 3, [0, 1], [0], [1.0])  # indptr length
+    with pytest.raises(DataError):
+        SparseMatrix(2, 3, [0, 2, 1], [0, 1], [1.0, 1.0])  # not monotone
+    with pytest.raises(DataError):
+        SparseMatrix(2, 3, [0, 1, 2], [0, 3], [1.0, 1.0])  # column out of range
+    with pytest.raises(DataError):
+        SparseMatrix(1, 3, [0, 2], [1, 1], [1.0, 1.0])  # not strictly increasing
+    with pytest.raises(DataError):
+        SparseMatrix(1, 3, [0, 1], [1], [np.nan])
+    # a new row may restart at a smaller column
+    SparseMatrix(2, 3, [0, 2, 3], [1, 2, 0], [1.0, 2.0, 3.0])
+    # empty pattern is legal
+    SparseMatrix(2, 3, [0, 0, 0], [], [])
+
+
+def test_from_coo_sorts_and_rejects_duplicates():
+    A = SparseMatrix.from_coo(3, 3, [2, 0, 0], [1, 2, 0], [5.0, 2.0, 1.0])
+    assert A.indptr.tolist() == [0, 2, 2, 3]
+    assert A.indices.tolist() == [0, 2, 1]
+    with pytest.raises(DataError):
+        SparseMatrix.from_coo(3, 3, [1, 1], [2, 2], [1.0, 1.0])
+    with pytest.raises(DataError):
+        SparseMatrix.from_coo(3, 3, [3], [0], [1.0])
+
+
+def _check_schedule(indptr, chunk):
+    items, splits, n_slots = sparse._schedule(indptr, chunk)
+    lens = np.diff(indptr)
+    if items is None:
+        assert lens.max(initial=0) <= chunk
+        return
+    # every stored entry is covered by exactly one item
+    cover = np.zeros(int(indptr[-1]), dtype=np.int64)
+    for r, b, e, s in items:
+        assert indptr[r] <= b < e <= indptr[r + 1] or b == e == indptr[r]
+        cover[b:e] += 1
+    assert (cover == 1).all()
+    # long rows own consecutive split slots, short rows write their row directly
+    slots = sorted(int(s) for s in items[:, 3] if s >= 0)
+    assert slots == list(range(n_slots))
+    for r, sb, se, _ in splits:
+        assert lens[r] > chunk and se - sb == -(-lens[r] // chunk)
+    # longest first
+    w = items[:, 2] - items[:, 1]
+    assert (np.diff(w) <= 0).all()
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_spmm_schedule_covers_pattern(seed):
+    rng = np.random.default_rng(seed)
+    lens = np.minimum(rng.zipf(1.6, size=500), 3000)
+    lens[::37] = 0  # empty rows
+    indptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    for chunk in (32, 64, 256):
+        _check_schedule(indptr, chunk)
+
+
+def test_spmm_schedule_chunk_size():
+    indptr = np.arange(0, 1001 * 200, 200, dtype=np.int64)  # cfg1: 1000 rows of 200
+    assert sparse._chunk_for(indptr) == sparse.MIN_CHUNK
+    big = np.array([0, 10**9], dtype=np.int64)
+    assert sparse._chunk_for(big) == sparse.SPLIT_CHUNK
+
+
+def test_gram_spectrum_rank_checks():
+    d = np.array([1e-3, 0.5, 4.0])
+    assert np.allclose(linalg.gram_spectrum(d), np.sqrt(d))
+    with pytest.raises(RankDeficiencyError):
+        linalg.gram_spectrum(np.array([-1.0, 0.0]))
+    with pytest.raises(RankDeficiencyError):
+        linalg.gram_spectrum(np.array([0.0, 1.0, 4.0]))
+
+
+def test_workloads_deterministic():
+    a, _ = workloads.cfg1_small()
+    b, _ = workloads.cfg1_small()
+    assert (a.rows == b.rows).all() and (a.cols == b.cols).all() and (a.values == b.values).all()
+    assert a.rows.max() < a.m and a.cols.max() < a.n
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_product_path_fails_loudly_without_cuda():
+    A = SparseMatrix.from_coo(30, 20, np.arange(20), np.arange(20), np.ones(20))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        rsvd.rsvd_bki(A, rsvd.RsvdParams(k=2, p=1, s=1))
+    o, _ = workloads.cfg1_small()
+    obs = sparse.ObservationSet(o.m, o.n, o.rows, o.cols, o.values)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        completion.svt_fast(obs, completion.SvtParams(i_max=1))
