@@ -179,8 +179,10 @@ int lr_syevj_f64(int n, double* A, long long lda, double* d, double* V, long lon
  * iteration (+ MGS inside clusters closer than 1e-8*||A||), then the
  * back-transform.  Eigenvalues ascending in d, eigenvectors in V; A is not
  * modified.  LAPACK-level accuracy (absolute eps*||A||), the default solver
- * behind sym_eig / eig_svd (linalg.py:153-202).  clusters_host (optional)
- * receives the number of re-orthonormalised clusters.  Synchronizes once. */
+ * behind sym_eig / eig_svd (linalg.py:153-202).  Clusters are found on the
+ * device; the call is asynchronous unless clusters_host is non-NULL, in which
+ * case it synchronizes the stream and stores the number of re-orthonormalised
+ * clusters there. */
 long long lr_syevd_workspace_doubles(int n);
 int lr_syevd_f64(int n, const double* A, long long lda, double* d, double* V, long long ldv, double* work,
                  int* clusters_host, void* stream);

@@ -595,8 +595,7 @@ __global__ void inviter_kernel(const double* __restrict__ d, const double* __res
 }
 
 // modified Gram-Schmidt (twice) over a cluster [k0, k1) of columns of Z (n x n row-major)
-__global__ void __launch_bounds__(256) cluster_mgs_kernel(double* Z, int n, const int* clusters) {
-  const int k0 = clusters[2 * blockIdx.x], k1 = clusters[2 * blockIdx.x + 1];
+__device__ void cluster_mgs_one(double* Z, int n, const int k0, const int k1) {
   __shared__ double red[32];
   __shared__ double coef;
   for (int pass = 0; pass < 2; ++pass) {
@@ -621,6 +620,43 @@ __global__ void __launch_bounds__(256) cluster_mgs_kernel(double* Z, int n, cons
       __syncthreads();
     }
   }
+}
+
+// Clusters of the ascending eigenvalues w: maximal runs [k0, k1), k1 - k0 > 1,
+// of neighbours within ctol = 1e-8 * max(|lambda|) (bounds[3]).  One warp, 32
+// entries per step: a run starts where the gap to the left is open and the gap
+// to the right closed, ends where the reverse holds; the k-th start pairs with
+// the k-th end.  Written to clusters[0 .. 2 ncl) and count[0] on the device, so
+// the eigensolver never waits for the host.
+__global__ void cluster_find_kernel(const double* __restrict__ w, const double* __restrict__ bounds, int n,
+                                    int* __restrict__ clusters, int* __restrict__ count) {
+  const int lane = threadIdx.x;
+  const double ctol = 1e-8 * fmax(bounds[3], 1e-300);
+  const unsigned below = (1u << lane) - 1u;
+  int cs = 0, ce = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    bool st = false, en = false;
+    if (i < n) {
+      const double wi = w[i];
+      const bool prev_close = i > 0 && wi - w[i - 1] <= ctol;
+      const bool next_close = i + 1 < n && w[i + 1] - wi <= ctol;
+      st = !prev_close && next_close;
+      en = prev_close && !next_close;
+    }
+    const unsigned bs = __ballot_sync(~0u, st), be = __ballot_sync(~0u, en);
+    if (st) clusters[2 * (cs + __popc(bs & below))] = i;
+    if (en) clusters[2 * (ce + __popc(be & below)) + 1] = i + 1;
+    cs += __popc(bs);
+    ce += __popc(be);
+  }
+  if (lane == 0) count[0] = cs;
+}
+
+// grid-stride over the clusters found by cluster_find_kernel (count on the device)
+__global__ void __launch_bounds__(256) cluster_mgs_kernel(double* Z, int n, const int* clusters, const int* count) {
+  const int ncl = count[0];
+  for (int c = blockIdx.x; c < ncl; c += gridDim.x) cluster_mgs_one(Z, n, clusters[2 * c], clusters[2 * c + 1]);
 }
 
 // T factor of each block of kWY reflectors (dlarft, forward, columnwise):
@@ -906,39 +942,16 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
   inviter_kernel<<<(n + 63) / 64, 64, 0, s>>>(d, e, n, w, bounds, Z, U1, U2, Lm, Dg, Pv);
   LR_CHECK_LAUNCH();
   if (timing) cudaEventRecord(ev[3], s);
-  // 4. clusters (host decides from the eigenvalues: one small D2H)
-  double* wh = new double[n + 4];
-  LR_CHECK_CUDA(cudaMemcpyAsync(wh, w, N * sizeof(double), cudaMemcpyDeviceToHost, s));
-  LR_CHECK_CUDA(cudaMemcpyAsync(wh + n, bounds, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
-  LR_CHECK_CUDA(cudaStreamSynchronize(s));
-  const double ctol = 1e-8 * fmax(wh[n + 3], 1e-300);
-  int* ch = new int[2 * n];
-  int ncl = 0;
-  for (int i = 0; i < n;) {
-    int j = i + 1;
-    while (j < n && wh[j] - wh[j - 1] <= ctol) ++j;
-    if (j - i > 1) {
-      ch[2 * ncl] = i;
-      ch[2 * ncl + 1] = j;
-      ++ncl;
-    }
-    i = j;
+  // 4. clusters, found on the device (no host round trip inside the eigensolver)
+  int* ncl_dev = clus + 2 * N;  // inside the 64-double pad after the cluster pairs
+  cluster_find_kernel<<<1, 32, 0, s>>>(w, bounds, n, clus, ncl_dev);
+  LR_CHECK_LAUNCH();
+  cluster_mgs_kernel<<<std::max(1, std::min(n / 2, 64)), 256, 0, s>>>(Z, n, clus, ncl_dev);
+  LR_CHECK_LAUNCH();
+  if (clusters_host) {  // optional diagnostic: costs a stream sync
+    LR_CHECK_CUDA(cudaMemcpyAsync(clusters_host, ncl_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LR_CHECK_CUDA(cudaStreamSynchronize(s));
   }
-  if (ncl) {
-    cudaError_t ce = cudaMemcpyAsync(clus, ch, 2 * ncl * sizeof(int), cudaMemcpyHostToDevice, s);
-    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
-    if (ce != cudaSuccess) {
-      delete[] wh;
-      delete[] ch;
-      set_error("syevd: cluster upload: %s", cudaGetErrorString(ce));
-      return LR_ERR_CUDA;
-    }
-    cluster_mgs_kernel<<<ncl, 256, 0, s>>>(Z, n, clus);
-  }
-  delete[] wh;
-  delete[] ch;
-  if (ncl) LR_CHECK_LAUNCH();
-  if (clusters_host) *clusters_host = ncl;
   if (timing) cudaEventRecord(ev[4], s);
   // 5. back-transform and eigenvalues out
   // blocked (compact WY) back-transform: Z <- B_0 (B_1 (... (B_last Z))),
@@ -969,6 +982,8 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d_out, double* V
   if (timing) {
     cudaEventRecord(ev[5], s);
     cudaEventSynchronize(ev[5]);
+    int ncl = 0;
+    cudaMemcpy(&ncl, ncl_dev, sizeof(int), cudaMemcpyDeviceToHost);
     float t[5];
     for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
     fprintf(stderr, "syevd n=%d G=%d: tridiag %.3f bisect %.3f inviter %.3f clusters(%d) %.3f backtr %.3f ms\n", n,

@@ -392,9 +392,9 @@ def sym_eig_dev(B, symmetrize=True):
     V = device.empty(n, n)
     if EIG_METHOD == "syevd":
         work = device.arena().get("syevd_work", int(_native.load().lr_syevd_workspace_doubles(n)))
-        ncl = ctypes.c_int(0)
+        # clusters_host = NULL: the cluster count stays on the device (no stream sync)
         _native.call("lr_syevd_f64", n, device.ptr(A), device.ld(A), device.ptr(d), device.ptr(V), device.ld(V),
-                     device.ptr(work), ctypes.byref(ncl), _st(), meta={"n": n})
+                     device.ptr(work), None, _st(), meta={"n": n})
         return V, d
     work = device.arena().get("syevj_work", int(_native.load().lr_syevj_workspace_doubles(n)))
     sweeps = ctypes.c_int(0)

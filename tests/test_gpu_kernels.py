@@ -246,6 +246,41 @@ def test_sym_eig_matches_numpy(n):
     assert rel(B @ V, V * d) <= 1e-12
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,groups", [(40, [1, 1, 1, 2, 3, 3]), (300, None)])
+def test_sym_eig_clusters(n, groups):
+    """Repeated eigenvalues: the device cluster finder + MGS keep V orthonormal
+    (n = 300: 150 equal pairs, more clusters than the MGS grid)."""
+    import ctypes
+
+    import torch
+
+    from paper_1810_06860_b200 import _native, device
+    from paper_1810_06860_b200.linalg import sym_eig
+
+    rng = np.random.default_rng(n)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    if groups is None:
+        d0 = np.repeat(np.arange(1.0, n // 2 + 1), 2)
+    else:
+        d0 = np.concatenate([groups, 10.0 + np.arange(n - len(groups))])
+    B = (Q * d0) @ Q.T
+    B = (B + B.T) / 2
+    V, d = sym_eig(B)
+    assert np.max(np.abs(d - np.sort(d0))) <= 1e-12 * d0.max() * 10
+    assert rel(V.T @ V, np.eye(n)) <= 1e-12 * max(1, n / 10)
+    assert rel(B @ V, V * d) <= 1e-12
+    # raw ABI with the optional host count
+    A = device.to_device(B)
+    dd, VV = device.vector(n), device.empty(n, n)
+    work = torch.empty(int(_native.load().lr_syevd_workspace_doubles(n)), dtype=torch.float64, device="cuda")
+    ncl = ctypes.c_int(-1)
+    _native.call("lr_syevd_f64", n, device.ptr(A), device.ld(A), device.ptr(dd), device.ptr(VV), device.ld(VV),
+                 device.ptr(work), ctypes.byref(ncl), device.stream())
+    expect = n // 2 if groups is None else 2
+    assert ncl.value == expect
+
+
 def test_eig_svd_golden_and_acceptance_01(golden):
     from paper_1810_06860_b200.linalg import eig_svd
 
