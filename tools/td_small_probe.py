@@ -2,7 +2,7 @@
 import sys, time, numpy as np, torch
 sys.path.insert(0, '.')
 from paper_1810_06860_b200 import device, linalg
-for n in (16, 32, 64, 84, 96, 110, 128):
+for n in ([int(a) for a in sys.argv[1:]] or (16, 32, 64, 84, 96, 110, 128)):
     X = np.random.default_rng(n).standard_normal((3 * n, n)); B = X.T @ X; G = device.to_device(B)
     for _ in range(2): linalg.sym_eig_dev(G)
     torch.cuda.synchronize(); ts = []
