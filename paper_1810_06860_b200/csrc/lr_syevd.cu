@@ -814,7 +814,9 @@ static TdPlan td_plan(int n) {
   // CTAs: every CTA re-reads the broadcast vectors each column, so fewer,
   // fatter CTAs cut L2 contention (tunable: LR_TD_ROWS = rows per CTA)
   static const int rows_pref = getenv("LR_TD_ROWS") ? atoi(getenv("LR_TD_ROWS")) : 8;  // swept: tools/td_rows_probe.py
-  int G = n <= 96 ? 1 : (n + rows_pref - 1) / rows_pref;
+  // one CTA (no grid barrier) up to single_max (tunable: LR_TD_SINGLE_MAX)
+  static const int single_max = getenv("LR_TD_SINGLE_MAX") ? atoi(getenv("LR_TD_SINGLE_MAX")) : 96;
+  int G = n <= single_max ? 1 : (n + rows_pref - 1) / rows_pref;
   if (G > sms) G = sms;
   int rows_per = (n + G - 1) / G;
   G = (n + rows_per - 1) / rows_per;
