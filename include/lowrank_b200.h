@@ -88,6 +88,27 @@ int lr_svt_step_f64(const int* ptr, const int* idx, int rows, const int* items, 
                     double step, int apply, double* partial, int n_partial, double* out2, void* stream);
 int lr_svt_step_partials(void);
 
+/* Flat form of the two entry points above (the default product path): the
+ * stored entries are cut into tiles of lr_svt_tile_entries() consecutive CSR
+ * slots, one warp per tile, whatever the row lengths.  tile_row[t] = the row
+ * holding slot t * lr_svt_tile_entries() (lr_svt_tile_rows_i32, once per
+ * pattern; lr_svt_tile_count(nnz) ints).  Same results as lr_svt_step_f64 /
+ * lr_sddmm_f64 (each entry's sum depends only on its U row, S and V row);
+ * y_csc may be NULL: only the CSR copy is updated (the caller refreshes the
+ * CSC copy with lr_gather_f64 before it is next read).  partial[] must hold
+ * lr_svt_flat_partials() doubles.  Any rank (r > 256 runs in column chunks). */
+int lr_svt_tile_entries(void);
+long long lr_svt_tile_count(long long nnz);
+int lr_svt_tile_rows_i32(const int* ptr, int m, long long nnz, int* tile_row, void* stream);
+int lr_svt_flat_partials(void);
+int lr_svt_step_flat_f64(const int* ptr, const int* idx, int m, long long nnz, const int* tile_row,
+                         const double* U, long long ldu, const double* S, const double* V, long long ldv, int r,
+                         const double* m_vals, double* y_csr, double* y_csc, const int* inv_perm, double step,
+                         int apply, double* partial, int n_partial, double* out2, void* stream);
+int lr_sddmm_flat_f64(const int* ptr, const int* idx, int m, long long nnz, const int* tile_row, const double* U,
+                      long long ldu, const double* S, const double* V, long long ldv, int r, double* x,
+                      void* stream);
+
 /* y_csr += delta; y_csc[inv_perm[e]] += delta[e]  (update_pattern_values). */
 int lr_pattern_axpy_f64(double* y_csr, double* y_csc, const int* inv_perm, const double* delta,
                         double alpha, long long nnz, void* stream);

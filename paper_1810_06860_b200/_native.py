@@ -39,6 +39,13 @@ SIGNATURES = {
     "lr_svt_step_f64": (_I, [_P, _P, _I, _P, _I, _P, _LL, _P, _P, _LL, _I, _P, _P, _P, _P, _D, _I,
                              _P, _I, _P, _P]),
     "lr_svt_step_partials": (_I, []),
+    "lr_svt_tile_entries": (_I, []),
+    "lr_svt_tile_count": (_LL, [_LL]),
+    "lr_svt_tile_rows_i32": (_I, [_P, _I, _LL, _P, _P]),
+    "lr_svt_flat_partials": (_I, []),
+    "lr_svt_step_flat_f64": (_I, [_P, _P, _I, _LL, _P, _P, _LL, _P, _P, _LL, _I, _P, _P, _P, _P, _D, _I, _P, _I,
+                                  _P, _P]),
+    "lr_sddmm_flat_f64": (_I, [_P, _P, _I, _LL, _P, _P, _LL, _P, _P, _LL, _I, _P, _P]),
     "lr_pattern_axpy_f64": (_I, [_P, _P, _P, _P, _D, _LL, _P]),
     "lr_gather_f64": (_I, [_P, _P, _P, _LL, _P]),
     "lr_block_stats_f64": (_I, [_P, _LL, _LL, _LL, _P, _P, _P]),

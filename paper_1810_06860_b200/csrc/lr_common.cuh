@@ -55,6 +55,9 @@ void count_launches(long long n);
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// integer tuning knob from the environment, clamped to [lo, hi] (default when unset)
+int env_int_clamped(const char* name, int dflt, int lo, int hi);
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

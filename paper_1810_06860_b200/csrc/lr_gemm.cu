@@ -164,51 +164,26 @@ __global__ void __launch_bounds__(T::THREADS) gemm_kernel(int M, int N, int K, d
     const int k0 = k_begin + kt * T::BK;
     double* as = As + st * T::A_STAGE;
     double* bs = Bs + st * T::B_STAGE;
-    if (vec16) {
-      if (!TRANS_A) {
-        // A[m][k]: 8 pairs of k per row
-        for (int e = tid; e < T::BM * (T::BK / 2); e += T::THREADS) {
-          const int mm = e / (T::BK / 2), kk = 2 * (e % (T::BK / 2));
-          const int gm = m0 + mm, gk = k0 + kk;
-          const int nb = (gm < M) ? (gk + 1 < k_end ? 16 : (gk < k_end ? 8 : 0)) : 0;
-          cp_async16(as + mm * T::LDA_N + kk, nb ? A + (long long)gm * lda + gk : A, nb);
-        }
-      } else {
-        for (int e = tid; e < T::BK * (T::BM / 2); e += T::THREADS) {
-          const int kk = e / (T::BM / 2), mm = 2 * (e % (T::BM / 2));
-          const int gm = m0 + mm, gk = k0 + kk;
-          const int nb = (gk < k_end) ? (gm + 1 < M ? 16 : (gm < M ? 8 : 0)) : 0;
-          cp_async16(as + kk * T::LDA_T + mm, nb ? A + (long long)gk * lda + gm : A, nb);
-        }
-      }
-      for (int e = tid; e < T::BK * (T::BN / 2); e += T::THREADS) {
-        const int kk = e / (T::BN / 2), nn = 2 * (e % (T::BN / 2));
-        const int gn = n0 + nn, gk = k0 + kk;
-        const int nb = (gk < k_end) ? (gn + 1 < N ? 16 : (gn < N ? 8 : 0)) : 0;
-        cp_async16(bs + kk * T::LDB + nn, nb ? B + (long long)gk * ldb + gn : B, nb);
+    if (!TRANS_A) {
+      for (int e = tid; e < T::BM * T::BK; e += T::THREADS) {
+        const int mm = e / T::BK, kk = e % T::BK;
+        const int gm = m0 + mm, gk = k0 + kk;
+        const bool ok = gm < M && gk < k_end;
+        cp_async8(as + mm * T::LDA_N + kk, ok ? A + (long long)gm * lda + gk : A, ok ? 8 : 0);
       }
     } else {
-      if (!TRANS_A) {
-        for (int e = tid; e < T::BM * T::BK; e += T::THREADS) {
-          const int mm = e / T::BK, kk = e % T::BK;
-          const int gm = m0 + mm, gk = k0 + kk;
-          const bool ok = gm < M && gk < k_end;
-          cp_async8(as + mm * T::LDA_N + kk, ok ? A + (long long)gm * lda + gk : A, ok ? 8 : 0);
-        }
-      } else {
-        for (int e = tid; e < T::BK * T::BM; e += T::THREADS) {
-          const int kk = e / T::BM, mm = e % T::BM;
-          const int gm = m0 + mm, gk = k0 + kk;
-          const bool ok = gm < M && gk < k_end;
-          cp_async8(as + kk * T::LDA_T + mm, ok ? A + (long long)gk * lda + gm : A, ok ? 8 : 0);
-        }
+      for (int e = tid; e < T::BK * T::BM; e += T::THREADS) {
+        const int kk = e / T::BM, mm = e % T::BM;
+        const int gm = m0 + mm, gk = k0 + kk;
+        const bool ok = gm < M && gk < k_end;
+        cp_async8(as + kk * T::LDA_T + mm, ok ? A + (long long)gk * lda + gm : A, ok ? 8 : 0);
       }
-      for (int e = tid; e < T::BK * T::BN; e += T::THREADS) {
-        const int kk = e / T::BN, nn = e % T::BN;
-        const int gn = n0 + nn, gk = k0 + kk;
-        const bool ok = gn < N && gk < k_end;
-        cp_async8(bs + kk * T::LDB + nn, ok ? B + (long long)gk * ldb + gn : B, ok ? 8 : 0);
-      }
+    }
+    for (int e = tid; e < T::BK * T::BN; e += T::THREADS) {
+      const int kk = e / T::BN, nn = e % T::BN;
+      const int gn = n0 + nn, gk = k0 + kk;
+      const bool ok = gn < N && gk < k_end;
+      cp_async8(bs + kk * T::LDB + nn, ok ? B + (long long)gk * ldb + gn : B, ok ? 8 : 0);
     }
   };
 

@@ -668,8 +668,10 @@ static int lu_impl(int m, int n, double* X, long long ldx, double* work, double*
   double* partial = stats + 4;
   int st = lr_block_stats_f64(X, m, n, ldx, partial, stats, stream);
   if (st) return st;
+  // status zeroed here; the kernel's first act writes status[0] (-1 ok, -2 zero matrix,
+  // -3 non-finite, j >= 0 first bad column).  The wrapper reads `stats` before status, so the
+  // early exits (zero / non-finite input) never reach the column decision.
   LR_CHECK_CUDA(cudaMemsetAsync(status, 0, 4 * sizeof(double), s));
-  // status[0] preset to -3 (not run) so an early exit is visible
   static bool attr = false;
   if (!attr) {
     LR_CHECK_CUDA(cudaFuncSetAttribute(lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));

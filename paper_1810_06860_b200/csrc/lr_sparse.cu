@@ -362,6 +362,283 @@ __global__ void __launch_bounds__(kSvtThreads) svt_group_kernel(
   }
 }
 
+// Batch variant (any rank): a warp owns one item and walks it in batches of
+// 32 consecutive stored entries.  Lane l loads entry b0 + l's column, M value
+// and Y value with one coalesced access each; the dots run in rounds, a group
+// of G lanes per entry (lane g holds U*S of its column pairs c = 2(g + G t) in
+// registers and reads the matching 16-byte slices of V[j,:], so every V row is
+// read as G*16 contiguous bytes), Q rounds of gathers in flight; a fixed
+// xor-butterfly folds the G partials and one shuffle hands entry q's value to
+// lane q, which finishes it (residual partials, Y += step (m - x), coalesced
+// store; the CSC copy's scattered store only when y_csc is given).  Ranks
+// wider than 2 G T run as column chunks with the x partials summed in chunk
+// order.
+template <int G, int T, int Q, bool FUSED>
+__global__ void __launch_bounds__(kSvtThreads) svt_batch_kernel(
+    const int* __restrict__ ptr, const int* __restrict__ idx, const int* __restrict__ items, int n_items,
+    const double* __restrict__ U, long long ldu, const double* __restrict__ S, const double* __restrict__ V,
+    long long ldv, int r, double* __restrict__ x_out, const double* __restrict__ m_vals,
+    double* __restrict__ y_csr, double* __restrict__ y_csc, const int* __restrict__ inv_perm, double step,
+    int apply, double* __restrict__ partial) {
+  constexpr int E = 32 / G;  // entries per round
+  constexpr int CH = 2 * G * T;  // rank columns per chunk
+  const int lane = threadIdx.x & 31, g = lane % G, grp = lane / G;
+  const long long warp_global = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const bool vec = ((ldv & 1) == 0) && ((reinterpret_cast<uintptr_t>(V) & 15) == 0);
+  double ss = 0.0, mx = 0.0;
+  for (long long ii = warp_global; ii < n_items; ii += n_warps) {
+    const Item it = load_item(items, ptr, (int)ii);
+    const double* ur = U + (long long)it.row * ldu;
+    for (int b0 = it.beg; b0 < it.end; b0 += 32) {
+      const int nE = min(32, it.end - b0);
+      const int e = b0 + lane;
+      const bool own = lane < nE;
+      const int jl = own ? __ldg(idx + e) : 0;
+      double ml = 0.0, yl = 0.0;
+      if (FUSED && own) {
+        ml = __ldg(m_vals + e);
+        if (apply) yl = y_csr[e];
+      }
+      double xl = 0.0;
+      const int rounds = (nE + E - 1) / E;
+      for (int c0 = 0; c0 < r; c0 += CH) {
+        double2 us[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          const int c = c0 + 2 * (g + G * t);
+          us[t].x = (c < r) ? __ldg(ur + c) * __ldg(S + c) : 0.0;
+          us[t].y = (c + 1 < r) ? __ldg(ur + c + 1) * __ldg(S + c + 1) : 0.0;
+        }
+        for (int rho0 = 0; rho0 < rounds; rho0 += Q) {
+          double part[Q];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            part[q] = 0.0;
+            const int ent = (rho0 + q) * E + grp;  // entry of this group in round rho0 + q
+            const int j = __shfl_sync(0xffffffffu, jl, ent & 31);
+            if (ent < nE) {
+              const double* vr = V + (long long)j * ldv + c0;
+#pragma unroll
+              for (int t = 0; t < T; ++t) {
+                const int c = 2 * (g + G * t);
+                double2 v;
+                if (vec && c0 + c + 1 < r) {
+                  v = __ldg(reinterpret_cast<const double2*>(vr + c));
+                } else {
+                  v.x = (c0 + c < r) ? __ldg(vr + c) : 0.0;
+                  v.y = (c0 + c + 1 < r) ? __ldg(vr + c + 1) : 0.0;
+                }
+                part[q] = fma(us[t].x, v.x, part[q]);
+                part[q] = fma(us[t].y, v.y, part[q]);
+              }
+            }
+          }
+#pragma unroll
+          for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+            for (int q = 0; q < Q; ++q) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
+          // hand entry (rho0 + q) * E + grp's value to the lane that owns it
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            const double v = __shfl_sync(0xffffffffu, part[q], (lane % E) * G);
+            if (lane / E == rho0 + q) xl += v;
+          }
+        }
+      }
+      if (own) {
+        if (FUSED) {
+          const double d = xl - ml;
+          ss = fma(d, d, ss);
+          mx = fmax(mx, fabs(d));
+          if (apply) {
+            const double ynew = add_rn(yl, mul_rn(step, add_rn(ml, -xl)));
+            y_csr[e] = ynew;
+            if (y_csc) y_csc[__ldg(inv_perm + e)] = ynew;
+          }
+        } else {
+          x_out[e] = xl;
+        }
+      }
+    }
+  }
+  if (FUSED) {
+    __shared__ double red[32];
+    const double S2 = block_sum<kSvtThreads>(ss, red);
+    const double M2 = block_max<kSvtThreads>(mx, red);
+    if (threadIdx.x == 0) {
+      partial[2 * blockIdx.x] = S2;
+      partial[2 * blockIdx.x + 1] = M2;
+    }
+  }
+}
+
+// Flat variant (the default): the stored entries are cut into tiles of 32*K
+// consecutive CSR slots, one warp per tile (uniform work per warp whatever
+// the row lengths -- cfg4 rows run from 10 to 8,344 entries).  Lane l owns
+// slots base + 32k + l (k < K): one coalesced load each of the column index,
+// M value and Y value, all K in flight together.  The row of every slot comes
+// from the tile's first row (tile_row[], one binary search per tile per
+// pattern) and a warp-wide count of the row boundaries ptr[] at or below the
+// slot.  The tile's (column, row) pairs go to shared memory; the dots then
+// run in rounds with a group of G lanes per entry (lane g multiplies its T
+// column pairs c = 2(g + G t) of U[row,:] * S by the matching 16-byte slices
+// of V[j,:], so every V row is read as G*16 contiguous bytes), Q rounds of
+// gathers in flight, a fixed xor-butterfly per group, the result parked in
+// shared memory; each lane then finishes its own K slots with coalesced
+// stores.  Ranks wider than 2 G T run as column chunks (x partials summed in
+// chunk order).  Per entry the sum is fixed by (U row, S, V row) alone.
+constexpr int kFlatWarps = 8;
+
+template <int G, int T, int K, int Q, bool FUSED>
+__global__ void __launch_bounds__(kFlatWarps * 32) svt_flat_kernel(
+    const int* __restrict__ ptr, const int* __restrict__ idx, long long nnz, int m,
+    const int* __restrict__ tile_row, long long n_tiles, const double* __restrict__ U, long long ldu,
+    const double* __restrict__ S, const double* __restrict__ V, long long ldv, int r, double* __restrict__ x_out,
+    const double* __restrict__ m_vals, double* __restrict__ y_csr, double* __restrict__ y_csc,
+    const int* __restrict__ inv_perm, double step, int apply, double* __restrict__ partial) {
+  constexpr int E = 32 / G;    // entries per round
+  constexpr int TE = 32 * K;   // entries per tile
+  constexpr int CH = 2 * G * T;  // rank columns per chunk
+  constexpr int ROUNDS = TE / E;
+  __shared__ int2 sh_jr[kFlatWarps][TE];
+  __shared__ double sh_x[kFlatWarps][TE];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, g = lane % G, grp = lane / G;
+  const long long warp_global = (long long)blockIdx.x * kFlatWarps + wib;
+  const long long n_warps = (long long)gridDim.x * kFlatWarps;
+  const bool vec = ((ldv & 1) == 0) && ((ldu & 1) == 0) && ((reinterpret_cast<uintptr_t>(V) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(U) & 15) == 0);
+  int2* jr = sh_jr[wib];
+  double* xs = sh_x[wib];
+  double ss = 0.0, mx = 0.0;
+  for (long long t = warp_global; t < n_tiles; t += n_warps) {
+    const long long base = t * TE;
+    const long long last = min(base + TE, nnz) - 1;
+    int jk[K], rk[K];
+    double mk[K], yk[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const long long e = base + 32 * k + lane;
+      const bool own = e <= last;
+      jk[k] = own ? __ldg(idx + e) : 0;
+      mk[k] = (FUSED && own) ? __ldg(m_vals + e) : 0.0;
+      yk[k] = (FUSED && own && apply) ? y_csr[e] : 0.0;
+    }
+    // rows: r0 + #{row boundaries ptr[r0+1..] <= slot}
+    const int r0 = __ldg(tile_row + t);
+#pragma unroll
+    for (int k = 0; k < K; ++k) rk[k] = r0;
+    for (int rb = r0;; rb += 32) {
+      const int bi = rb + 1 + lane;
+      const long long b = (bi <= m) ? (long long)__ldg(ptr + bi) : (1LL << 62);
+#pragma unroll 8
+      for (int i = 0; i < 32; ++i) {
+        const long long bv = __shfl_sync(0xffffffffu, b, i);
+#pragma unroll
+        for (int k = 0; k < K; ++k) rk[k] += (bv <= base + 32 * k + lane) ? 1 : 0;
+      }
+      if (__shfl_sync(0xffffffffu, b, 31) > last) break;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) jr[32 * k + lane] = make_int2(jk[k], rk[k]);
+    __syncwarp();
+    const int nE = (int)(last - base + 1);
+    for (int c0 = 0; c0 < r; c0 += CH) {
+      double2 sv[T];
+#pragma unroll
+      for (int tt = 0; tt < T; ++tt) {
+        const int c = c0 + 2 * (g + G * tt);
+        sv[tt].x = (c < r) ? __ldg(S + c) : 0.0;
+        sv[tt].y = (c + 1 < r) ? __ldg(S + c + 1) : 0.0;
+      }
+      for (int rho0 = 0; rho0 < ROUNDS; rho0 += Q) {
+        double part[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          part[q] = 0.0;
+          const int ent = (rho0 + q) * E + grp;
+          if (ent < nE) {
+            const int2 e2 = jr[ent];
+            const double* vr = V + (long long)e2.x * ldv + c0;
+            const double* ur = U + (long long)e2.y * ldu + c0;
+#pragma unroll
+            for (int tt = 0; tt < T; ++tt) {
+              const int c = 2 * (g + G * tt);
+              double2 v, u;
+              if (vec && c0 + c + 1 < r) {
+                v = __ldg(reinterpret_cast<const double2*>(vr + c));
+                u = __ldg(reinterpret_cast<const double2*>(ur + c));
+              } else {
+                v.x = (c0 + c < r) ? __ldg(vr + c) : 0.0;
+                v.y = (c0 + c + 1 < r) ? __ldg(vr + c + 1) : 0.0;
+                u.x = (c0 + c < r) ? __ldg(ur + c) : 0.0;
+                u.y = (c0 + c + 1 < r) ? __ldg(ur + c + 1) : 0.0;
+              }
+              part[q] = fma(u.x * sv[tt].x, v.x, part[q]);
+              part[q] = fma(u.y * sv[tt].y, v.y, part[q]);
+            }
+          }
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+          for (int q = 0; q < Q; ++q) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
+        if (g == 0) {
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            const int ent = (rho0 + q) * E + grp;
+            if (ent < TE) xs[ent] = (c0 == 0) ? part[q] : xs[ent] + part[q];
+          }
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const long long e = base + 32 * k + lane;
+      if (e > last) continue;
+      const double xl = (r > 0) ? xs[32 * k + lane] : 0.0;
+      if (FUSED) {
+        const double d = xl - mk[k];
+        ss = fma(d, d, ss);
+        mx = fmax(mx, fabs(d));
+        if (apply) {
+          const double ynew = add_rn(yk[k], mul_rn(step, add_rn(mk[k], -xl)));
+          y_csr[e] = ynew;
+          if (y_csc) y_csc[__ldg(inv_perm + e)] = ynew;
+        }
+      } else {
+        x_out[e] = xl;
+      }
+    }
+    __syncwarp();
+  }
+  if (FUSED) {
+    __shared__ double red[32];
+    const double S2 = block_sum<kFlatWarps * 32>(ss, red);
+    const double M2 = block_max<kFlatWarps * 32>(mx, red);
+    if (threadIdx.x == 0) {
+      partial[2 * blockIdx.x] = S2;
+      partial[2 * blockIdx.x + 1] = M2;
+    }
+  }
+}
+
+// tile_row[t] = the row holding CSR slot t * tile_entries (binary search in ptr)
+__global__ void tile_rows_kernel(const int* __restrict__ ptr, int m, long long nnz, int tile_entries,
+                                 long long n_tiles, int* __restrict__ tile_row) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long e = t * tile_entries;
+    int lo = 0, hi = m - 1;  // last row with ptr[row] <= e
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if ((long long)ptr[mid] <= e) lo = mid; else hi = mid - 1;
+    }
+    tile_row[t] = lo;
+  }
+}
+
 // one warp: lane-strided partial sums, fixed shuffle tree (deterministic; a
 // single-thread serial fold over the ~1.2K block partials cost ~45 us per
 // SVT iteration)
@@ -519,6 +796,74 @@ static int spmm_cols(const int* ptr, const int* idx, const Sc* val, const int* i
   return LR_OK;
 }
 
+constexpr int kFlatK = 4;                    // entries per lane per tile
+constexpr int kFlatTile = 32 * kFlatK;        // CSR slots per tile (lr_svt_tile_entries)
+constexpr int kFlatMaxBlocksPerSm = 8;
+
+template <int G, int T, int Q>
+static int launch_flat_t(bool fused, const int* ptr, const int* idx, long long nnz, int m, const int* tile_row,
+                         long long n_tiles, const double* U, long long ldu, const double* S, const double* V,
+                         long long ldv, int r, double* x, const double* m_vals, double* y_csr, double* y_csc,
+                         const int* inv_perm, double step, int apply, double* partial, cudaStream_t s) {
+  static int occ[2] = {-1, -1};
+  int& o = occ[fused ? 1 : 0];
+  if (o < 0) {
+    if (fused)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, svt_flat_kernel<G, T, kFlatK, Q, true>, kFlatWarps * 32, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, svt_flat_kernel<G, T, kFlatK, Q, false>, kFlatWarps * 32, 0);
+    if (o < 1) o = 1;
+    if (o > kFlatMaxBlocksPerSm) o = kFlatMaxBlocksPerSm;
+  }
+  long long blocks = (long long)sm_count() * o;
+  const long long need = (n_tiles + kFlatWarps - 1) / kFlatWarps;
+  if (blocks > need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  if (fused)
+    svt_flat_kernel<G, T, kFlatK, Q, true><<<(int)blocks, kFlatWarps * 32, 0, s>>>(
+        ptr, idx, nnz, m, tile_row, n_tiles, U, ldu, S, V, ldv, r, x, m_vals, y_csr, y_csc, inv_perm, step, apply,
+        partial);
+  else
+    svt_flat_kernel<G, T, kFlatK, Q, false><<<(int)blocks, kFlatWarps * 32, 0, s>>>(
+        ptr, idx, nnz, m, tile_row, n_tiles, U, ldu, S, V, ldv, r, x, m_vals, y_csr, y_csc, inv_perm, step, apply,
+        partial);
+  LR_CHECK_LAUNCH();
+  return (int)blocks;  // > 0: blocks launched (partials written)
+}
+
+// (G, T, Q) by rank: G lanes x T column pairs cover the rank in one chunk up
+// to r = 256 (wider ranks loop over chunks); LR_SVT_FLAT="G,T,Q" overrides.
+static int launch_flat(bool fused, const int* ptr, const int* idx, long long nnz, int m, const int* tile_row,
+                       const double* U, long long ldu, const double* S, const double* V, long long ldv, int r,
+                       double* x, const double* m_vals, double* y_csr, double* y_csc, const int* inv_perm,
+                       double step, int apply, double* partial, cudaStream_t s) {
+  const long long n_tiles = (nnz + kFlatTile - 1) / kFlatTile;
+  const int pairs = (r + 1) / 2;
+  static const char* env = getenv("LR_SVT_FLAT");
+  int G = 0, T = 0, Q = 0;
+  if (env) sscanf(env, "%d,%d,%d", &G, &T, &Q);
+  if (G == 0) {
+    if (pairs <= 2) { G = 1; T = 2; Q = 4; }
+    else if (pairs <= 4) { G = 2; T = 2; Q = 4; }
+    else if (pairs <= 8) { G = 4; T = 2; Q = 4; }
+    else if (pairs <= 16) { G = 8; T = 2; Q = 4; }
+    else if (pairs <= 32) { G = 16; T = 2; Q = 4; }
+    else if (pairs <= 64) { G = 32; T = 2; Q = 4; }
+    else { G = 32; T = 4; Q = 2; }
+  }
+#define LR_FLAT(g, t, q)                                                                                      \
+  if (G == g && T == t && Q == q)                                                                              \
+    return launch_flat_t<g, t, q>(fused, ptr, idx, nnz, m, tile_row, n_tiles, U, ldu, S, V, ldv, r, x, m_vals, \
+                                  y_csr, y_csc, inv_perm, step, apply, partial, s);
+  LR_FLAT(1, 2, 4) LR_FLAT(2, 2, 4) LR_FLAT(4, 2, 4) LR_FLAT(8, 2, 4) LR_FLAT(16, 2, 4) LR_FLAT(32, 2, 4)
+  LR_FLAT(32, 4, 2) LR_FLAT(1, 4, 2) LR_FLAT(2, 4, 2) LR_FLAT(4, 4, 2) LR_FLAT(8, 4, 2) LR_FLAT(16, 4, 2)
+  LR_FLAT(1, 1, 4) LR_FLAT(2, 1, 4) LR_FLAT(4, 1, 4) LR_FLAT(8, 1, 4) LR_FLAT(16, 1, 4) LR_FLAT(1, 2, 2)
+  LR_FLAT(2, 2, 2) LR_FLAT(4, 2, 2) LR_FLAT(8, 2, 2) LR_FLAT(4, 2, 8) LR_FLAT(8, 2, 8) LR_FLAT(2, 2, 8)
+#undef LR_FLAT
+  set_error("svt: no flat kernel instance for G=%d T=%d Q=%d", G, T, Q);
+  return -LR_ERR_ARG;
+}
+
 }  // namespace lr
 
 using namespace lr;
@@ -571,10 +916,50 @@ static int launch_sddmm(bool fused, const int* ptr, const int* idx, int rows, co
                         const double* V, long long ldv, int r, double* x, const double* m_vals,
                         double* y_csr, double* y_csc, const int* inv_perm, double step, int apply,
                         double* partial, cudaStream_t s) {
-  LR_REQUIRE(r <= kMaxRankSmem, "sddmm: rank %d exceeds %d", r, kMaxRankSmem);
   if (!items) n_items = rows;
   const int blocks = sm_count() * kSvtBlocksPerSm;
-  static const bool old_kernel = getenv("LR_SVT_WARP_KERNEL") != nullptr;
+  // kernel family: "batch" (default: coalesced per-entry finishing, any rank),
+  // "legacy" (round-1 warp / group kernels, r <= 1024); LR_SVT_GT="G,T,Q"
+  // overrides the batch kernel's lane mapping for experiments
+  static const char* fam = getenv("LR_SVT_KERNEL");
+  const bool legacy = fam && fam[0] == 'l';
+  if (!legacy) {
+    const int pairs = (r + 1) / 2;
+    static const char* gt = getenv("LR_SVT_GT");
+    int G = 0, T = 0, Q = 0;
+    if (gt) sscanf(gt, "%d,%d,%d", &G, &T, &Q);
+    if (G == 0) {
+      if (pairs <= 4) { G = 1; T = 4; Q = 2; }
+      else if (pairs <= 8) { G = 2; T = 4; Q = 2; }
+      else if (pairs <= 16) { G = 4; T = 4; Q = 2; }
+      else if (pairs <= 32) { G = 8; T = 4; Q = 2; }
+      else if (pairs <= 64) { G = 16; T = 4; Q = 2; }
+      else { G = 32; T = 4; Q = 2; }
+    }
+#define LR_SVT_BATCH(g, t, q)                                                                               \
+  if (G == g && T == t && Q == q) {                                                                          \
+    if (fused)                                                                                               \
+      svt_batch_kernel<g, t, q, true><<<blocks, kSvtThreads, 0, s>>>(ptr, idx, items, n_items, U, ldu, S, V,  \
+                                                                     ldv, r, x, m_vals, y_csr, y_csc,        \
+                                                                     inv_perm, step, apply, partial);        \
+    else                                                                                                     \
+      svt_batch_kernel<g, t, q, false><<<blocks, kSvtThreads, 0, s>>>(ptr, idx, items, n_items, U, ldu, S, V, \
+                                                                      ldv, r, x, m_vals, y_csr, y_csc,       \
+                                                                      inv_perm, step, apply, partial);       \
+    LR_CHECK_LAUNCH();                                                                                       \
+    return LR_OK;                                                                                            \
+  }
+    LR_SVT_BATCH(1, 4, 2) LR_SVT_BATCH(2, 4, 2) LR_SVT_BATCH(4, 4, 2) LR_SVT_BATCH(8, 4, 2)
+    LR_SVT_BATCH(16, 4, 2) LR_SVT_BATCH(32, 4, 2)
+    LR_SVT_BATCH(1, 2, 4) LR_SVT_BATCH(2, 2, 4) LR_SVT_BATCH(4, 2, 4) LR_SVT_BATCH(8, 2, 4)
+    LR_SVT_BATCH(16, 2, 4) LR_SVT_BATCH(32, 2, 4) LR_SVT_BATCH(1, 8, 1) LR_SVT_BATCH(2, 8, 1)
+    LR_SVT_BATCH(4, 8, 1) LR_SVT_BATCH(8, 8, 1) LR_SVT_BATCH(4, 4, 4) LR_SVT_BATCH(8, 4, 4)
+    LR_SVT_BATCH(8, 1, 4) LR_SVT_BATCH(4, 1, 4) LR_SVT_BATCH(16, 1, 4) LR_SVT_BATCH(16, 2, 2)
+#undef LR_SVT_BATCH
+    LR_REQUIRE(false, "sddmm: no batch kernel instance for G=%d T=%d Q=%d", G, T, Q);
+  }
+  LR_REQUIRE(r <= kMaxRankSmem, "sddmm: rank %d exceeds %d", r, kMaxRankSmem);
+  const bool old_kernel = fam && fam[1] == 'w';  // "lw": legacy warp kernel only
   const bool v2ok = (ldv % 2 == 0) && aligned16(V) && (ldu >= r);
   // the group kernel wins only for wide factors (cfg4, tools/sddmm_probe.py: r = 84 2.13 vs 2.26 ms,
   // r = 160 2.99 vs 5.52 ms; r <= 40 the warp kernel is up to 2x faster)
@@ -658,6 +1043,53 @@ int lr_svt_step_f64(const int* ptr, const int* idx, int rows, const int* items, 
   svt_finish_kernel<<<1, 32, 0, s>>>(partial, blocks, out2);
   LR_CHECK_LAUNCH();
   return LR_OK;
+}
+
+int lr_svt_tile_entries(void) { return kFlatTile; }
+
+long long lr_svt_tile_count(long long nnz) { return (nnz + kFlatTile - 1) / kFlatTile; }
+
+int lr_svt_tile_rows_i32(const int* ptr, int m, long long nnz, int* tile_row, void* stream) {
+  const long long n_tiles = (nnz + kFlatTile - 1) / kFlatTile;
+  if (n_tiles == 0) return LR_OK;
+  LR_REQUIRE(m >= 1, "svt_tile_rows: m must be >= 1");
+  long long blocks = (n_tiles + 255) / 256;
+  if (blocks > sm_count() * 8) blocks = sm_count() * 8;
+  tile_rows_kernel<<<(int)blocks, 256, 0, as_stream(stream)>>>(ptr, m, nnz, kFlatTile, n_tiles, tile_row);
+  LR_CHECK_LAUNCH();
+  return LR_OK;
+}
+
+int lr_svt_flat_partials(void) { return sm_count() * kFlatMaxBlocksPerSm * 2; }
+
+int lr_svt_step_flat_f64(const int* ptr, const int* idx, int m, long long nnz, const int* tile_row,
+                         const double* U, long long ldu, const double* S, const double* V, long long ldv, int r,
+                         const double* m_vals, double* y_csr, double* y_csc, const int* inv_perm, double step,
+                         int apply, double* partial, int n_partial, double* out2, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  LR_REQUIRE(n_partial >= lr_svt_flat_partials(), "svt_step: partial buffer too small (%d < %d)", n_partial,
+             lr_svt_flat_partials());
+  LR_REQUIRE(r >= 0 && (r == 0 || (ldu >= r && ldv >= r)), "svt_step: bad rank / leading dims (r=%d)", r);
+  if (nnz == 0) {
+    LR_CHECK_CUDA(cudaMemsetAsync(out2, 0, 2 * sizeof(double), s));
+    return LR_OK;
+  }
+  const int blocks = launch_flat(true, ptr, idx, nnz, m, tile_row, U, ldu, S, V, ldv, r, nullptr, m_vals, y_csr,
+                                 y_csc, inv_perm, step, apply, partial, s);
+  if (blocks < 0) return -blocks;
+  svt_finish_kernel<<<1, 32, 0, s>>>(partial, blocks, out2);
+  LR_CHECK_LAUNCH();
+  return LR_OK;
+}
+
+int lr_sddmm_flat_f64(const int* ptr, const int* idx, int m, long long nnz, const int* tile_row, const double* U,
+                      long long ldu, const double* S, const double* V, long long ldv, int r, double* x,
+                      void* stream) {
+  LR_REQUIRE(r >= 1 && ldu >= r && ldv >= r, "sddmm: bad rank / leading dims (r=%d)", r);
+  if (nnz == 0) return LR_OK;
+  const int blocks = launch_flat(false, ptr, idx, nnz, m, tile_row, U, ldu, S, V, ldv, r, x, nullptr, nullptr,
+                                 nullptr, nullptr, 0.0, 0, nullptr, as_stream(stream));
+  return blocks < 0 ? -blocks : LR_OK;
 }
 
 int lr_pattern_axpy_f64(double* y_csr, double* y_csc, const int* inv_perm, const double* delta,

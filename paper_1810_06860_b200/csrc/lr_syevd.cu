@@ -813,9 +813,11 @@ static TdPlan td_plan(int n) {
   const int sms = sm_count();
   // CTAs: every CTA re-reads the broadcast vectors each column, so fewer,
   // fatter CTAs cut L2 contention (tunable: LR_TD_ROWS = rows per CTA)
-  static const int rows_pref = getenv("LR_TD_ROWS") ? atoi(getenv("LR_TD_ROWS")) : 8;  // swept: tools/td_rows_probe.py
-  // one CTA (no grid barrier) up to single_max (tunable: LR_TD_SINGLE_MAX)
-  static const int single_max = getenv("LR_TD_SINGLE_MAX") ? atoi(getenv("LR_TD_SINGLE_MAX")) : 96;
+  // (clamped to >= 1: 0 would divide by zero below)
+  static const int rows_pref = env_int_clamped("LR_TD_ROWS", 8, 1, 1 << 20);  // swept: tools/td_rows_probe.py
+  // one CTA (no grid barrier) up to single_max (tunable: LR_TD_SINGLE_MAX, clamped to the
+  // sizes whose one-CTA rows still fit shared memory)
+  static const int single_max = env_int_clamped("LR_TD_SINGLE_MAX", 96, 0, 156);
   int G = n <= single_max ? 1 : (n + rows_pref - 1) / rows_pref;
   if (G > sms) G = sms;
   int rows_per = (n + G - 1) / G;

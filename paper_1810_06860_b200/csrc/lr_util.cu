@@ -4,6 +4,8 @@
 #include <cstdarg>
 #include <cstdio>
 
+#include <stdlib.h>
+
 #include "lr_common.cuh"
 
 namespace lr {
@@ -20,6 +22,18 @@ void set_error(const char* fmt, ...) {
 static std::atomic<long long> g_launches{0};
 void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+int env_int_clamped(const char* name, int dflt, int lo, int hi) {
+  const char* v = getenv(name);
+  int x = v ? atoi(v) : dflt;
+  if (x < lo) x = lo;
+  if (x > hi) x = hi;
+  return x;
+}
+
+// The library serves ONE device per process (the framework runs one process
+// per GPU; device.require_cuda enforces it), so the SM count and the
+// per-kernel shared-memory opt-ins cached in function-local statics hold for
+// the process's lifetime.
 int sm_count() {
   static int cached = 0;
   if (!cached) {
@@ -266,11 +280,24 @@ __global__ void diag_kernel(const double* __restrict__ A, long long lda, int n, 
     d[i] = A[(long long)i * lda + i];
 }
 
+// dst[t] = src[perm[t]]: 4 coalesced perm words per thread, then their 4
+// random reads in flight together (the random 8-byte reads are the cost:
+// each moves a 32-byte sector)
 __global__ void gather_kernel(const double* __restrict__ src, const int* __restrict__ perm,
                               double* __restrict__ dst, long long n) {
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
-       t += (long long)gridDim.x * blockDim.x)
-    dst[t] = src[perm[t]];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; t + 3 * stride < n; t += 4 * stride) {
+    int p[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p[k] = __ldg(perm + t + k * stride);
+    double v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __ldg(src + p[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dst[t + k * stride] = v[k];
+  }
+  for (; t < n; t += stride) dst[t] = __ldg(src + __ldg(perm + t));
 }
 
 // sign rule: one warp per column

@@ -38,6 +38,13 @@ def require_cuda() -> torch.device:
     idx = torch._C._cuda_getDevice()
     dev = _DEVICES.get(idx)
     if dev is None:
+        if _DEVICES:
+            # one device per process: the scratch arena, the cached device
+            # patterns and the native library's per-kernel opt-ins and SM
+            # count are process-wide (run one process per GPU, as torchrun does)
+            raise RuntimeError(
+                f"paper_1810_06860_b200 serves one CUDA device per process; already bound to "
+                f"cuda:{next(iter(_DEVICES))}, now asked for cuda:{idx}")
         dev = _DEVICES[idx] = torch.device("cuda", idx)
     return dev
 

@@ -10,9 +10,11 @@ reference are replaced by the native library:
             the unique positive-diagonal R of X = QR       (linalg.py:101-124)
   lu_pl     dgetrf + P L                    -> cooperative GEPP kernel
                                                             (linalg.py:127-150)
-  sym_eig   dsyevd                          -> parallel block Jacobi
+  sym_eig   dsyevd                          -> Householder tridiagonalization +
+            bisection + inverse iteration (lr_syevd_f64); the parallel
+            block-Jacobi solver lr_syevj_f64 is opt-in (EIG_METHOD)
                                                             (linalg.py:153-169)
-  eig_svd   dsyrk + dsyevd + dgemm          -> DMMA syrk + Jacobi + DMMA gemm
+  eig_svd   dsyrk + dsyevd + dgemm          -> DMMA syrk + syevd + DMMA gemm
                                                             (linalg.py:172-202)
   oracle_svd dgesdd (dense, capped)         -> Gram + Jacobi, U re-orthonormalised
             by CholeskyQR2 (orthonormal completion for null directions)
@@ -453,8 +455,7 @@ def eig_svd_dev(A, cols=None, check=True):
     try:
         V, d = sym_eig_dev(G, symmetrize=False)
     except NumericalError:
-        if check:
-            _check_dev(A, "eig_svd input")  # a non-finite input is the reference's ValueError
+        _check_dev(A, "oracle_svd input")  # a non-finite input is the reference's ValueError
         raise
     dh = device.to_host(d)
     # a non-finite input shows as non-finite Gram eigenvalues: only then is
@@ -530,8 +531,7 @@ def _tall_dense_svd_dev(A):
     try:
         V, d = sym_eig_dev(G, symmetrize=False)
     except NumericalError:
-        if check:
-            _check_dev(A, "eig_svd input")  # a non-finite input is the reference's ValueError
+        _check_dev(A, "oracle_svd input")  # a non-finite input is the reference's ValueError
         raise
     dh = device.to_host(d)[::-1].copy()  # descending
     S = np.sqrt(np.maximum(dh, 0.0))

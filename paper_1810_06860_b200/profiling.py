@@ -4,8 +4,12 @@ models.
 Algorithmic bytes / flops per launch (fp64 = 8 B, int32 = 4 B):
   spmm   (rows r, cols c, width w, nnz):  B = 12 nnz + 4 (r+1) + 8 c w + 8 r w,
                                           F = 2 nnz w
-  svt step (m, n, rank r, nnz):           B = 4 (m+1) + 40 nnz + 8 (m+n) r + 8 r,
+  svt step (m, n, rank r, nnz):           B = 4 (m+1) + 28 nnz + 8 (m+n) r + 8 r,
                                           F = 2 r nnz + 4 nnz
+        per entry: column index 4, M 8, Y (CSR) read + write 16; with the
+        in-step CSC scatter (completion.CSC_SCATTER) + 12 (inverse perm 4,
+        CSC store 8) = SURVEY 8(d)'s 40 B/nnz
+  csc refresh (lr_gather_f64, nnz):       B = 20 nnz (perm 4, CSR value 8, CSC store 8)
   gemm   (M, N, K):                       F = 2 M N K  (SYRK: M (M+1) K, one triangle),
                                           B = 8 (M K + K N + M N)
 The dense kernels are bound by the fp64 tensor peak, the sparse ones by HBM
@@ -30,7 +34,13 @@ def spmm_model(meta):
 
 def svt_model(meta):
     nnz, m, n, r = meta["nnz"], meta["m"], meta["n"], meta["r"]
-    return 4 * (m + 1) + 40 * nnz + 8 * (m + n) * r + 8 * r, 2 * r * nnz + 4 * nnz
+    per = 40 if meta.get("csc_scatter", True) else 28
+    return 4 * (m + 1) + per * nnz + 8 * (m + n) * r + 8 * r, 2 * r * nnz + 4 * nnz
+
+
+def gather_model(meta):
+    nnz = meta["nnz"]
+    return 20 * nnz, 0
 
 
 def gemm_model(meta):
@@ -42,7 +52,7 @@ def gemm_model(meta):
 
 
 MODELS = {"lr_spmm_f64": ("hbm", spmm_model), "lr_spmm_f32": ("hbm", spmm_model),
-          "lr_svt_step_f64": ("hbm", svt_model),
+          "lr_svt_step_f64": ("hbm", svt_model), "lr_svt_step_flat_f64": ("hbm", svt_model), "lr_gather_f64": ("hbm", gather_model),
           "lr_gemm_f64": ("tensor", gemm_model)}
 
 

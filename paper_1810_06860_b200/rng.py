@@ -75,6 +75,140 @@ def gaussian_matrix(rng: RngState, rows: int, cols: int) -> np.ndarray:
     return np.ascontiguousarray(z.reshape((cols, rows)).T)
 
 
+# ------------------------------------------------- threaded host producer
+#
+# The parity Omega is numpy's own arithmetic (above), but one thread of it
+# costs ~0.35 s per cfg2 call (5.5M normals).  The draw splits exactly:
+# Philox4x64 words are counter-addressed (numpy's Philox.advance(k) skips k
+# four-word blocks), and every Box-Muller output depends on its own pair of
+# uniforms only, through numpy's element-wise ufuncs (log, sqrt, cos, sin),
+# whose per-element results do not depend on where a chunk starts
+# (tests/test_host_logic.py::test_threaded_gaussian_is_bit_exact checks it on
+# the host it runs on).  So T threads each fill a slice of the uniforms and of
+# the normals, in place, into a caller-provided (pinned) buffer -- the numpy
+# ufuncs and the Philox fill release the GIL.
+
+HOST_THREADS = None  # None: os.cpu_count()
+_POOL = None
+
+
+def _pool():
+    global _POOL
+    if _POOL is None:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+
+        _POOL = ThreadPoolExecutor(max_workers=HOST_THREADS or os.cpu_count() or 1,
+                                   thread_name_prefix="lr-omega")
+    return _POOL
+
+
+def _uniform_slice(seed: int, start: int, out: np.ndarray) -> None:
+    bg = np.random.Philox(key=seed)
+    bg.advance(start // 4)
+    gen = np.random.Generator(bg)
+    skip = start % 4
+    if skip:
+        gen.random(skip)
+    gen.random(out=out)
+
+
+def normals_column_major(seed: int, rows: int, cols: int, out: np.ndarray = None) -> np.ndarray:
+    """Omega = gaussian_matrix(RngState(seed), rows, cols) in COLUMN-major
+    order (the draw order: column c is out[c*rows:(c+1)*rows]), bit-identical
+    to the one-thread draw, computed by the thread pool into `out`."""
+    _check_shape(rows, cols)
+    count = rows * cols
+    npairs = (count + 1) // 2
+    u = np.empty(2 * npairs)
+    z = np.empty(2 * npairs) if (out is None or count % 2) else None
+    pool = _pool()
+    nt = max(1, min(pool._max_workers, (2 * npairs) // (1 << 16)))
+    # uniforms: contiguous slices of the counter space
+    cuts = [(2 * npairs * t) // nt for t in range(nt + 1)]
+    list(pool.map(lambda t: _uniform_slice(seed, cuts[t], u[cuts[t]:cuts[t + 1]]), range(nt)))
+    dst = z if z is not None else out.reshape(-1)[: 2 * npairs]
+    pc = [(npairs * t) // nt for t in range(nt + 1)]
+
+    def box_muller(t):
+        a, b = pc[t], pc[t + 1]
+        if a == b:
+            return
+        radius = np.sqrt(-2.0 * np.log(1.0 - u[a:b]))
+        angle = 2.0 * np.pi * u[npairs + a:npairs + b]
+        dst[2 * a:2 * b:2] = radius * np.cos(angle)
+        dst[2 * a + 1:2 * b:2] = radius * np.sin(angle)
+
+    list(pool.map(box_muller, range(nt)))
+    if out is None:
+        return z[:count]
+    if z is not None:
+        out.reshape(-1)[:count] = z[:count]
+    return out.reshape(-1)[:count]
+
+
+def _pinned_normals(seed: int, rows: int, cols: int):
+    import torch
+
+    count = rows * cols
+    host = torch.empty(count + (count & 1), dtype=torch.float64, pin_memory=True)
+    normals_column_major(seed, rows, cols, out=host.numpy())
+    return host
+
+
+_PREFETCH = {}
+
+
+def prefetch_normals(seed: int, rows: int, cols: int) -> None:
+    """Start drawing Omega(seed, rows, cols) on the host pool in the
+    background (the SVT loop calls this for the next fresh inner SVD while the
+    GPU runs the current iteration).  At most a few draws are kept."""
+    key = (int(seed), int(rows), int(cols))
+    if key in _PREFETCH or rows < 1 or cols < 1:
+        return
+    while len(_PREFETCH) >= 2:
+        _PREFETCH.pop(next(iter(_PREFETCH)))
+    import threading
+    from concurrent.futures import Future
+
+    fut = Future()
+
+    def run():
+        try:
+            fut.set_result(_pinned_normals(*key))
+        except BaseException as exc:  # pragma: no cover - surfaced by take_normals
+            fut.set_exception(exc)
+
+    threading.Thread(target=run, daemon=True, name="lr-omega-prefetch").start()
+    _PREFETCH[key] = fut
+
+
+def take_normals(seed: int, rows: int, cols: int):
+    """Pinned column-major Omega(seed, rows, cols): the prefetched draw when
+    one matches, else drawn now."""
+    fut = _PREFETCH.pop((int(seed), int(rows), int(cols)), None)
+    if fut is not None:
+        return fut.result()
+    return _pinned_normals(seed, rows, cols)
+
+
+def gaussian_matrix_fast(rng: RngState, rows: int, cols: int) -> np.ndarray:
+    """gaussian_matrix(rng, rows, cols), bit for bit, from the thread pool;
+    `rng` advances exactly as the one-thread draw advances it."""
+    _check_shape(rows, cols)
+    total = 2 * ((rows * cols + 1) // 2)
+    if rng.position != 0:
+        return gaussian_matrix(rng, rows, cols)
+    z = normals_column_major(rng.seed, rows, cols)
+    bg = np.random.Philox(key=rng.seed)
+    bg.advance(total // 4)
+    rng._gen = np.random.Generator(bg)
+    if total % 4:
+        rng._gen.random(total % 4)
+    rng.position += total
+    return np.ascontiguousarray(z.reshape((cols, rows)).T)
+
+
 def gaussian_matrix_device(seed: int, rows: int, cols: int, out=None):
     """Device Omega = gaussian_matrix(RngState(seed), rows, cols) generated by
     lr_gaussian_f64 directly into a padded device block (or into `out`)."""

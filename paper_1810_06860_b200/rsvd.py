@@ -12,13 +12,15 @@ Drop-in for /root/reference/pkg/src/lowrank/rsvd.py:
 Rank deficiency reroutes through the dense device SVD when allow_fallback,
 else re-raises with the same advice suffixes (rsvd.py:81-126).
 
-Omega is gaussian_matrix(RngState(seed), n, k+s).  `omega="device"`
-(default, OMEGA_SOURCE) generates it on the GPU from the same numpy Philox
-stream (uniform words bit-exact, normals within 4e-15 of the host values --
+Omega is gaussian_matrix(RngState(seed), n, k+s).  `omega="host"` (the
+default, OMEGA_SOURCE) draws it with numpy on the host -- the reference's own
+arithmetic, bit for bit, split over a thread pool (rng.normals_column_major)
+-- and uploads it in draw order for a device-side transpose; the SVT loop
+prefetches the next fresh call's draw while the GPU works.  `omega="device"`
+generates it on the GPU from the same numpy Philox stream (uniform words
+bit-exact, normals within 4e-15 of the host values --
 tests/test_gpu_kernels.py::test_device_gaussian_matches_host), so no n x w
-block crosses PCIe per call; `omega="host"` draws it with numpy on the host
-and uploads it (the reference's own arithmetic, bit for bit).  The parity
-suite runs both.
+block crosses PCIe.  The parity suite runs both.
 """
 
 from __future__ import annotations
@@ -34,7 +36,10 @@ from .linalg import (DevSvd, LazyQ, SvdResult, eig_svd_congruent_dev, eig_svd_de
 from .rng import RngState, gaussian_matrix, gaussian_matrix_device
 from .sparse import SparseMatrix, frobenius, spmm_dev, spmm_dev32, spmm_t_dev, spmm_t_dev32
 
-OMEGA_SOURCE = "device"
+# Omega's producer: "host" (the parity default: numpy's own draw, north_star's
+# "the same Gaussian test matrix passed in from the host") or "device"
+# (lr_gaussian_f64, the same Philox words, normals within 4e-15; no PCIe)
+OMEGA_SOURCE = "host"
 # rsvd_bki leaves the last CholeskyQR pass unformed (linalg.LazyQ): Y^T Q and
 # Q V run through Q1 and R2^{-1}; Subspace.Q forms Q only when asked.
 LAZY_LAST_PASS = True
@@ -128,7 +133,26 @@ def _copy(src, dst):
 def _omega(seed: int, n: int, w: int, source: str):
     if source == "device":
         return gaussian_matrix_device(seed, n, w)
-    return device.to_device(gaussian_matrix(RngState(seed), n, w))
+    return omega_from_host(seed, n, w)
+
+
+def omega_from_host(seed: int, n: int, w: int):
+    """Omega = gaussian_matrix(RngState(seed), n, w) drawn on the HOST with
+    numpy's own arithmetic (bit-identical to the reference's draw; threaded,
+    rng.normals_column_major) into page-locked memory in draw (column-major)
+    order, uploaded, and transposed into the row-major device block on the
+    GPU (lr_transpose_f64) -- the host never does the strided transpose."""
+    from .rng import take_normals
+
+    device.require_cuda()
+    count = n * w
+    host = take_normals(seed, n, w)
+    Zt = device.vector(count).view(w, n) if count else device.empty(w, n)
+    Zt.view(-1).copy_(host[:count], non_blocking=True)
+    device.TRAFFIC["h2d"] += 8 * count
+    Om = device.empty(n, w)
+    _native.call("lr_transpose_f64", device.ptr(Zt), n, w, n, device.ptr(Om), device.ld(Om), device.stream())
+    return Om
 
 
 def _lu_block(block, fb: _Fallback):

@@ -353,6 +353,8 @@ class ShardedEngine:
     """completion._svt_loop's matrix side spread over ranks; also the
     sharded rSVD-BKI (`bki`).  Factors U are row-sharded by R_g, V by C_g."""
 
+    omega_source = "device"  # every rank draws Omega on its own GPU (no host draw to prefetch)
+
     def __init__(self, obs: ObservationSet, exchange: Exchange = None, kernels=None):
         self.ex = exchange if exchange is not None else Exchange()
         self.K = kernels if kernels is not None else DeviceKernels()

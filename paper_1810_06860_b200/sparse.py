@@ -184,6 +184,20 @@ class DevicePattern:
             hp.csc_sched = _schedule(device.to_host(t_ptr).astype(np.int64))
         self.csc = _Side(rows=A.cols, ptr=t_ptr, idx=t_idx, sched=hp.csc_sched)
 
+    def tile_rows(self):
+        """Row of the first slot of every flat SVT tile (lr_svt_tile_rows_i32),
+        built on the device once per pattern."""
+        tr = getattr(self, "_tile_rows", None)
+        if tr is None:
+            lib = _native.load()
+            n_tiles = int(lib.lr_svt_tile_count(self.nnz))
+            tr = torch.empty(max(n_tiles, 1), dtype=torch.int32, device=device.require_cuda())
+            if n_tiles:
+                _native.call("lr_svt_tile_rows_i32", device.ptr(self.csr.ptr), self.csr.rows, self.nnz,
+                             device.ptr(tr), device.stream())
+            self._tile_rows = tr
+        return tr
+
     def values(self, host_vals: np.ndarray):
         """(csr, csc) device value copies of host values in CSR order."""
         pre = self._prefetch
@@ -218,6 +232,7 @@ class SparseMatrix:
         self._pattern = None  # DevicePattern (shared structure)
         self._dvals = None  # (csr, csc) device values
         self._host_stale = False
+        self._csc_stale = False  # CSR copy updated in place; CSC copy refreshed on demand
 
     # ------------------------------------------------------------ checks
     def _validate(self) -> None:
@@ -349,10 +364,30 @@ class SparseMatrix:
             self._hprep = getattr(other, "_hprep", None)
 
     def device_values(self):
-        """(csr, csc) device value vectors, created from the host data once."""
+        """(csr, csc) device value vectors, created from the host data once.
+        After an in-place update of the CSR copy alone (the fused SVT step,
+        `mark_csc_stale`) the CSC copy is refreshed here by one gather pass
+        (csc[s] = csr[perm[s]]: coalesced perm read and store, one random 8-byte
+        read per entry) before anything reads it."""
         if self._dvals is None:
             self._dvals = self.pattern().values(self._data)
+            self._csc_stale = False
+        elif self._csc_stale:
+            vc, vt = self._dvals
+            if self.nnz:
+                _native.call("lr_gather_f64", device.ptr(vc), device.ptr(self.pattern().perm), device.ptr(vt),
+                             self.nnz, device.stream(), meta={"nnz": self.nnz})
+            self._csc_stale = False
         return self._dvals
+
+    def device_values_csr(self):
+        """The CSR device value vector (no CSC refresh)."""
+        if self._dvals is None:
+            self.device_values()
+        return self._dvals[0]
+
+    def mark_csc_stale(self):
+        self._csc_stale = True
 
     def device_values32(self):
         """(csr, csc) fp32 copies of the device values (fp32 mode), rounded
@@ -443,6 +478,12 @@ def spmm_t(A: SparseMatrix, X):
     return out if _is_torch(X) else device.to_host(out)
 
 
+# SDDMM / fused SVT step kernel family: "flat" (tiles of consecutive CSR
+# slots, one warp each; lr_*_flat_f64) or "items" (a warp per row / row chunk;
+# lr_sddmm_f64 / lr_svt_step_f64)
+SVT_KERNEL = "flat"
+
+
 def project_pattern_dev(U, S, V, pattern: SparseMatrix, out=None):
     dp = pattern.pattern()
     r = int(S.shape[0])
@@ -452,6 +493,11 @@ def project_pattern_dev(U, S, V, pattern: SparseMatrix, out=None):
         return out
     if r == 0:
         _native.call("lr_fill_f64", device.ptr(out), 1, pattern.nnz, 1, 0.0, device.stream())
+        return out
+    if SVT_KERNEL == "flat":
+        _native.call("lr_sddmm_flat_f64", device.ptr(dp.csr.ptr), device.ptr(dp.csr.idx), dp.csr.rows,
+                     pattern.nnz, device.ptr(dp.tile_rows()), device.ptr(U), device.ld(U), device.ptr(S),
+                     device.ptr(V), device.ld(V), r, device.ptr(out), device.stream())
         return out
     _native.call("lr_sddmm_f64", device.ptr(dp.csr.ptr), device.ptr(dp.csr.idx), dp.csr.rows,
                  device.ptr(dp.csr.items), dp.csr.n_items, device.ptr(U), device.ld(U), device.ptr(S),

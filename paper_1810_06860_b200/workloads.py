@@ -17,7 +17,8 @@ cfg4  138493x26744, 20,000,263 ratings: row counts Zipf(1.0) floor 20 capped
       (exponential races for heavy rows, oversampled i.i.d. draws + dedup
       for light rows); values from a rank-20 N(0,1/sqrt(20)) product
       standardized to mean 3.5 / std 1, snapped to the 0.5 grid in [0.5,5];
-      10% held out with a seeded permutation               (seed 4)
+      10% held out by the reference's split_observations(obs, 0.9,
+      RngState(0)) (ingest.py:141-165; seed 0 = the CLI default)  (seed 4)
 cfg5  1e6x2e5, 2e8 uniform positions, rank-100 product + N(0, 0.01^2) noise
       (sigma = 0.01)                                          (seed 5)
 """
@@ -110,7 +111,23 @@ def _zipf_counts(m, n, total, s, floor):
     return c
 
 
-def cfg4(seed=4, m=138_493, n=26_744, total=20_000_263, rank=20, train=0.9, row_cap=9_184):
+def split_observations(count, train_fraction, rng):
+    """Train/test tags of the reference's split_observations
+    (/root/reference/pkg/src/lowrank/ingest.py:141-165): n_train =
+    round(fraction * count); the first n_train entries of rng.permutation(count)
+    are TRAIN (0), the rest TEST (1)."""
+    if not 0.0 < train_fraction < 1.0:
+        raise ValueError(f"train fraction must be in (0, 1), got {train_fraction}")
+    n_train = int(round(train_fraction * count))
+    if n_train == 0 or n_train == count:
+        raise ValueError(f"fraction {train_fraction} yields an empty split on {count} observations")
+    perm = rng.permutation(count)
+    split = np.ones(count, dtype=np.uint8)
+    split[perm[:n_train]] = 0
+    return split
+
+
+def cfg4(seed=4, m=138_493, n=26_744, total=20_000_263, rank=20, train=0.9, row_cap=9_184, split_seed=0):
     """row_cap: largest per-row count (SURVEY.md 8d probe of the rating shape:
     row nnz 43 / 83 / 9,184 min/median/max); without it the literal Zipf(1)
     head fills ~60 rows completely."""
@@ -164,9 +181,9 @@ def cfg4(seed=4, m=138_493, n=26_744, total=20_000_263, rank=20, train=0.9, row_
     x = np.einsum("er,er->e", F[i], G[j])
     x = (x - x.mean()) / x.std() + 3.5
     vals = np.clip(np.rint(x * 2.0) / 2.0, 0.5, 5.0)
-    perm = rng.permutation(i.size)
-    split = np.ones(i.size, np.uint8)
-    split[perm[: int(round(train * i.size))]] = 0
+    from .rng import RngState
+
+    split = split_observations(i.size, train, RngState(split_seed))
     return Observations(m, n, i, j, vals, split)
 
 

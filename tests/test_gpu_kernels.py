@@ -444,3 +444,44 @@ def test_convert_roundtrip_and_rounding():
     f = device.to_f32(d)
     back = device.to_host(device.to_f64(f))
     np.testing.assert_array_equal(back, x.astype(np.float32).astype(np.float64))
+
+
+@pytest.mark.parametrize("m,n,nnz,long_rows,empty_tail,r", [
+    (300, 200, 4000, 0, 0, 1), (300, 200, 4000, 2, 0, 5), (1000, 700, 30000, 3, 40, 17),
+    (5000, 3000, 200000, 1, 0, 48), (700, 600, 50000, 0, 100, 84), (400, 900, 60000, 2, 0, 300),
+    (2000, 1500, 100000, 0, 0, 1100)])
+def test_svt_step_flat_matches_oracle_and_refreshes_csc(m, n, nnz, long_rows, empty_tail, r):
+    """The flat fused SVT step (lr_svt_step_flat_f64, the product default):
+    residual and updated values against a numpy restatement of
+    completion.py:373-386, the CSC copy refreshed on demand (lr_gather_f64)
+    against the updated CSR values through the reference's stable argsort,
+    patterns with empty rows (a tail of empty rows and scattered ones), dense
+    rows, and ranks on both sides of the one-chunk limit (256) and of the
+    round-1 kernels' 1024 limit."""
+    import torch
+
+    from paper_1810_06860_b200 import completion, device
+    from paper_1810_06860_b200.sparse import ObservationSet
+
+    i, j, v = rand_pattern(m, n, nnz, seed=m + r, long_rows=long_rows)
+    keep = i < m - empty_tail
+    i, j, v = i[keep], j[keep], v[keep]
+    eng = completion.DeviceEngine(ObservationSet(m, n, i, j, v))
+    eng.m_norm = eng.observed_norm()
+    eng.start(1.7)
+    rng = np.random.default_rng(r)
+    U, V, S = rng.standard_normal((m, r)), rng.standard_normal((n, r)), rng.random(r) + 0.5
+    y0 = eng.Y.data.copy()
+    resid, deferred = eng.step(device.to_device(U), S, device.to_device(V), r, 0.37)
+    assert deferred is None
+    order = np.lexsort((j, i))
+    ii, jj, mm = i[order], j[order], v[order]
+    x = np.einsum("er,er->e", U[ii] * S, V[jj])
+    assert abs(resid - np.linalg.norm(x - mm) / np.linalg.norm(mm)) <= 1e-12 * max(resid, 1e-300)
+    y_ref = y0 + 0.37 * (mm - x)
+    y_dev = eng.Y.data
+    assert rel(y_dev, y_ref) <= 1e-13
+    yc, yt = eng.Y.device_values()  # CSC refresh
+    tperm = np.argsort(jj, kind="stable")
+    assert np.array_equal(device.to_host(yt), device.to_host(yc)[tperm])
+    assert torch.equal(yc.cpu(), torch.from_numpy(y_dev))

@@ -177,17 +177,11 @@ def test_svt_reference_test_case_recycling(golden):
                        ("tc_none_", dict(epsilon=1e-2, seed=7, strategy="none"))):
         got = completion.svt_fast(ob, completion.SvtParams(**kw))
         _compare_trace(got, golden, prefix)
-    # long reuse-q run (178 iterations, 143 recycles): recycling feeds rounding
-    # differences back into Y every step and the trajectory is chaotic (SURVEY
-    # 0.1 item 4), so parity is a long exact prefix plus the same outcome.
+    # the long reuse-q run (178 iterations, 143 recycles) is held to the
+    # reference's own reproducibility: see _compare_chaotic
     got = completion.svt_fast(ob, completion.SvtParams(epsilon=1e-2, seed=7, strategy="reuse-q", i_reuse=25))
-    ref_res = golden["tc_rq_residual"]
-    first_diff = next((i for i, t in enumerate(got.trace)
-                       if i >= len(ref_res) or abs(t.residual - ref_res[i]) > 1e-6 * ref_res[i]), len(got.trace))
-    assert first_diff >= 60, first_diff
-    _compare_trace(got, golden, "tc_rq_", exact_upto=first_diff, rtol=1e-6) if False else None
-    assert got.converged and bool(golden["tc_rq_converged"])
-    assert abs(got.iterations - len(ref_res)) <= 0.1 * len(ref_res)
+    _compare_chaotic(got, golden, "tc_rq_", "tc_rq")
+    assert got.converged
 
 
 def test_svt_cfg1_defaults_parity(golden):
@@ -398,3 +392,114 @@ def test_fp32_mode_recycling_and_fallback_paths():
     # rank-3 spectrum must not
     assert s64.fallbacks > 0
     assert np.max(np.abs(r32.S[:3] - r64.S[:3]) / r64.S[:3]) <= 1e-4
+
+
+# ---------------------------------------------------------------- round 2 goldens
+
+@pytest.fixture(scope="module")
+def golden2():
+    import os
+
+    return dict(np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                     "reference_golden_r02.npz")))
+
+
+def _compare_chaotic(got, g, prefix, ens, g2=None):
+    """Parity of a recycling trace whose trajectory the reference itself cannot
+    reproduce to the last digit.  tests/golden/
+    make_golden_r02.py reran the REAL reference with every observed value moved
+    by at most one ulp (6 seeds) and recorded where each rerun's residuals left
+    the unperturbed run (1e-13, 1e-10, 1e-8, 1e-6 relative).  The bar:
+      * iteration count within 1 and the same convergence outcome;
+      * the discrete trace (k, r, p, q, source) identical until the reference
+        moves by 1e-6 against itself;
+      * residuals within 1e-8 until the reference moves by 1e-13 against itself
+        (a rerun with different rounding in every kernel -- which any other
+        BLAS, thread count or GPU has -- cannot be held tighter than a rerun
+        with one perturbation at the start)."""
+    src = g2 if g2 is not None else g
+    if g2 is None:
+        import os
+
+        src = dict(np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                        "reference_golden_r02.npz")))
+    first = src[f"ens_{ens}_first_diff"]  # 1-based iterations, columns 1e-13 / 1e-10 / 1e-8 / 1e-6
+    assert set(src[f"ens_{ens}_iterations"].tolist()) == {int(src[f"ens_{ens}_base_iterations"])}
+    n_ref = len(g[prefix + "k"])
+    assert abs(got.iterations - n_ref) <= 1, (got.iterations, n_ref)
+    assert got.converged == bool(g[prefix + "converged"])
+    discrete_upto = min(int(first[:, 3].min()) - 1, got.iterations, n_ref)
+    resid_upto = min(int(first[:, 0].min()) - 1, got.iterations, n_ref)
+    tr = got.trace[:discrete_upto]
+    for name, attr in (("k", "k"), ("r", "r"), ("p", "p"), ("q", "q"), ("source", "svd_source")):
+        ours = [getattr(t, attr) for t in tr]
+        ref = list(g[prefix + name][:discrete_upto])
+        bad = next((i for i, (a, b) in enumerate(zip(ours, ref)) if a != b), None)
+        assert bad is None, f"{prefix}{name} differs at iteration {bad + 1}: {ours[bad]} vs {ref[bad]}"
+    np.testing.assert_allclose([t.residual for t in got.trace[:resid_upto]], g[prefix + "residual"][:resid_upto],
+                               rtol=1e-8)
+    return discrete_upto, resid_upto
+
+
+@pytest.mark.parametrize("prefix,ens,kw", [
+    ("svt_small_rq_", "small_rq", dict(epsilon=1e-3, seed=4, strategy="reuse-q", i_reuse=20)),
+    ("svt_small_ru_", "small_ru", dict(epsilon=1e-3, seed=4, strategy="reuse-u", i_reuse=20)),
+])
+def test_svt_small_recycling_goldens(golden, golden2, prefix, ens, kw):
+    """The 500-iteration recycling runs of the small case: both reach i_max
+    without converging in the reference (reuse-q after 440 recycles, reuse-u
+    after 428); same outcome and the reference-reproducible prefix."""
+    from paper_1810_06860_b200 import completion, workloads
+
+    obs, _ = workloads.cfg1_small()
+    got = completion.svt_fast(_obs(obs), completion.SvtParams(**kw))
+    assert not bool(golden[prefix + "converged"]) and got.iterations == 500 and not got.converged
+    d, r = _compare_chaotic(got, golden, prefix, ens, golden2)
+    assert d >= 100 and r >= 80
+    n_rec = sum(t.svd_source.startswith("recycle") for t in got.trace)
+    n_ref = int(sum(str(x).startswith("recycle") for x in golden[prefix + "source"]))
+    assert abs(n_rec - n_ref) <= 0.05 * n_ref, (n_rec, n_ref)
+
+
+def test_svt_cfg1_reuse_q_instability(golden2):
+    """SURVEY 0.1 item 4 on BASELINE configs[0] (eps = 1e-3, svt_fast reuse-q,
+    i_reuse = 50): the streak rule lowers p during recycling, the forced fresh
+    BKI at p = 1 throws the residual up by two orders of magnitude and the run
+    never converges -- while svt_reference(bki) converges in 61 iterations
+    (test_svt_cfg1_tight_tolerance).  The GPU must reproduce both."""
+    from paper_1810_06860_b200 import completion, workloads
+
+    obs, _ = workloads.cfg1()
+    got = completion.svt_fast(_obs(obs), completion.SvtParams(epsilon=1e-3, seed=0, strategy="reuse-q", i_reuse=50))
+    g = golden2
+    assert not bool(g["cfg1rq_converged"]) and got.iterations == 500 and not got.converged
+    _compare_chaotic(got, g, "cfg1rq_", "cfg1rq", g)
+    res = np.array([t.residual for t in got.trace])
+    ref = g["cfg1rq_residual"]
+    # the blow-up: first iteration whose residual jumps by > 10x over the previous one
+    jump = lambda r: int(np.argmax(r[1:] > 10 * r[:-1])) + 2
+    assert jump(res) == jump(ref), (jump(res), jump(ref))
+    assert res[jump(res) - 2] < 1e-2 < 0.1 < res[jump(res) - 1]
+
+
+@pytest.mark.parametrize("name", ["pi", "bki"])
+def test_rsvd_cfg2_matches_reference(golden2, name):
+    """BASELINE configs[1]: rsvd_pi / rsvd_bki (k=100, s=10, p=5, seed 0) on
+    the seeded 100000 x 50000, 5M-nnz matrix with the host-drawn Omega of the
+    reference's gaussian_matrix, against the REAL reference's outputs
+    (tests/golden/make_golden_r02.py): singular values within 1e-8 relative
+    (north_star), qb_error within 1e-10, the rank-100 product on the first 256
+    rows / columns within 1e-8 of its norm."""
+    from paper_1810_06860_b200 import rsvd, workloads
+    from paper_1810_06860_b200.sparse import SparseMatrix
+
+    o = workloads.cfg2()
+    A = SparseMatrix.from_coo(o.m, o.n, o.rows, o.cols, o.values)
+    fn = rsvd.rsvd_pi if name == "pi" else rsvd.rsvd_bki
+    res, _ = fn(A, rsvd.RsvdParams(k=100, p=5, s=10, seed=0), omega="host")
+    S_ref = golden2[f"cfg2_{name}_S"]
+    assert float(np.max(np.abs(res.S - S_ref) / S_ref)) <= 1e-8
+    assert abs(rsvd.qb_error(A, res) - float(golden2[f"cfg2_{name}_qb"])) <= 1e-10
+    P = (res.U[:256] * res.S) @ res.V[:256].T
+    P_ref = (golden2[f"cfg2_{name}_U256"] * S_ref) @ golden2[f"cfg2_{name}_V256"].T
+    assert rel(P, P_ref) <= 1e-8

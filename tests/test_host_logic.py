@@ -136,3 +136,40 @@ def test_product_path_fails_loudly_without_cuda():
     obs = sparse.ObservationSet(o.m, o.n, o.rows, o.cols, o.values)
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         completion.svt_fast(obs, completion.SvtParams(i_max=1))
+
+
+def test_split_observations_matches_reference():
+    """workloads.split_observations (cfg4's holdout) against the REAL
+    reference's ingest.split_observations tags (tests/golden/make_golden_r02.py)."""
+    import os
+
+    from paper_1810_06860_b200 import workloads
+    from paper_1810_06860_b200.rng import RngState
+
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_golden_r02.npz"))
+    for count, frac, seed in ((1000, 0.9, 0), (777, 0.8, 42)):
+        got = workloads.split_observations(count, frac, RngState(seed))
+        assert np.array_equal(got, g[f"split_{count}_{seed}"])
+    with pytest.raises(ValueError, match="train fraction"):
+        workloads.split_observations(10, 1.0, RngState(0))
+    with pytest.raises(ValueError, match="empty split"):
+        workloads.split_observations(3, 0.01, RngState(0))
+
+
+@pytest.mark.parametrize("rows,cols,seed", [(50000, 110, 7), (37, 11, 3), (1001, 3, 5), (1, 1, 9),
+                                            (26744, 65, 2 ** 62 + 11)])
+def test_threaded_gaussian_is_bit_exact(rows, cols, seed):
+    """The threaded host Omega (rng.normals_column_major, the parity default's
+    producer) equals the one-thread reference draw bit for bit on this host,
+    and leaves the stream where the one-thread draw leaves it."""
+    from paper_1810_06860_b200 import rng as R
+
+    ref = R.gaussian_matrix(R.RngState(seed), rows, cols)
+    st = R.RngState(seed)
+    got = R.gaussian_matrix_fast(st, rows, cols)
+    assert np.array_equal(got, ref)
+    z = R.normals_column_major(seed, rows, cols)
+    assert np.array_equal(z.reshape(cols, rows).T, ref)
+    st2 = R.RngState(seed)
+    R.gaussian_matrix(st2, rows, cols)
+    assert st.position == st2.position and np.array_equal(st.uniform(7), st2.uniform(7))
