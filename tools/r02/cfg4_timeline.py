@@ -1,0 +1,96 @@
+"""cfg4 SVT job (bench.py's settings) with a host + device timeline of every
+native call: GPU busy time vs job time, the largest GPU-idle gaps and the
+native call that ended each gap, and a cProfile of the host side.
+Usage: python tools/r02/cfg4_timeline.py [job|cprofile]"""
+import cProfile
+import os
+import pstats
+import sys
+import time
+from collections import defaultdict
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_1810_06860_b200 import _native, completion, profiling, workloads  # noqa: E402
+from paper_1810_06860_b200.sparse import ObservationSet  # noqa: E402
+
+
+class TL(profiling.Profiler):
+    def run(self, name, meta, fn, args):
+        h0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = fn(*args)
+        e1.record()
+        self.records.append((name, meta, e0, e1, h0, time.perf_counter()))
+        return st
+
+
+o4 = workloads.cfg4()
+obs = ObservationSet(o4.m, o4.n, o4.rows, o4.cols, o4.values, o4.split)
+params = bench.cfg4_params()
+eng = completion.DeviceEngine(obs)
+
+
+def job():
+    return completion._svt_loop(obs, params, "rsvd-bki", params.strategy, engine=eng)
+
+
+for _ in range(2):
+    job()
+torch.cuda.synchronize()
+mode = sys.argv[1] if len(sys.argv) > 1 else "job"
+if mode == "cprofile":
+    pr = cProfile.Profile()
+    t0 = time.perf_counter()
+    pr.enable()
+    res = job()
+    torch.cuda.synchronize()
+    pr.disable()
+    print(f"{res.iterations} iterations in {time.perf_counter() - t0:.3f} s")
+    pstats.Stats(pr).sort_stats("tottime").print_stats(30)
+    pstats.Stats(pr).sort_stats("cumtime").print_stats(40)
+    sys.exit(0)
+
+tl = TL()
+_native.PROFILER = tl
+base = torch.cuda.Event(enable_timing=True)
+base.record()
+h_base = time.perf_counter()
+res = job()
+endev = torch.cuda.Event(enable_timing=True)
+endev.record()
+torch.cuda.synchronize()
+h_end = time.perf_counter()
+_native.PROFILER = None
+total = base.elapsed_time(endev)
+busy = 0.0
+gaps = []
+prev_end = 0.0
+per = defaultdict(float)
+for name, meta, e0, e1, h0, h1 in tl.records:
+    g0, g1 = base.elapsed_time(e0), base.elapsed_time(e1)
+    busy += g1 - g0
+    per[name] += g1 - g0
+    if g0 - prev_end > 0.02:
+        gaps.append((g0 - prev_end, name, prev_end, 1e3 * (h0 - h_base)))
+    prev_end = max(prev_end, g1)
+print(f"{res.iterations} iterations: device span {total:.1f} ms, native busy {busy:.1f} ms "
+      f"({busy / total:.2%}), host wall {1e3 * (h_end - h_base):.1f} ms, {len(tl.records)} native calls")
+gsum = defaultdict(lambda: [0, 0.0])
+for g, name, *_ in gaps:
+    gsum[name][0] += 1
+    gsum[name][1] += g
+print("idle gaps > 20 us, by the native call that ended them (count, total ms):")
+for name, (c, t) in sorted(gsum.items(), key=lambda kv: -kv[1][1]):
+    print(f"  {name:28s} {c:5d} {t:9.2f}")
+print("busy by call (ms):")
+for name, t in sorted(per.items(), key=lambda kv: -kv[1]):
+    print(f"  {name:28s} {t:9.2f}")
+print("largest 15 gaps (ms, next call, gpu t, host t):")
+for g in sorted(gaps, reverse=True)[:15]:
+    print(f"  {g[0]:7.3f} {g[1]:28s} gpu {g[2]:9.2f} host {g[3]:9.2f}")
