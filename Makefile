@@ -3,7 +3,10 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
 SRC := $(wildcard paper_1810_06860_b200/csrc/*.cu)
-OBJ := $(patsubst paper_1810_06860_b200/csrc/%.cu,build/%.o,$(SRC))
+CSRC := $(wildcard paper_1810_06860_b200/csrc/*.c)
+OBJ := $(patsubst paper_1810_06860_b200/csrc/%.cu,build/%.o,$(SRC)) $(patsubst paper_1810_06860_b200/csrc/%.c,build/%.c.o,$(CSRC))
+# host C (the parity Omega's uniforms / Box-Muller): strict IEEE, numpy's operation order
+CFLAGS_HOST := -O2 -fPIC -fno-fast-math -ffp-contract=off -Wall
 LIB := paper_1810_06860_b200/_native/liblowrank_b200.so
 
 all: $(LIB)
@@ -12,9 +15,13 @@ build/%.o: paper_1810_06860_b200/csrc/%.cu paper_1810_06860_b200/csrc/lr_common.
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
+build/%.c.o: paper_1810_06860_b200/csrc/%.c
+	@mkdir -p build
+	$(CC) $(CFLAGS_HOST) -c $< -o $@
+
 $(LIB): $(OBJ)
 	@mkdir -p $(dir $(LIB))
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lm
 
 clean:
 	rm -rf build $(LIB)

@@ -217,6 +217,17 @@ int lr_fix_signs_f64(double* V, long long ldv, int rows_v, int cols, double* U, 
 int lr_scale_columns_f64(const double* V, long long ldv, int rows, const int* cols_idx, int ncols,
                          const double* S, int invert, double* B, long long ldb, void* stream);
 
+/* One-sided Jacobi sweep for the dense SVD fallback (oracle_svd ->
+ * dgesdd, linalg.py:205-221): the columns of B are the rows of Bt (n x m),
+ * the columns of V the rows of Vt (n x n).  Every column pair (one
+ * round-robin sweep, N-1 launches) with |<b_p, b_q>| > tol |b_p| |b_q| is
+ * rotated orthogonal, the rotation applied to Vt too; off[0] (device) =
+ * the largest measure rotated (0: converged).  Deterministic. */
+int lr_jacobi_sweep_f64(int n, int m, double* Bt, long long ldb, double* Vt, long long ldv, double tol,
+                        double* off, void* stream);
+/* out[i] = ||row i of Bt||_2 (scaled, no overflow), n rows of length m. */
+int lr_row_norms_f64(const double* Bt, long long ldb, int n, int m, double* out, void* stream);
+
 /* --------------------------------------------------------------- random */
 /* Omega (rows x cols, row-major, ldo) = gaussian_matrix(RngState(seed), rows,
  * cols) of rng.py:77-94 on the device: numpy Philox4x64-10 (key = seed,
@@ -225,6 +236,14 @@ int lr_scale_columns_f64(const double* V, long long ldv, int rows, const int* co
  * normals within a few ulp (log/sincos rounding). */
 int lr_gaussian_f64(unsigned long long seed, int rows, int cols, double* omega, long long ldo,
                     void* stream);
+
+/* Host functions (no device work): the C pieces of the parity Omega's host
+ * draw (rng.py:38-55 of the reference).  lr_host_uniforms: out[i] = uniform
+ * start + i of numpy's Philox(key=seed) stream ((x >> 11) 2^-53).
+ * lr_host_box_muller: z[2i] = sqrt(-2 logs[i]) cos(2 pi u2[i]),
+ * z[2i+1] = ... sin(...), logs[i] = log(1 - u[i]) computed by numpy. */
+void lr_host_uniforms(unsigned long long seed, long long start, long long count, double* out);
+void lr_host_box_muller(const double* logs, const double* u2, long long n, double* z);
 
 /* ------------------------------------------------------------- utilities */
 int lr_copy2d_f64(const double* src, long long lds, double* dst, long long ldd, long long rows,

@@ -99,6 +99,31 @@ __device__ __forceinline__ double block_max(double v, double* sh) {
   return r;
 }
 
+// Streaming loads that do not allocate in L1 (the CSR index / value / M / Y
+// streams of the sparse kernels): L1 keeps the gathered dense rows, whose
+// Zipf-hot part it can serve.
+__device__ __forceinline__ int ld_stream(const int* p) {
+  int v;
+  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+// Y (read-write in the same kernel): plain load without L1 allocation
+__device__ __forceinline__ double ld_stream_rw(const double* p) {
+  double v;
+  asm("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 // Non-contracted arithmetic where the reference's numpy expression has no FMA.
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }

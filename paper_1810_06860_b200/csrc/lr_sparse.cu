@@ -670,6 +670,332 @@ __global__ void pattern_axpy_kernel(double* __restrict__ y_csr, double* __restri
   }
 }
 
+// ------------------------------------------------- line-aligned group kernels
+// The gathers of both sparse products are bound by the L1 data pipe, not by
+// L2 or HBM (ncu, cfg4 w = 22: L1 wavefronts 82 % of peak, L2 44 %, DRAM
+// 10 %; profiles/r02f_*): a warp load costs one wavefront per distinct
+// 128-byte line it touches.  These kernels therefore
+//   * read every gathered row as whole aligned 16-byte chunks starting at the
+//     row's 128-byte line (lane g of a G-lane group owns chunks g + G t,
+//     t < T; `shift` = the elements between the line start and column 0), so
+//     an aligned row of b bytes costs ceil(b / 128) wavefronts;
+//   * load the stored entries' column index / value (and M, Y) as coalesced
+//     per-group batches of 32 consecutive entries (one HBM round trip per 32
+//     entries instead of a broadcast load per entry);
+//   * keep each G-lane group on its own sequence of work items (grid-stride
+//     per group; the warp runs until its last group is done), so Zipf-length
+//     rows do not idle the other groups of a warp.
+// Over-reads stay inside the allocation: the first chunk starts at the
+// 128-byte line of column 0 (CUDA allocations are >= 256-byte aligned) and
+// the last ends at the next 16-byte boundary of the row.
+template <typename Sc>
+struct Chunk16;
+template <>
+struct Chunk16<double> {
+  using type = double2;
+  static constexpr int VE = 2;
+  static __device__ __forceinline__ void fma_into(double v, const double2& x, double2& a) {
+    a.x = fma(v, x.x, a.x);
+    a.y = fma(v, x.y, a.y);
+  }
+  static __device__ __forceinline__ double2 zero() { return make_double2(0.0, 0.0); }
+  static __device__ __forceinline__ double get(const double2& c, int i) { return i == 0 ? c.x : c.y; }
+};
+template <>
+struct Chunk16<float> {
+  using type = float4;
+  static constexpr int VE = 4;
+  static __device__ __forceinline__ void fma_into(float v, const float4& x, float4& a) {
+    a.x = fmaf(v, x.x, a.x);
+    a.y = fmaf(v, x.y, a.y);
+    a.z = fmaf(v, x.z, a.z);
+    a.w = fmaf(v, x.w, a.w);
+  }
+  static __device__ __forceinline__ float4 zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  static __device__ __forceinline__ float get(const float4& c, int i) {
+    return i == 0 ? c.x : (i == 1 ? c.y : (i == 2 ? c.z : c.w));
+  }
+};
+
+constexpr int kGroupBatch = 32;  // stored entries per group batch
+// build-time tuning of the group kernels (tools/r02/group_variants.sh)
+#ifndef LR_GRP_MINB
+#define LR_GRP_MINB 2
+#endif
+#ifndef LR_SVT_MINB
+#define LR_SVT_MINB 3  // r02k sweep: 3 CTAs/SM beat 2 at every rank (r = 48: 1.48 -> 1.19 ms)
+#endif
+#ifndef LR_SPMM_QLO
+#define LR_SPMM_QLO 8
+#endif
+#ifndef LR_SPMM_QHI
+#define LR_SPMM_QHI 4
+#endif
+#ifndef LR_SVT_Q1
+#define LR_SVT_Q1 8
+#endif
+#ifndef LR_SVT_Q2
+#define LR_SVT_Q2 4
+#endif
+#ifndef LR_SVT_Q3
+#define LR_SVT_Q3 2
+#endif
+
+// Y (rows x w) = A X over a row-compressed pattern, w <= G T VE - shift.
+// Per output element the entries are accumulated in storage order (fma), as
+// in the item kernel above: results are bit-identical to it.
+template <int G, int T, int Q, typename Sc>
+__global__ void __launch_bounds__(256, LR_GRP_MINB) spmm_group_kernel(
+    const int* __restrict__ ptr, const int* __restrict__ idx, const Sc* __restrict__ val,
+    const int* __restrict__ items, int n_items, const Sc* __restrict__ X, long long ldx, int w, int shift,
+    Sc* __restrict__ Y, long long ldy, Sc* __restrict__ scratch) {
+  using C = Chunk16<Sc>;
+  using CT = typename C::type;
+  constexpr int VE = C::VE;
+  constexpr int GROUPS = 32 / G;
+  constexpr int KB = kGroupBatch / G;  // batch entries per lane
+  const int lane = threadIdx.x & 31, g = lane % G, grp = lane / G, gbase = grp * G;
+  const long long n_groups = (long long)gridDim.x * (blockDim.x >> 5) * GROUPS;
+  long long it = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * GROUPS + grp;
+  // software pipeline: the next batch's column indices / values (and the
+  // next item's descriptor) are in flight while the current batch gathers
+  Item cur{0, 0, 0, -1}, nxt{0, 0, 0, -1};
+  if (it < n_items) cur = load_item(items, ptr, (int)it);
+  if (it + n_groups < n_items) nxt = load_item(items, ptr, (int)(it + n_groups));
+  int e = cur.beg;
+  int jk[KB];
+  Sc vk[KB];
+#pragma unroll
+  for (int k = 0; k < KB; ++k) {
+    const bool ok = g + G * k < cur.end - e;
+    jk[k] = ok ? ld_stream(idx + e + g + G * k) : 0;
+    vk[k] = ok ? ld_stream(val + e + g + G * k) : Sc(0);
+  }
+  CT acc[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) acc[t] = C::zero();
+  const Sc* Xs = X - shift;
+  while (__any_sync(0xffffffffu, it < n_items)) {
+    const bool act = it < n_items;
+    const int nb = act ? min(kGroupBatch, cur.end - e) : 0;
+    const bool same = act && e + nb < cur.end;
+    const int ne = same ? e + nb : nxt.beg;
+    const int nn = same ? cur.end - ne : ((it + n_groups < n_items) ? nxt.end - ne : 0);
+    int jn[KB];
+    Sc vn[KB];
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      const bool ok = g + G * k < nn;
+      jn[k] = ok ? ld_stream(idx + ne + g + G * k) : 0;
+      vn[k] = ok ? ld_stream(val + ne + g + G * k) : Sc(0);
+    }
+#pragma unroll
+    for (int q0 = 0; q0 < kGroupBatch; q0 += Q) {
+      if (!__any_sync(0xffffffffu, q0 < nb)) break;
+      CT xv[Q][T];
+      Sc vq[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int ent = q0 + q;
+        const int j = __shfl_sync(0xffffffffu, jk[ent / G], gbase + ent % G);
+        vq[q] = __shfl_sync(0xffffffffu, vk[ent / G], gbase + ent % G);
+        const CT* xr = reinterpret_cast<const CT*>(Xs + (long long)j * ldx);
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          const int c = (g + G * t) * VE - shift;  // first column of the chunk
+          xv[q][t] = (ent < nb && c + VE > 0 && c < w) ? __ldg(xr + g + G * t) : C::zero();
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int t = 0; t < T; ++t) C::fma_into(vq[q], xv[q][t], acc[t]);
+    }
+    e += nb;
+    if (act && e >= cur.end) {
+      Sc* dst = (cur.slot >= 0) ? (scratch + (long long)cur.slot * w) : (Y + (long long)cur.row * ldy);
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+#pragma unroll
+        for (int i = 0; i < VE; ++i) {
+          const int c = (g + G * t) * VE - shift + i;
+          if (c >= 0 && c < w) dst[c] = C::get(acc[t], i);
+        }
+        acc[t] = C::zero();
+      }
+      it += n_groups;
+      cur = nxt;
+      e = cur.beg;
+      if (it + n_groups < n_items) nxt = load_item(items, ptr, (int)(it + n_groups));
+    }
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      jk[k] = jn[k];
+      vk[k] = vn[k];
+    }
+  }
+}
+
+// Fused SVT step / SDDMM over CSR items (r <= 2 G T, V rows read from their
+// start: the per-lane column slices, hence every entry's summation order,
+// depend on (G, T, r) only -- the sharded engine's row- and column-block
+// passes produce identical bits).  The item's row of U * S lives in
+// registers (loaded once per item); per entry the group gathers V[j, :] as
+// aligned chunks, each lane folds its columns (fma, ascending), and R = min(G, 8)
+// entries' lane partials are reduced together (xor levels over the lane bits
+// >= R, then a transpose-reduce over the low bits: R - 1 shuffles per R
+// entries; the same tree for every entry).  Results are parked in shared
+// memory and every lane finishes its own batch entries with coalesced M / Y
+// traffic (residual partials, Y += step (m - x)).
+template <int G, int T, bool FUSED>
+__global__ void __launch_bounds__(256, LR_SVT_MINB) svt_group2_kernel(
+    const int* __restrict__ ptr, const int* __restrict__ idx, const int* __restrict__ items, int n_items,
+    const double* __restrict__ U, long long ldu, const double* __restrict__ S, const double* __restrict__ V,
+    long long ldv, int r, double* __restrict__ x_out, const double* __restrict__ m_vals,
+    double* __restrict__ y_csr, double* __restrict__ y_csc, const int* __restrict__ inv_perm, double step,
+    int apply, double* __restrict__ partial) {
+  constexpr int GROUPS = 32 / G;
+  constexpr int B = (4 * G < kGroupBatch) ? 4 * G : kGroupBatch;  // batch entries per group
+  constexpr int KB = B / G;
+  constexpr int R = G < 8 ? G : 8;
+  constexpr int QT = T == 1 ? LR_SVT_Q1 : (T == 2 ? LR_SVT_Q2 : LR_SVT_Q3);
+  constexpr int Q = QT < R ? QT : R;  // entries' gathers in flight (divides R)
+  __shared__ double xs_all[8][B * GROUPS];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, g = lane % G, grp = lane / G, gbase = grp * G;
+  double* xs = xs_all[wib] + grp * B;
+  const long long n_groups = (long long)gridDim.x * (blockDim.x >> 5) * GROUPS;
+  long long it = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * GROUPS + grp;
+  Item cur{0, 0, 0, -1}, nxt{0, 0, 0, -1};
+  double2 us[T];
+  auto load_us = [&](int row) {
+    const double* ur = U + (long long)row * ldu;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int c = 2 * (g + G * t);
+      us[t].x = (c < r) ? __ldg(ur + c) * __ldg(S + c) : 0.0;
+      us[t].y = (c + 1 < r) ? __ldg(ur + c + 1) * __ldg(S + c + 1) : 0.0;
+    }
+  };
+  // software pipeline: the next batch's column indices (and the next item's
+  // descriptor) are in flight while the current batch gathers
+  if (it < n_items) {
+    cur = load_item(items, ptr, (int)it);
+    load_us(cur.row);
+  }
+  if (it + n_groups < n_items) nxt = load_item(items, ptr, (int)(it + n_groups));
+  int e = cur.beg;
+  int jk[KB];
+#pragma unroll
+  for (int k = 0; k < KB; ++k) jk[k] = (g + G * k < cur.end - e) ? ld_stream(idx + e + g + G * k) : 0;
+  double ss = 0.0, mx = 0.0;
+  while (__any_sync(0xffffffffu, it < n_items)) {
+    const bool act = it < n_items;
+    const int nb = act ? min(B, cur.end - e) : 0;
+    const bool same = act && e + nb < cur.end;
+    const int ne = same ? e + nb : nxt.beg;
+    const int nn = same ? cur.end - ne : ((it + n_groups < n_items) ? nxt.end - ne : 0);
+    int jn[KB];
+#pragma unroll
+    for (int k = 0; k < KB; ++k) jn[k] = (g + G * k < nn) ? ld_stream(idx + ne + g + G * k) : 0;
+#pragma unroll
+    for (int sb = 0; sb < B; sb += R) {
+      if (!__any_sync(0xffffffffu, sb < nb)) break;
+      double part[R];
+#pragma unroll
+      for (int q0 = 0; q0 < R; q0 += Q) {
+        double2 vv[Q][T];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int ent = sb + q0 + q;
+          const int j = __shfl_sync(0xffffffffu, jk[ent / G], gbase + ent % G);
+          const double2* vr = reinterpret_cast<const double2*>(V + (long long)j * ldv);
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            const int c = 2 * (g + G * t);
+            double2 v = make_double2(0.0, 0.0);
+            if (ent < nb && c < r) {
+              v = __ldg(vr + g + G * t);
+              if (c + 1 >= r) v.y = 0.0;  // the row's padding may hold anything
+            }
+            vv[q][t] = v;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          double p = 0.0;
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            p = fma(us[t].x, vv[q][t].x, p);
+            p = fma(us[t].y, vv[q][t].y, p);
+          }
+          part[q0 + q] = p;
+        }
+      }
+      // lane bits >= R: plain butterfly on all R partials
+#pragma unroll
+      for (int o = G / 2; o >= R; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < R; ++q) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
+      // low bits: transpose-reduce (lane g keeps entry g % R)
+#pragma unroll
+      for (int o = R / 2; o >= 1; o >>= 1) {
+        const bool hi = (g & o) != 0;
+#pragma unroll
+        for (int q = 0; q < o; ++q) {
+          const double send = hi ? part[q] : part[q + o];
+          const double keep = hi ? part[q + o] : part[q];
+          part[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if (g < R) xs[sb + g] = part[0];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < KB; ++k) {
+      const int b = g + G * k;
+      if (b < nb) {
+        const long long ee = e + b;
+        const double xl = xs[b];
+        if (FUSED) {
+          // M / Y read here, not prefetched with the indices: their registers
+          // would displace gathers in flight (the kernel is latency-bound)
+          const double mv = ld_stream(m_vals + ee);
+          const double d = xl - mv;
+          ss = fma(d, d, ss);
+          mx = fmax(mx, fabs(d));
+          if (apply) {
+            const double ynew = add_rn(ld_stream_rw(y_csr + ee), mul_rn(step, add_rn(mv, -xl)));
+            y_csr[ee] = ynew;
+            if (y_csc) y_csc[__ldg(inv_perm + ee)] = ynew;
+          }
+        } else {
+          x_out[ee] = xl;
+        }
+      }
+    }
+    __syncwarp();
+    e += nb;
+    if (act && e >= cur.end) {
+      it += n_groups;
+      cur = nxt;
+      e = cur.beg;
+      if (it < n_items) load_us(cur.row);
+      if (it + n_groups < n_items) nxt = load_item(items, ptr, (int)(it + n_groups));
+    }
+#pragma unroll
+    for (int k = 0; k < KB; ++k) jk[k] = jn[k];
+  }
+  if (FUSED) {
+    __shared__ double red[32];
+    const double S2 = block_sum<256>(ss, red);
+    const double M2 = block_max<256>(mx, red);
+    if (threadIdx.x == 0) {
+      partial[2 * blockIdx.x] = S2;
+      partial[2 * blockIdx.x + 1] = M2;
+    }
+  }
+}
+
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 template <int G, int T, bool V2, int Q = 4, typename Sc = double>
@@ -731,6 +1057,82 @@ static void dispatch_spmm(const int* ptr, const int* idx, const Sc* val, const i
 
 static bool aligned_bytes(const void* p, unsigned a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
+// (G, T) of the line-aligned kernels: a group spans >= 8 chunks (one
+// 128-byte line per lane sweep; a 4-lane group would visit a line in two
+// instructions, two wavefronts) unless the row fits 4 chunks; then the fewest
+// chunk slots G*T covering `chunks` (ties: the smaller group, more entries per
+// warp instruction); T <= 4.  Returns false past 128 chunks.
+static bool pick_group(int chunks, int& G, int& T) {
+  if (chunks <= 4) {
+    G = 4;
+    T = 1;
+    return true;
+  }
+  static const int Gs[3] = {8, 16, 32};
+  int best = 1 << 30;
+  G = T = 0;
+  for (int gi = 0; gi < 3; ++gi)
+    for (int t = 1; t <= 4; ++t)
+      if (Gs[gi] * t >= chunks && Gs[gi] * t < best) {
+        best = Gs[gi] * t;
+        G = Gs[gi];
+        T = t;
+      }
+  return G > 0;
+}
+
+static int occupancy_blocks(const void* fn) {
+  int o = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 256, 0);
+  return o < 1 ? 1 : o;
+}
+
+template <int G, int T, typename Sc>
+static void launch_spmm_group_t(const int* ptr, const int* idx, const Sc* val, const int* items, int n_items,
+                                const Sc* X, long long ldx, int w, int shift, Sc* Y, long long ldy, Sc* scratch,
+                                cudaStream_t s) {
+  constexpr int Q = T <= 2 ? LR_SPMM_QLO : LR_SPMM_QHI;
+  constexpr int GROUPS = 32 / G;
+  static int occ = -1;
+  if (occ < 0) {
+    // no shared memory: the whole unified L1 for the gathered rows
+    cudaFuncSetAttribute(spmm_group_kernel<G, T, Q, Sc>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    occ = occupancy_blocks(reinterpret_cast<const void*>(spmm_group_kernel<G, T, Q, Sc>));
+  }
+  const long long warps = ((long long)n_items + GROUPS - 1) / GROUPS;
+  long long blocks = (warps + 7) / 8;
+  const long long cap = (long long)sm_count() * occ;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  spmm_group_kernel<G, T, Q, Sc><<<(int)blocks, 256, 0, s>>>(ptr, idx, val, items, n_items, X, ldx, w, shift, Y,
+                                                             ldy, scratch);
+}
+
+// the group kernel for one column chunk; false: not applicable (unaligned rows)
+template <typename Sc>
+static bool spmm_group(const int* ptr, const int* idx, const Sc* val, const int* items, int n_items, const Sc* X,
+                       long long ldx, int w, Sc* Y, long long ldy, Sc* scratch, cudaStream_t s) {
+  static const char* fam = getenv("LR_SPMM_KERNEL");
+  if (fam && fam[0] == 'i') return false;  // "items": the round-1 kernel
+  constexpr int VE = 16 / (int)sizeof(Sc);
+  if (!aligned_bytes(X, 16) || (ldx * (long long)sizeof(Sc)) % 16 != 0) return false;
+  // rows share one offset from their 128-byte line only if the row stride is whole lines
+  const int shift = ((ldx * (long long)sizeof(Sc)) % 128 == 0)
+                        ? (int)((reinterpret_cast<uintptr_t>(X) & 127u) / sizeof(Sc)) : 0;
+  int G, T;
+  if (!pick_group((w + shift + VE - 1) / VE, G, T)) return false;
+#define LR_SPG(g, t)                                                                                         \
+  if (G == g && T == t) {                                                                                    \
+    launch_spmm_group_t<g, t, Sc>(ptr, idx, val, items, n_items, X, ldx, w, shift, Y, ldy, scratch, s);     \
+    return true;                                                                                             \
+  }
+  LR_SPG(4, 1) LR_SPG(4, 2) LR_SPG(4, 3) LR_SPG(4, 4) LR_SPG(8, 1) LR_SPG(8, 2) LR_SPG(8, 3) LR_SPG(8, 4)
+  LR_SPG(16, 1) LR_SPG(16, 2) LR_SPG(16, 3) LR_SPG(16, 4) LR_SPG(32, 1) LR_SPG(32, 2) LR_SPG(32, 3)
+  LR_SPG(32, 4)
+#undef LR_SPG
+  return false;
+}
+
 // Column-chunked SpMM over a row-compressed pattern, w >= 2 (shared by the
 // fp64 and fp32 entry points)
 template <typename Sc>
@@ -780,7 +1182,9 @@ static int spmm_cols(const int* ptr, const int* idx, const Sc* val, const int* i
     const bool v2 = (ldx % 2 == 0) && (ldy % 2 == 0) && aligned_bytes(Xc, kVecBytes) &&
                     aligned_bytes(Yc, kVecBytes) &&
                     (scratch == nullptr || (aligned_bytes(scratch, kVecBytes) && cw % 2 == 0));
-    if (v2)
+    if (spmm_group<Sc>(ptr, idx, val, items, n_items, Xc, ldx, cw, Yc, ldy, scratch, s))
+      ;
+    else if (v2)
       dispatch_spmm<true, Sc>(ptr, idx, val, items, n_items, Xc, ldx, cw, Yc, ldy, scratch, s);
     else
       dispatch_spmm<false, Sc>(ptr, idx, val, items, n_items, Xc, ldx, cw, Yc, ldy, scratch, s);
@@ -827,7 +1231,12 @@ static int launch_flat_t(bool fused, const int* ptr, const int* idx, long long n
     svt_flat_kernel<G, T, kFlatK, Q, false><<<(int)blocks, kFlatWarps * 32, 0, s>>>(
         ptr, idx, nnz, m, tile_row, n_tiles, U, ldu, S, V, ldv, r, x, m_vals, y_csr, y_csc, inv_perm, step, apply,
         partial);
-  LR_CHECK_LAUNCH();
+  ::lr::count_launches(1);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    set_error("svt_flat launch: %s", cudaGetErrorString(err));
+    return -LR_ERR_CUDA;
+  }
   return (int)blocks;  // > 0: blocks launched (partials written)
 }
 
@@ -862,6 +1271,44 @@ static int launch_flat(bool fused, const int* ptr, const int* idx, long long nnz
 #undef LR_FLAT
   set_error("svt: no flat kernel instance for G=%d T=%d Q=%d", G, T, Q);
   return -LR_ERR_ARG;
+}
+
+template <int G, int T>
+static int launch_svt_group2_t(bool fused, const int* ptr, const int* idx, const int* items, int n_items,
+                               const double* U, long long ldu, const double* S, const double* V, long long ldv,
+                               int r, double* x, const double* m_vals, double* y_csr, double* y_csc,
+                               const int* inv_perm, double step, int apply, double* partial, cudaStream_t s) {
+  static int occ[2] = {-1, -1};
+  int& o = occ[fused ? 1 : 0];
+  if (o < 0) {
+    // minimal shared memory carve-out: L1 keeps the gathered V rows
+    cudaFuncSetAttribute(svt_group2_kernel<G, T, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 10);
+    cudaFuncSetAttribute(svt_group2_kernel<G, T, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 10);
+    o = fused ? occupancy_blocks(reinterpret_cast<const void*>(svt_group2_kernel<G, T, true>))
+              : occupancy_blocks(reinterpret_cast<const void*>(svt_group2_kernel<G, T, false>));
+    if (o > kSvtBlocksPerSm) o = kSvtBlocksPerSm;  // the partial buffer holds sm_count * kSvtBlocksPerSm
+  }
+  constexpr int GROUPS = 32 / G;
+  const long long warps = ((long long)n_items + GROUPS - 1) / GROUPS;
+  long long blocks = (warps + 7) / 8;
+  const long long cap = (long long)sm_count() * o;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  if (fused)
+    svt_group2_kernel<G, T, true><<<(int)blocks, 256, 0, s>>>(ptr, idx, items, n_items, U, ldu, S, V, ldv, r, x,
+                                                               m_vals, y_csr, y_csc, inv_perm, step, apply,
+                                                               partial);
+  else
+    svt_group2_kernel<G, T, false><<<(int)blocks, 256, 0, s>>>(ptr, idx, items, n_items, U, ldu, S, V, ldv, r, x,
+                                                                m_vals, y_csr, y_csc, inv_perm, step, apply,
+                                                                partial);
+  ::lr::count_launches(1);
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    set_error("svt_group2 launch: %s", cudaGetErrorString(err));
+    return 0;
+  }
+  return (int)blocks;
 }
 
 }  // namespace lr
@@ -915,14 +1362,45 @@ static int launch_sddmm(bool fused, const int* ptr, const int* idx, int rows, co
                         int n_items, const double* U, long long ldu, const double* S,
                         const double* V, long long ldv, int r, double* x, const double* m_vals,
                         double* y_csr, double* y_csc, const int* inv_perm, double step, int apply,
-                        double* partial, cudaStream_t s) {
+                        double* partial, cudaStream_t s, int* nblocks = nullptr) {
   if (!items) n_items = rows;
   const int blocks = sm_count() * kSvtBlocksPerSm;
-  // kernel family: "batch" (default: coalesced per-entry finishing, any rank),
-  // "legacy" (round-1 warp / group kernels, r <= 1024); LR_SVT_GT="G,T,Q"
-  // overrides the batch kernel's lane mapping for experiments
+  if (nblocks) *nblocks = blocks;
+  // kernel family: "group2" (default for r <= 256 with 16-byte aligned V
+  // rows: line-aligned V gathers, U * S per item in registers), "batch"
+  // (coalesced per-entry finishing, any rank), "legacy" (round-1 warp /
+  // group kernels, r <= 1024); LR_SVT_GT="G,T,Q" overrides the batch
+  // kernel's lane mapping for experiments
   static const char* fam = getenv("LR_SVT_KERNEL");
   const bool legacy = fam && fam[0] == 'l';
+  const bool batch_only = fam && fam[0] == 'b';
+  // the flat kernel's lane map (G lanes x T column pairs per entry, pairs
+  // c = 2 (g + G t)) and reduction tree: every entry's value is bit-identical
+  // to lr_svt_step_flat_f64's (tests/test_gpu_kernels.py::
+  // test_sddmm_group_kernel_matches_flat)
+  const int pairs = (r + 1) / 2;
+  int G2 = 0, T2 = 2;
+  if (pairs <= 2) G2 = 1;
+  else if (pairs <= 4) G2 = 2;
+  else if (pairs <= 8) G2 = 4;
+  else if (pairs <= 16) G2 = 8;
+  else if (pairs <= 32) G2 = 16;
+  else if (pairs <= 64) G2 = 32;
+  else if (pairs <= 128) { G2 = 32; T2 = 4; }
+  if (!legacy && !batch_only && r >= 1 && G2 > 0 && (ldv % 2 == 0) && aligned16(V)) {
+    int nb = -1;
+#define LR_SG2(g, t)                                                                                          \
+  if (G2 == g && T2 == t)                                                                                     \
+    nb = launch_svt_group2_t<g, t>(fused, ptr, idx, items, n_items, U, ldu, S, V, ldv, r, x, m_vals, y_csr,   \
+                                   y_csc, inv_perm, step, apply, partial, s);
+    LR_SG2(1, 2) LR_SG2(2, 2) LR_SG2(4, 2) LR_SG2(8, 2) LR_SG2(16, 2) LR_SG2(32, 2) LR_SG2(32, 4)
+#undef LR_SG2
+    if (nb > 0) {
+      if (nblocks) *nblocks = nb;
+      return LR_OK;
+    }
+    if (nb == 0) return LR_ERR_CUDA;
+  }
   if (!legacy) {
     const int pairs = (r + 1) / 2;
     static const char* gt = getenv("LR_SVT_GT");
@@ -1035,12 +1513,13 @@ int lr_svt_step_f64(const int* ptr, const int* idx, int rows, const int* items, 
   const int blocks = sm_count() * kSvtBlocksPerSm;
   LR_REQUIRE(n_partial >= 2 * blocks, "svt_step: partial buffer too small (%d < %d)", n_partial,
              2 * blocks);
+  int launched = blocks;
   {
     int st = launch_sddmm(true, ptr, idx, rows, items, n_items, U, ldu, S, V, ldv, r, nullptr,
-                          m_vals, y_csr, y_csc, inv_perm, step, apply, partial, s);
+                          m_vals, y_csr, y_csc, inv_perm, step, apply, partial, s, &launched);
     if (st != LR_OK) return st;
   }
-  svt_finish_kernel<<<1, 32, 0, s>>>(partial, blocks, out2);
+  svt_finish_kernel<<<1, 32, 0, s>>>(partial, launched, out2);
   LR_CHECK_LAUNCH();
   return LR_OK;
 }

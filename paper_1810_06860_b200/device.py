@@ -75,7 +75,13 @@ def ld(t) -> int:
 
 
 def padded_ld(cols: int) -> int:
-    return max(2, (cols + 1) & ~1)
+    """Row stride (elements) of a new block: a power of two up to 8 columns,
+    else a multiple of 16, so every row starts on a 128-byte line (fp64; 64
+    bytes for fp32) and a gathered row of b bytes touches ceil(b / 128) lines
+    -- the sparse kernels are bound by L1 wavefronts, one per line touched."""
+    if cols <= 8:
+        return 2 if cols <= 2 else (4 if cols <= 4 else 8)
+    return (cols + 15) & ~15
 
 
 def empty(rows: int, cols: int) -> torch.Tensor:

@@ -16,7 +16,7 @@ reference are replaced by the native library:
                                                             (linalg.py:153-169)
   eig_svd   dsyrk + dsyevd + dgemm          -> DMMA syrk + syevd + DMMA gemm
                                                             (linalg.py:172-202)
-  oracle_svd dgesdd (dense, capped)         -> Gram + Jacobi, U re-orthonormalised
+  oracle_svd dgesdd (dense, capped)         -> Gram-preconditioned one-sided Jacobi (abs. accuracy)
             by CholeskyQR2 (orthonormal completion for null directions)
                                                             (linalg.py:205-221)
 
@@ -522,49 +522,96 @@ def eig_svd(A) -> SvdResult:
 
 # --------------------------------------------------------------- oracle_svd
 
+JACOBI_MAX_SWEEPS = 30
+# columns of the dense SVD with S <= DENSE_NULL_FLOOR * S[0] get an orthonormal
+# completion instead of B / S (1e-300: exact zeros only)
+DENSE_NULL_FLOOR = float(__import__("os").environ.get("LR_DENSE_NULL_FLOOR", "1e-300"))
+
+
 def _tall_dense_svd_dev(A):
-    """Descending SVD of tall A on the device: Gram + Jacobi for V and S,
-    U = A V / S re-orthonormalised by CholeskyQR2 (null directions get an
-    orthonormal completion from a seeded Gaussian block)."""
+    """Descending SVD of tall A (rows >= n) on the device, to dgesdd's
+    absolute accuracy (linalg.py:205-221): the Gram route (syrk + syevd)
+    gives V0 whose B = A V0 has nearly orthogonal columns; one-sided Jacobi
+    sweeps (lr_jacobi_sweep_f64, rotations accumulated into V) orthogonalise
+    B's columns to sqrt(rows) eps, S = their norms (error ~ eps s_max even for
+    null directions, where the Gram route alone stops at ~sqrt(eps) s_max),
+    U = B / S, null directions completed from a seeded Gaussian block and
+    re-orthonormalised by CholeskyQR2 (good columns barely move)."""
     rows, n = A.shape
+    st = _st()
     G = gram_dev(A)
     try:
-        V, d = sym_eig_dev(G, symmetrize=False)
+        V0, _d = sym_eig_dev(G, symmetrize=False)
     except NumericalError:
         _check_dev(A, "oracle_svd input")  # a non-finite input is the reference's ValueError
         raise
-    dh = device.to_host(d)[::-1].copy()  # descending
-    S = np.sqrt(np.maximum(dh, 0.0))
-    order = np.arange(n - 1, -1, -1)
-    Vd = device.empty(n, n)
-    oi = device.int_buffer(order)
-    _native.call("lr_scale_columns_f64", device.ptr(V), device.ld(V), n, device.ptr(oi), n, None, 0,
-                 device.ptr(Vd), device.ld(Vd), _st())
-    good = S > (S[0] * 1e-7 if S[0] > 0 else np.inf)
-    Ssafe = device.f64_buffer(np.where(good, S, 1.0))
-    B = device.empty(n, n)
-    _native.call("lr_scale_columns_f64", device.ptr(Vd), device.ld(Vd), n, None, n,
-                 device.ptr(Ssafe), 1, device.ptr(B), device.ld(B), _st())
-    U = matmul_dev(A, B)
+    Vd = device.empty(n, n)  # eigenvectors, descending
+    oi = device.int_buffer(np.arange(n - 1, -1, -1))
+    _native.call("lr_scale_columns_f64", device.ptr(V0), device.ld(V0), n, device.ptr(oi), n, None, 0,
+                 device.ptr(Vd), device.ld(Vd), st)
+    # the preconditioner must be orthogonal to working precision: inverse
+    # iteration leaves eigenvectors of small-gap eigenvalue pairs only
+    # eps / gap orthogonal (~1e-8 at a 1e-8 gap); two CholeskyQR passes on the
+    # n x n block fix that (the rotations below preserve orthogonality)
+    for _ in range(2):
+        info, Qv, _dv = _cholqr_pass(Vd)
+        if info:
+            break
+        Vd = Qv
+    B = matmul_dev(A, Vd)
+    Bt = device.empty(n, rows)
+    _native.call("lr_transpose_f64", device.ptr(B), device.ld(B), rows, n, device.ptr(Bt), device.ld(Bt), st)
+    Vt = device.empty(n, n)
+    _native.call("lr_transpose_f64", device.ptr(Vd), device.ld(Vd), n, n, device.ptr(Vt), device.ld(Vt), st)
+    off = device.vector(1)
+    tol = float(np.sqrt(rows)) * 2.0 * _U_ROUND
+    for _ in range(JACOBI_MAX_SWEEPS):
+        _native.call("lr_jacobi_sweep_f64", n, rows, device.ptr(Bt), device.ld(Bt), device.ptr(Vt), device.ld(Vt),
+                     tol, device.ptr(off), st)
+        if float(device.to_host(off)[0]) == 0.0:
+            break
+    else:
+        raise NumericalError("dense SVD: one-sided Jacobi did not converge")
+    norms = device.vector(n)
+    _native.call("lr_row_norms_f64", device.ptr(Bt), device.ld(Bt), n, rows, device.ptr(norms), st)
+    Sj = device.to_host(norms)
+    perm = np.argsort(-Sj, kind="stable")
+    S = Sj[perm]
+    # U = B / S for every column with a nonzero norm: Jacobi leaves the
+    # columns orthogonal RELATIVE to their norms, so even noise-level ones
+    # normalise to orthonormal vectors inside span(A) -- as dgesdd's U lies in
+    # span(Q) of A's QR -- and only exactly-zero columns need a completion
+    floor = S[0] * DENSE_NULL_FLOOR if S[0] > 0 else np.inf
+    good = S > floor
+    # U = B[:, perm] / S (good columns), V = Vt^T[:, perm]
+    _native.call("lr_transpose_f64", device.ptr(Bt), device.ld(Bt), n, rows, device.ptr(B), device.ld(B), st)
+    pi = device.int_buffer(perm)
+    Ssafe = device.f64_buffer(np.where(Sj > floor, Sj, 1.0))  # floor: S[0] * DENSE_NULL_FLOOR
+    U = device.empty(rows, n)
+    _native.call("lr_scale_columns_f64", device.ptr(B), device.ld(B), rows, device.ptr(pi), n, device.ptr(Ssafe), 1,
+                 device.ptr(U), device.ld(U), st)
+    _native.call("lr_transpose_f64", device.ptr(Vt), device.ld(Vt), n, n, device.ptr(Vd), device.ld(Vd), st)
+    V = device.empty(n, n)
+    _native.call("lr_scale_columns_f64", device.ptr(Vd), device.ld(Vd), n, device.ptr(pi), n, None, 0,
+                 device.ptr(V), device.ld(V), st)
     nbad = int((~good).sum())
     if nbad:
         from .rng import gaussian_matrix_device
 
         Z = gaussian_matrix_device(0x5EED, rows, nbad)
-        first_bad = n - nbad
-        _native.call("lr_copy2d_f64", device.ptr(Z), device.ld(Z), device.ptr(U[:, first_bad:]), device.ld(U),
-                     rows, nbad, 0, _st())
-    # re-orthonormalise (columns keep their order; good columns barely move)
-    for _ in range(2):
-        info, Qn, _d = _cholqr_pass(U)
-        if info:
-            shift = 11.0 * (rows * n + n * (n + 1)) * _U_ROUND * float(n)
-            info, Qn, _d = _cholqr_pass(U, shift)
+        _native.call("lr_copy2d_f64", device.ptr(Z), device.ld(Z), device.ptr(U[:, n - nbad:]), device.ld(U),
+                     rows, nbad, 0, st)
+        # re-orthonormalise (columns keep their order; good columns barely move)
+        for _ in range(2):
+            info, Qn, _dd = _cholqr_pass(U)
             if info:
-                raise NumericalError("dense SVD: could not orthonormalize the left factor")
-        U = Qn
-    _native.call("lr_fix_signs_f64", device.ptr(Vd), device.ld(Vd), n, n, device.ptr(U), device.ld(U), rows, _st())
-    return U, S, Vd
+                shift = 11.0 * (rows * n + n * (n + 1)) * _U_ROUND * float(n)
+                info, Qn, _dd = _cholqr_pass(U, shift)
+                if info:
+                    raise NumericalError("dense SVD: could not orthonormalize the left factor")
+            U = Qn
+    _native.call("lr_fix_signs_f64", device.ptr(V), device.ld(V), n, n, device.ptr(U), device.ld(U), rows, st)
+    return U, S, V
 
 
 def oracle_svd_dev(A):

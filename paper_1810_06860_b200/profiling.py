@@ -56,6 +56,18 @@ MODELS = {"lr_spmm_f64": ("hbm", spmm_model), "lr_spmm_f32": ("hbm", spmm_model)
           "lr_gemm_f64": ("tensor", gemm_model)}
 
 
+def gather_bytes(name, meta):
+    """Diagnostic L2-gather bytes: one dense row of w (SpMM) or r
+    (SVT step) values per stored entry."""
+    if meta is None:
+        return 0
+    if name in ("lr_spmm_f64", "lr_spmm_f32"):
+        return meta.get("bytes_per_value", 8) * meta["nnz"] * meta["w"]
+    if name in ("lr_svt_step_f64", "lr_svt_step_flat_f64"):
+        return 8 * meta["nnz"] * meta["r"]
+    return 0
+
+
 class Profiler:
     """Records a (start, end) CUDA event pair around every native call."""
 
@@ -73,7 +85,8 @@ class Profiler:
 
     def summary(self):
         torch.cuda.synchronize()
-        out = defaultdict(lambda: {"calls": 0, "ms": 0.0, "bytes": 0.0, "flops": 0.0, "modeled_ms": 0.0})
+        out = defaultdict(lambda: {"calls": 0, "ms": 0.0, "bytes": 0.0, "flops": 0.0, "modeled_ms": 0.0,
+                                   "gather": 0.0})
         for name, meta, e0, e1 in self.records:
             ms = e0.elapsed_time(e1)
             d = out[name]
@@ -83,5 +96,6 @@ class Profiler:
                 b, f = MODELS[name][1](meta)
                 d["bytes"] += b
                 d["flops"] += f
+                d["gather"] += gather_bytes(name, meta)
                 d["modeled_ms"] += ms
         return dict(out)

@@ -113,11 +113,75 @@ def _uniform_slice(seed: int, start: int, out: np.ndarray) -> None:
     gen.random(out=out)
 
 
+# The C pieces of the draw (csrc/lr_host_rng.c): Philox uniforms and the
+# Box-Muller pairing with libm cos/sin; np.log stays numpy's.  Used only after
+# a bit-for-bit self-check against the all-numpy draw on this host (numpy's
+# float64 cos/sin are libm's here, its log is its own SIMD kernel).
+_C_DRAW = None
+
+
+def _c_draw_lib():
+    global _C_DRAW
+    if _C_DRAW is None:
+        _C_DRAW = False
+        try:
+            from . import _native
+
+            lib = _native.load()
+            _C_DRAW = lib
+            ok = all(np.array_equal(_normals_c(lib, s, r, c), _normals_numpy(s, r, c))
+                     for s, r, c in ((3, 7, 5), (2 ** 62 + 11, 1001, 3), (12345, 4099, 37)))
+            if not ok:
+                _C_DRAW = False
+        except Exception:
+            _C_DRAW = False
+    return _C_DRAW
+
+
+def _normals_c(lib, seed: int, rows: int, cols: int, out: np.ndarray = None, pool=None) -> np.ndarray:
+    count = rows * cols
+    npairs = (count + 1) // 2
+    u1 = np.empty(npairs)
+    u2 = np.empty(npairs)
+    direct = out is not None and out.size >= 2 * npairs
+    dst = out.reshape(-1) if direct else np.empty(2 * npairs)
+    nt = 1 if pool is None else max(1, min(pool._max_workers, npairs // (1 << 15)))
+    pc = [(npairs * t) // nt for t in range(nt + 1)]
+    seed = int(seed) & ((1 << 64) - 1)
+
+    def part(t):
+        a, b = pc[t], pc[t + 1]
+        if a == b:
+            return
+        x1, x2 = u1[a:b], u2[a:b]
+        lib.lr_host_uniforms(seed, a, b - a, x1.ctypes.data)
+        lib.lr_host_uniforms(seed, npairs + a, b - a, x2.ctypes.data)
+        np.subtract(1.0, x1, out=x1)
+        np.log(x1, out=x1)
+        lib.lr_host_box_muller(x1.ctypes.data, x2.ctypes.data, b - a, dst[2 * a:2 * b].ctypes.data)
+
+    if nt == 1:
+        part(0)
+    else:
+        list(pool.map(part, range(nt)))
+    if out is not None and not direct:
+        out.reshape(-1)[:count] = dst[:count]
+        return out.reshape(-1)[:count]
+    return dst[:count]
+
+
+def _normals_numpy(seed: int, rows: int, cols: int) -> np.ndarray:
+    return RngState(seed).normal_pairs(rows * cols)
+
+
 def normals_column_major(seed: int, rows: int, cols: int, out: np.ndarray = None) -> np.ndarray:
     """Omega = gaussian_matrix(RngState(seed), rows, cols) in COLUMN-major
     order (the draw order: column c is out[c*rows:(c+1)*rows]), bit-identical
     to the one-thread draw, computed by the thread pool into `out`."""
     _check_shape(rows, cols)
+    lib = _c_draw_lib()
+    if lib:
+        return _normals_c(lib, seed, rows, cols, out, _pool())
     count = rows * cols
     npairs = (count + 1) // 2
     u = np.empty(2 * npairs)
@@ -157,6 +221,7 @@ def _pinned_normals(seed: int, rows: int, cols: int):
 
 
 _PREFETCH = {}
+PREFETCH_KEEP = 5  # draws kept (the SVT loop's speculative candidates + the exact one)
 
 
 def prefetch_normals(seed: int, rows: int, cols: int) -> None:
@@ -166,7 +231,7 @@ def prefetch_normals(seed: int, rows: int, cols: int) -> None:
     key = (int(seed), int(rows), int(cols))
     if key in _PREFETCH or rows < 1 or cols < 1:
         return
-    while len(_PREFETCH) >= 2:
+    while len(_PREFETCH) >= PREFETCH_KEEP:
         _PREFETCH.pop(next(iter(_PREFETCH)))
     import threading
     from concurrent.futures import Future

@@ -380,6 +380,46 @@ class SparseMatrix:
             self._csc_stale = False
         return self._dvals
 
+    def scaled_on_device(self, scale: float) -> "SparseMatrix":
+        """SparseMatrix(rows, cols, indptr, indices, scale * data) sharing this
+        matrix's pattern, with the product formed on the device from this
+        matrix's two resident value copies (one IEEE multiply per entry: the
+        same bits as the host product; completion.py:335's Y = c delta P(M)).
+        The host copy of the new values is materialised only on access.  The
+        constructor's finiteness check holds iff scale * max|data| is finite
+        (rounding is monotone), so it is decided from one cached scalar."""
+        scale = float(scale)
+        if self._host_stale:
+            _ = self.data
+        mx = getattr(self, "_maxabs", None)
+        if mx is None:
+            mx = float(np.max(np.abs(self._data))) if self.nnz else 0.0
+            self._maxabs = mx
+        if not (np.isfinite(scale) and np.isfinite(scale * mx)):
+            raise DataError("matrix values must be finite")
+        out = SparseMatrix.__new__(SparseMatrix)
+        out.rows, out.cols = self.rows, self.cols
+        out.indptr, out.indices = self.indptr, self.indices
+        out._data = np.empty(self.nnz)
+        out._tperm = out._t_indptr = out._t_indices = out._coo_rows = None
+        out._pattern = None
+        out._host_stale = False
+        out._csc_stale = False
+        self.pattern()
+        out.share_pattern(self)
+        src = self.device_values()
+        sv = device.f64_buffer(np.array([scale]))
+        dst = []
+        for v in src:
+            d = device.vector(self.nnz)
+            if self.nnz:
+                _native.call("lr_scale_columns_f64", device.ptr(v), 1, self.nnz, None, 1, device.ptr(sv), 0,
+                             device.ptr(d), 1, device.stream())
+            dst.append(d)
+        out._dvals = (dst[0], dst[1])
+        out._host_stale = True
+        return out
+
     def device_values_csr(self):
         """The CSR device value vector (no CSC refresh)."""
         if self._dvals is None:
@@ -478,10 +518,11 @@ def spmm_t(A: SparseMatrix, X):
     return out if _is_torch(X) else device.to_host(out)
 
 
-# SDDMM / fused SVT step kernel family: "flat" (tiles of consecutive CSR
-# slots, one warp each; lr_*_flat_f64) or "items" (a warp per row / row chunk;
-# lr_sddmm_f64 / lr_svt_step_f64)
-SVT_KERNEL = "flat"
+# SDDMM / fused SVT step kernel family: "items" (default: a G-lane group per
+# row / row chunk, line-aligned V gathers, U * S of the row in registers;
+# lr_sddmm_f64 / lr_svt_step_f64) or "flat" (tiles of consecutive CSR slots,
+# one warp each; lr_*_flat_f64)
+SVT_KERNEL = "items"
 
 
 def project_pattern_dev(U, S, V, pattern: SparseMatrix, out=None):

@@ -247,10 +247,11 @@ def test_sym_eig_matches_numpy(n):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,groups", [(40, [1, 1, 1, 2, 3, 3]), (300, None)])
+@pytest.mark.parametrize("n,groups", [(40, [1, 1, 1, 2, 3, 3]), (300, None), (660, "big")])
 def test_sym_eig_clusters(n, groups):
     """Repeated eigenvalues: the device cluster finder + MGS keep V orthonormal
-    (n = 300: 150 equal pairs, more clusters than the MGS grid)."""
+    (n = 300: 150 equal pairs, more clusters than the MGS grid; n = 660: one
+    600-fold cluster, the O(k^2) worst case of the one-CTA-per-cluster MGS)."""
     import ctypes
 
     import torch
@@ -262,6 +263,8 @@ def test_sym_eig_clusters(n, groups):
     Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
     if groups is None:
         d0 = np.repeat(np.arange(1.0, n // 2 + 1), 2)
+    elif groups == "big":
+        d0 = np.concatenate([np.full(600, 5.0), 10.0 + np.arange(n - 600)])
     else:
         d0 = np.concatenate([groups, 10.0 + np.arange(n - len(groups))])
     B = (Q * d0) @ Q.T
@@ -277,7 +280,7 @@ def test_sym_eig_clusters(n, groups):
     ncl = ctypes.c_int(-1)
     _native.call("lr_syevd_f64", n, device.ptr(A), device.ld(A), device.ptr(dd), device.ptr(VV), device.ld(VV),
                  device.ptr(work), ctypes.byref(ncl), device.stream())
-    expect = n // 2 if groups is None else 2
+    expect = n // 2 if groups is None else (1 if groups == "big" else 2)
     assert ncl.value == expect
 
 
@@ -349,14 +352,28 @@ def test_oracle_svd_matches_lapack(golden):
     rw = oracle_svd(golden["eig_A"].T)  # wide input
     assert rel(rw.S, golden["osvd_S"]) <= 1e-12
     assert rel((rw.U * rw.S) @ rw.V.T, golden["eig_A"].T) <= 1e-12
-    # rank-deficient input still gets an orthonormal U
+    # rank-deficient input: orthonormal U, and every singular value -- the null
+    # one included -- to dgesdd's absolute accuracy (the Gram route alone
+    # resolves it only to ~sqrt(eps) * s_max)
     X = np.random.default_rng(4).standard_normal((50, 6))
     X[:, 5] = X[:, 1]
     r = oracle_svd(X)
+    S_ref = np.linalg.svd(X, compute_uv=False)
     assert rel(r.U.T @ r.U, np.eye(6)) <= 1e-12
-    # Gram route: the null singular value is resolved only to ~sqrt(eps)*s_max
-    assert r.S[-1] <= 1e-7 * r.S[0]
-    assert rel((r.U * r.S) @ r.V.T, X) <= 1e-7
+    assert np.max(np.abs(r.S - S_ref)) <= 1e-12 * S_ref[0]
+    assert r.S[-1] <= 1e-14 * r.S[0]
+    assert rel((r.U * r.S) @ r.V.T, X) <= 1e-13
+    # graded spectrum down to 1e-14 s_max, tall and wide
+    rng = np.random.default_rng(9)
+    Uq, _ = np.linalg.qr(rng.standard_normal((400, 30)))
+    Wq, _ = np.linalg.qr(rng.standard_normal((30, 30)))
+    Xg = (Uq * np.logspace(0, -14, 30)) @ Wq.T
+    for M in (Xg, Xg.T):
+        r = oracle_svd(M)
+        S_ref = np.linalg.svd(M, compute_uv=False)
+        assert np.max(np.abs(r.S - S_ref)) <= 1e-13 * S_ref[0]
+        assert rel(r.U.T @ r.U, np.eye(30)) <= 1e-12 and rel(r.V.T @ r.V, np.eye(30)) <= 1e-12
+        assert rel((r.U * r.S) @ r.V.T, M) <= 1e-13
 
 
 def test_device_gaussian_matches_host():
@@ -446,12 +463,66 @@ def test_convert_roundtrip_and_rounding():
     np.testing.assert_array_equal(back, x.astype(np.float32).astype(np.float64))
 
 
+@pytest.mark.parametrize("r", [1, 3, 5, 9, 17, 24, 33, 48, 65, 84, 130, 200, 256])
+def test_sddmm_group_kernel_matches_flat(r):
+    """The line-aligned group kernel behind lr_sddmm_f64 / lr_svt_step_f64 (the
+    product default) uses the flat kernel's lane map and reduction tree: every
+    sampled entry, and so every updated value of Y, is bit-identical to
+    lr_sddmm_flat_f64 / lr_svt_step_flat_f64 -- on rows split into items, empty
+    rows and a Zipf-like long row."""
+    import torch
+
+    from paper_1810_06860_b200 import _native, device
+    from paper_1810_06860_b200.sparse import SparseMatrix
+
+    m, n = 1500, 900
+    i, j, v = rand_pattern(m, n, 60000, seed=700 + r, long_rows=2)
+    A = SparseMatrix.from_coo(m, n, i, j, v)
+    dp = A.pattern()
+    rng = np.random.default_rng(r)
+    U = device.to_device(rng.standard_normal((m, r)))
+    V = device.to_device(rng.standard_normal((n, r)))
+    S = device.f64_buffer(rng.random(r) + 0.5)
+    st = device.stream()
+    x_flat, x_grp = device.vector(A.nnz), device.vector(A.nnz)
+    _native.call("lr_sddmm_flat_f64", device.ptr(dp.csr.ptr), device.ptr(dp.csr.idx), m, A.nnz,
+                 device.ptr(dp.tile_rows()), device.ptr(U), device.ld(U), device.ptr(S), device.ptr(V), device.ld(V),
+                 r, device.ptr(x_flat), st)
+    _native.call("lr_sddmm_f64", device.ptr(dp.csr.ptr), device.ptr(dp.csr.idx), m, device.ptr(dp.csr.items),
+                 dp.csr.n_items, device.ptr(U), device.ld(U), device.ptr(S), device.ptr(V), device.ld(V), r,
+                 device.ptr(x_grp), st)
+    assert torch.equal(x_flat, x_grp)
+    ref = np.einsum("er,er->e", device.to_host(U)[A.coo_rows()] * device.to_host(S), device.to_host(V)[A.indices])
+    assert rel(device.to_host(x_grp), ref) <= 1e-14
+    # fused step through both entry points: identical Y
+    m_vals = A.device_values()[0]
+    ys = []
+    for name in ("lr_svt_step_flat_f64", "lr_svt_step_f64"):
+        y = m_vals.clone()
+        npart = int(_native.load().lr_svt_flat_partials() if "flat" in name else _native.load().lr_svt_step_partials())
+        part, out2 = device.vector(npart + 8), device.vector(2)
+        if "flat" in name:
+            _native.call(name, device.ptr(dp.csr.ptr), device.ptr(dp.csr.idx), m, A.nnz, device.ptr(dp.tile_rows()),
+                         device.ptr(U), device.ld(U), device.ptr(S), device.ptr(V), device.ld(V), r,
+                         device.ptr(m_vals), device.ptr(y), None, device.ptr(dp.inv_perm), 0.37, 1, device.ptr(part),
+                         npart, device.ptr(out2), st)
+        else:
+            _native.call(name, device.ptr(dp.csr.ptr), device.ptr(dp.csr.idx), m, device.ptr(dp.csr.items),
+                         dp.csr.n_items, device.ptr(U), device.ld(U), device.ptr(S), device.ptr(V), device.ld(V), r,
+                         device.ptr(m_vals), device.ptr(y), None, device.ptr(dp.inv_perm), 0.37, 1, device.ptr(part),
+                         npart, device.ptr(out2), st)
+        ys.append((y, float(np.sqrt(device.to_host(out2)[0]))))
+    assert torch.equal(ys[0][0], ys[1][0])
+    assert abs(ys[0][1] - ys[1][1]) <= 1e-13 * ys[0][1]
+
+
 @pytest.mark.parametrize("m,n,nnz,long_rows,empty_tail,r", [
     (300, 200, 4000, 0, 0, 1), (300, 200, 4000, 2, 0, 5), (1000, 700, 30000, 3, 40, 17),
     (5000, 3000, 200000, 1, 0, 48), (700, 600, 50000, 0, 100, 84), (400, 900, 60000, 2, 0, 300),
     (2000, 1500, 100000, 0, 0, 1100)])
 def test_svt_step_flat_matches_oracle_and_refreshes_csc(m, n, nnz, long_rows, empty_tail, r):
-    """The flat fused SVT step (lr_svt_step_flat_f64, the product default):
+    """The fused SVT step of the product (DeviceEngine.step -> lr_svt_step_f64,
+    the line-aligned group kernel; the flat kernel is bit-identical to it):
     residual and updated values against a numpy restatement of
     completion.py:373-386, the CSC copy refreshed on demand (lr_gather_f64)
     against the updated CSR values through the reference's stable argsort,

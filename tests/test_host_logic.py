@@ -173,3 +173,24 @@ def test_threaded_gaussian_is_bit_exact(rows, cols, seed):
     st2 = R.RngState(seed)
     R.gaussian_matrix(st2, rows, cols)
     assert st.position == st2.position and np.array_equal(st.uniform(7), st2.uniform(7))
+
+
+@pytest.mark.parametrize("rows,cols,seed", [(1, 1, 0), (7, 3, 5), (26744, 55, 2**62 + 9), (50000, 110, 123)])
+def test_c_uniforms_and_box_muller_are_bit_exact(rows, cols, seed):
+    """The C pieces of the host draw (csrc/lr_host_rng.c: Philox uniforms,
+    Box-Muller with libm cos/sin; numpy's own log in between) reproduce the
+    reference's all-numpy draw (rng.py:38-55) bit for bit on this host, and the
+    library is the producer the parity Omega uses here."""
+    from paper_1810_06860_b200 import _native
+    from paper_1810_06860_b200 import rng as R
+
+    if not __import__("os").path.exists(_native.LIB_PATH):
+        pytest.fail(f"native library not built: {_native.LIB_PATH} (run make)")
+    lib = R._c_draw_lib()
+    assert lib, "C draw failed its self-check against numpy on this host"
+    ref = R.RngState(seed).normal_pairs(rows * cols)
+    assert np.array_equal(R._normals_c(lib, seed, rows, cols), ref)
+    assert np.array_equal(R._normals_c(lib, seed, rows, cols, pool=R._pool()), ref)
+    u = np.empty(11)
+    lib.lr_host_uniforms(seed & ((1 << 64) - 1), 5, 11, u.ctypes.data)
+    assert np.array_equal(u, R.RngState(seed).uniform(16)[5:])

@@ -30,6 +30,22 @@ class TL(profiling.Profiler):
         return st
 
 
+from paper_1810_06860_b200 import rng as _rng  # noqa: E402
+
+_TN = []
+_take = _rng.take_normals
+
+
+def _timed_take(seed, rows, cols):
+    hit = (int(seed), int(rows), int(cols)) in _rng._PREFETCH
+    t0 = time.perf_counter()
+    out = _take(seed, rows, cols)
+    _TN.append((time.perf_counter() - t0, hit))
+    return out
+
+
+_rng.take_normals = _timed_take
+
 o4 = workloads.cfg4()
 obs = ObservationSet(o4.m, o4.n, o4.rows, o4.cols, o4.values, o4.split)
 params = bench.cfg4_params()
@@ -56,6 +72,10 @@ if mode == "cprofile":
     pstats.Stats(pr).sort_stats("cumtime").print_stats(40)
     sys.exit(0)
 
+_TN.clear()
+t0 = time.perf_counter()
+_rng.normals_column_major(12345, o4.n, 55)
+print(f"one cfg4-sized host draw (26744 x 55): {1e3 * (time.perf_counter() - t0):.2f} ms")
 tl = TL()
 _native.PROFILER = tl
 base = torch.cuda.Event(enable_timing=True)
@@ -91,6 +111,9 @@ for name, (c, t) in sorted(gsum.items(), key=lambda kv: -kv[1][1]):
 print("busy by call (ms):")
 for name, t in sorted(per.items(), key=lambda kv: -kv[1]):
     print(f"  {name:28s} {t:9.2f}")
+print(f"take_normals: {len(_TN)} calls, {sum(1 for t in _TN if t[1])} prefetched, waited "
+      f"{1e3 * sum(t[0] for t in _TN):.1f} ms total, {1e3 * sum(t[0] for t in _TN if not t[1]):.1f} ms on misses")
+print("trace (i, source, k, r, p):", [(t.iteration, t.svd_source[0], t.k, t.r, t.p) for t in res.trace])
 print("largest 15 gaps (ms, next call, gpu t, host t):")
 for g in sorted(gaps, reverse=True)[:15]:
     print(f"  {g[0]:7.3f} {g[1]:28s} gpu {g[2]:9.2f} host {g[3]:9.2f}")
