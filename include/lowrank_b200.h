@@ -217,6 +217,20 @@ int lr_fix_signs_f64(double* V, long long ldv, int rows_v, int cols, double* U, 
 int lr_scale_columns_f64(const double* V, long long ldv, int rows, const int* cols_idx, int ncols,
                          const double* S, int invert, double* B, long long ldb, void* stream);
 
+/* ----------------------------------------------------------- COO -> CSR */
+/* Coordinate triples (int64 rows/cols, count entries; with split != NULL only
+ * the entries tagged `tag`) -> CSR on the device: SparseMatrix.from_coo
+ * (sparse.py:84-104; ObservationSet.train_matrix, :259-328).  ptr (m+1),
+ * col_out / src_out (int32: column, source index, in CSR order), vals_out
+ * (values gathered in CSR order, may be NULL).  Bit-exact with the host
+ * lexsort.  status_host[0]: 0 ok, 1 a coordinate out of range, 2 a
+ * non-finite value; [1] the CSR slot of the first duplicate cell (-1: none);
+ * [2] nnz.  Synchronizes the stream (twice). */
+long long lr_coo_to_csr_workspace_ints(int m, long long count);
+int lr_coo_to_csr_i32(int m, int n, long long count, const long long* rows, const long long* cols,
+                      const unsigned char* split, int tag, const double* vals, int* ptr, int* col_out, int* src_out,
+                      double* vals_out, int* work, long long work_ints, int* status_host, void* stream);
+
 /* One-sided Jacobi sweep for the dense SVD fallback (oracle_svd ->
  * dgesdd, linalg.py:205-221): the columns of B are the rows of Bt (n x m),
  * the columns of V the rows of Vt (n x n).  Every column pair (one
@@ -244,6 +258,11 @@ int lr_gaussian_f64(unsigned long long seed, int rows, int cols, double* omega, 
  * z[2i+1] = ... sin(...), logs[i] = log(1 - u[i]) computed by numpy. */
 void lr_host_uniforms(unsigned long long seed, long long start, long long count, double* out);
 void lr_host_box_muller(const double* logs, const double* u2, long long n, double* z);
+/* The same draw split for several widths at once (rng.Superset): cs[2j] =
+ * cos(2 pi u[j]), cs[2j+1] = sin(...) over a run of stream positions, and
+ * z[2i] = R[i] cs[2i], z[2i+1] = R[i] cs[2i+1] with R[i] = sqrt(-2 log(1 - u[i])). */
+void lr_host_cossin(const double* u, long long n, double* cs);
+void lr_host_bm_assemble(const double* R, const double* cs, long long n, double* z);
 
 /* ------------------------------------------------------------- utilities */
 int lr_copy2d_f64(const double* src, long long lds, double* dst, long long ldd, long long rows,

@@ -58,3 +58,23 @@ void lr_host_box_muller(const double* logs, const double* u2, long long n, doubl
     z[2 * i + 1] = radius * sin(angle);
   }
 }
+
+/* cs[2j] = cos(2 pi u[j]), cs[2j+1] = sin(2 pi u[j]): the angle halves of
+ * Box-Muller for a run of stream positions (shared by several draw widths). */
+void lr_host_cossin(const double* u, long long n, double* cs) {
+  const double two_pi = 2.0 * 3.141592653589793;
+  for (long long j = 0; j < n; ++j) {
+    const double angle = two_pi * u[j];
+    cs[2 * j] = cos(angle);
+    cs[2 * j + 1] = sin(angle);
+  }
+}
+
+/* z[2i] = R[i] * cs[2i], z[2i+1] = R[i] * cs[2i+1] (R[i] = sqrt(-2 log(1 - u[i])))
+ * -- numpy's radius * cos(angle), radius * sin(angle). */
+void lr_host_bm_assemble(const double* R, const double* cs, long long n, double* z) {
+  for (long long i = 0; i < n; ++i) {
+    z[2 * i] = R[i] * cs[2 * i];
+    z[2 * i + 1] = R[i] * cs[2 * i + 1];
+  }
+}

@@ -25,6 +25,26 @@ _READY = False
 _DEVICES = {}
 
 
+def cuda_ready() -> bool:
+    """A CUDA device and the native library are present (the device paths
+    of input preparation apply)."""
+    if _READY:
+        return True
+    try:
+        require_cuda()
+        return True
+    except (RuntimeError, ImportError):
+        return False
+
+
+def upload_async_i64(a) -> torch.Tensor:
+    """int64 host array -> device tensor, asynchronous when the host array is
+    page-locked (stream-ordered on the current stream)."""
+    h = np.ascontiguousarray(a, dtype=np.int64)
+    TRAFFIC["h2d"] += h.nbytes
+    return torch.from_numpy(h).to(require_cuda(), non_blocking=True)
+
+
 def require_cuda() -> torch.device:
     """The current CUDA device; raises without one (no CPU fallback).  The
     availability check and the library load run once per process."""

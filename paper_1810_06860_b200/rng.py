@@ -240,7 +240,8 @@ def prefetch_normals(seed: int, rows: int, cols: int) -> None:
 
     def run():
         try:
-            fut.set_result(_pinned_normals(*key))
+            sup = _superset_for(*key)
+            fut.set_result(_pinned_from_superset(sup, key[2]) if sup is not None else _pinned_normals(*key))
         except BaseException as exc:  # pragma: no cover - surfaced by take_normals
             fut.set_exception(exc)
 
@@ -248,12 +249,134 @@ def prefetch_normals(seed: int, rows: int, cols: int) -> None:
     _PREFETCH[key] = fut
 
 
+class Superset:
+    """One seed's draws for every width in [w_lo, w_hi] at ~the cost of one:
+    Box-Muller pairs uniform i with uniform P + i (P = ceil(rows w / 2)), so
+    the radii R[i] (uniforms [0, P_hi)) and the cos / sin of the uniforms at
+    stream positions [P_lo, 2 P_hi) serve every width; a width's normals are
+    then z[2i] = R[i] cos(2 pi u[P + i]), z[2i+1] = R[i] sin(...) -- the same
+    IEEE operations as the one-width draw, so bit-identical to it
+    (tests/test_host_logic.py::test_superset_draw_is_bit_exact).  The SVT
+    loop builds one at the top of each iteration for the next iteration's
+    plausible ranks, while the GPU runs the current inner SVD."""
+
+    def __init__(self, lib, seed: int, rows: int, w_lo: int, w_hi: int, pool=None):
+        self.lib, self.seed, self.rows, self.w_lo, self.w_hi = lib, int(seed), int(rows), int(w_lo), int(w_hi)
+        self.p_lo = (rows * w_lo + 1) // 2
+        self.p_hi = (rows * w_hi + 1) // 2
+        seed64 = self.seed & ((1 << 64) - 1)
+        self.R = np.empty(self.p_hi)
+        na = 2 * self.p_hi - self.p_lo
+        self.cs = np.empty(2 * na)
+        ua = np.empty(na)
+        nt = 1 if pool is None else max(1, min(pool._max_workers, self.p_hi // (1 << 15)))
+
+        def part(t):
+            a, b = (self.p_hi * t) // nt, (self.p_hi * (t + 1)) // nt
+            if b > a:
+                x = self.R[a:b]
+                lib.lr_host_uniforms(seed64, a, b - a, x.ctypes.data)
+                np.subtract(1.0, x, out=x)
+                np.log(x, out=x)
+                np.multiply(-2.0, x, out=x)
+                np.sqrt(x, out=x)
+            a, b = (na * t) // nt, (na * (t + 1)) // nt
+            if b > a:
+                y = ua[a:b]
+                lib.lr_host_uniforms(seed64, self.p_lo + a, b - a, y.ctypes.data)
+                lib.lr_host_cossin(y.ctypes.data, b - a, self.cs[2 * a:2 * b].ctypes.data)
+
+        if nt == 1:
+            part(0)
+        else:
+            list(pool.map(part, range(nt)))
+
+    def covers(self, rows: int, cols: int) -> bool:
+        return int(rows) == self.rows and self.w_lo <= int(cols) <= self.w_hi
+
+    def normals(self, cols: int, out: np.ndarray, pool=None) -> np.ndarray:
+        """Column-major Omega(seed, rows, cols) into out (>= 2 P entries)."""
+        P = (self.rows * int(cols) + 1) // 2
+        off = P - self.p_lo
+        z = out.reshape(-1)
+        nt = 1 if pool is None else max(1, min(pool._max_workers, P // (1 << 16)))
+        cuts = [(P * t) // nt for t in range(nt + 1)]
+
+        def part(t):
+            a, b = cuts[t], cuts[t + 1]
+            if b > a:
+                self.lib.lr_host_bm_assemble(self.R[a:b].ctypes.data, self.cs[2 * (off + a):2 * (off + b)].ctypes.data,
+                                             b - a, z[2 * a:2 * b].ctypes.data)
+
+        if nt == 1:
+            part(0)
+        else:
+            list(pool.map(part, range(nt)))
+        return z[: self.rows * int(cols)]
+
+
+_SUPERSETS = {}  # seed -> Future[Superset]
+
+
+def prefetch_superset(seed: int, rows: int, w_lo: int, w_hi: int) -> None:
+    """Start a Superset draw for seed over widths [w_lo, w_hi] in the
+    background (at most two seeds kept)."""
+    lib = _c_draw_lib()
+    if not lib or rows < 1 or w_lo < 1 or w_hi < w_lo:
+        return
+    key = int(seed)
+    old = _SUPERSETS.get(key)
+    if old is not None and old[0] == (int(rows), int(w_lo), int(w_hi)):
+        return
+    while len(_SUPERSETS) >= 2:
+        _SUPERSETS.pop(next(iter(_SUPERSETS)))
+    import threading
+    from concurrent.futures import Future
+
+    fut = Future()
+
+    def run():
+        try:
+            fut.set_result(Superset(lib, seed, rows, w_lo, w_hi, _pool()))
+        except BaseException as exc:  # pragma: no cover - surfaced on use
+            fut.set_exception(exc)
+
+    threading.Thread(target=run, daemon=True, name="lr-omega-superset").start()
+    _SUPERSETS[key] = ((int(rows), int(w_lo), int(w_hi)), fut)
+
+
+def _superset_for(seed: int, rows: int, cols: int):
+    ent = _SUPERSETS.get(int(seed))
+    if ent is None:
+        return None
+    (r, lo, hi), fut = ent
+    if r != int(rows) or not lo <= int(cols) <= hi:
+        return None
+    try:
+        return fut.result()
+    except Exception:
+        return None
+
+
+def _pinned_from_superset(sup: Superset, cols: int):
+    import torch
+
+    count = sup.rows * int(cols)
+    host = torch.empty(count + (count & 1), dtype=torch.float64, pin_memory=True)
+    sup.normals(cols, host.numpy(), _pool())
+    return host
+
+
 def take_normals(seed: int, rows: int, cols: int):
     """Pinned column-major Omega(seed, rows, cols): the prefetched draw when
-    one matches, else drawn now."""
+    one matches, else assembled from a Superset covering the width, else
+    drawn now."""
     fut = _PREFETCH.pop((int(seed), int(rows), int(cols)), None)
     if fut is not None:
         return fut.result()
+    sup = _superset_for(seed, rows, cols)
+    if sup is not None:
+        return _pinned_from_superset(sup, cols)
     return _pinned_normals(seed, rows, cols)
 
 

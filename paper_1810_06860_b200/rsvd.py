@@ -226,7 +226,7 @@ def _spmm_t_prec(Y: SparseMatrix, X, precision: str):
 
 
 def project_and_solve(Y: SparseMatrix, Q, k: int, fb: _Fallback, precision: str = "fp64",
-                      download: bool = False):
+                      download: bool = False, T_pre=None):
     """B^T = Y^T Q, small SVD, lift: the shared tail of Alg. 5 steps 8-10,
     recycle_q and rsvd_pi.  Returns the top-k DevSvd (descending).
     download: V's device->host copy starts (side stream) before U is lifted."""
@@ -234,16 +234,55 @@ def project_and_solve(Y: SparseMatrix, Q, k: int, fb: _Fallback, precision: str 
     idx = np.arange(W - 1, W - k - 1, -1)  # top-k of the ascending order, descending
     if isinstance(Q, LazyQ):
         # Q = Q1 Rinv unformed: B^T = (Y^T Q1) Rinv, U = Q1 (Rinv V_small)
-        T = _spmm_t_prec(Y, Q.base, precision)
+        T = T_pre if T_pre is not None else _spmm_t_prec(Y, Q.base, precision)
         S_sel, Vsel, Usel = _windowed_small_svd(T, idx, fb, Rinv=Q.Rinv)
         pend = device.to_host_async(Usel) if download else None
         U = matmul_dev(Q.base, matmul_dev(Q.Rinv, Vsel))
     else:
-        Bt = _spmm_t_prec(Y, Q, precision)
+        Bt = T_pre if T_pre is not None else _spmm_t_prec(Y, Q, precision)
         S_sel, Vsel, Usel = _windowed_small_svd(Bt, idx, fb)
         pend = device.to_host_async(Usel) if download else None
         U = matmul_dev(Q, Vsel)
     return DevSvd(U, device.f64_buffer(S_sel), Usel, np.asarray(S_sel, dtype=np.float64), pend)
+
+
+class Prestart:
+    """The first product of an inner SVD queued ahead of its call (the SVT
+    loop queues it behind the fused step, before reading the residual):
+    kind "bki": H (m x w (p_max + 1), block 0 = LU(Y Omega)) and the LU status
+    vector; kind "recycle-q": T = Y^T Q of the cached basis."""
+
+    def __init__(self, kind, **kw):
+        self.kind = kind
+        self.__dict__.update(kw)
+
+    def matches(self, params: "RsvdParams") -> bool:
+        return (self.kind == "bki" and params.k == self.k and params.s == self.s and params.seed == self.seed
+                and params.p <= self.p_max)
+
+
+def bki_prestart(A: SparseMatrix, k: int, s: int, seed: int, p_max: int, precision: str = "fp64"):
+    """Alg. 5 steps 1-2 of a coming rsvd_bki call: Omega (seed), H_0 = A Omega
+    and its LU (status left on the device), into an H block wide enough for
+    p_max Krylov steps.  None when the call will not use it (fp32 mode, the
+    careful path)."""
+    if not SPECULATIVE or _check_precision(precision) == "fp32":
+        return None
+    w = k + s
+    m, n = A.shape
+    Om = _omega(seed, n, w, OMEGA_SOURCE)
+    H = device.empty(m, w * (p_max + 1))
+    lu_status = device.vector(4 * (p_max + 1))
+    spmm_dev(A, Om, out=H[:, 0:w])
+    _lu_block_async(H[:, 0:w], lu_status[0:3])
+    return Prestart("bki", k=k, s=s, seed=seed, p_max=p_max, H=H, lu_status=lu_status)
+
+
+def recycle_prestart(Y: SparseMatrix, cached: "Subspace", precision: str = "fp64"):
+    """The product B^T = Y^T Q (Q1 for an unformed basis) of a coming recycle_q."""
+    Q = cached.Q_any
+    base = Q.base if isinstance(Q, LazyQ) else Q
+    return Prestart("recycle-q", Q=Q, T=_spmm_t_prec(Y, base, precision))
 
 
 def _check_precision(precision: str) -> str:
@@ -252,7 +291,8 @@ def _check_precision(precision: str) -> str:
     return precision
 
 
-def _krylov_orth(A: SparseMatrix, Om, params: RsvdParams, spec: bool, fp32: bool, lazy: bool, fb: _Fallback):
+def _krylov_orth(A: SparseMatrix, Om, params: RsvdParams, spec: bool, fp32: bool, lazy: bool, fb: _Fallback,
+                 pre: Prestart = None):
     """Alg. 5 steps 1-7 from a given Omega: Krylov blocks H_0..H_p (LU-
     normalised) and the basis.  spec: LU statuses and the CholeskyQR route's
     decisions stay on the device (no host synchronisation at all: the body
@@ -260,8 +300,12 @@ def _krylov_orth(A: SparseMatrix, Om, params: RsvdParams, spec: bool, fp32: bool
     w = params.k + params.s
     W = w * (params.p + 1)
     m, n = A.shape
-    lu_status = device.vector(4 * (params.p + 1)) if spec else None
-    H = device.empty(m, W)
+    if pre is not None:  # H_0 and its LU already queued (bki_prestart)
+        H = pre.H[:, :W]
+        lu_status = pre.lu_status[:4 * (params.p + 1)]
+    else:
+        lu_status = device.vector(4 * (params.p + 1)) if spec else None
+        H = device.empty(m, W)
 
     def normalise(i):
         if spec:
@@ -273,9 +317,10 @@ def _krylov_orth(A: SparseMatrix, Om, params: RsvdParams, spec: bool, fp32: bool
         H32, T32 = device.empty32(m, w), device.empty32(n, w)
         spmm_dev32(A, device.to_f32(Om), out=H32)
         device.to_f64(H32, out=H[:, 0:w])
-    else:
+    elif pre is None:
         spmm_dev(A, Om, out=H[:, 0:w])
-    normalise(0)
+    if pre is None:
+        normalise(0)
     T = None if fp32 else device.empty(n, w)
     for i in range(1, params.p + 1):
         if fp32:
@@ -295,7 +340,7 @@ def _krylov_orth(A: SparseMatrix, Om, params: RsvdParams, spec: bool, fp32: bool
 
 
 def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = False, omega=None,
-                 precision: str = "fp64", download: bool = False, _speculate: bool = True):
+                 precision: str = "fp64", download: bool = False, _speculate: bool = True, pre: Prestart = None):
     """Device Alg. 5 -> (DevSvd, Q device, fallbacks).
 
     precision="fp32" (north_star's optional fp32 mode, singular values within
@@ -321,8 +366,10 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
     # per steady-state cfg1-sized call, but ~6 ms per capture, and the SVT
     # loop's k changes make captures outnumber replays -- not kept.)
     spec = SPECULATIVE and _speculate
-    Om = _omega(params.seed, n, w, omega or OMEGA_SOURCE)
-    H, Q, lu_status, probe = _krylov_orth(A, Om, params, spec, fp32, lazy, fb)
+    use_pre = (pre is not None and spec and not fp32 and (omega or OMEGA_SOURCE) == OMEGA_SOURCE
+               and pre.matches(params))
+    Om = None if use_pre else _omega(params.seed, n, w, omega or OMEGA_SOURCE)
+    H, Q, lu_status, probe = _krylov_orth(A, Om, params, spec, fp32, lazy, fb, pre=pre if use_pre else None)
     if spec:
         st = device.to_host(lu_status).reshape(-1, 4)[:, :3]
         diag_h, infos_h = device.to_host(probe[0]), device.to_host(probe[1])

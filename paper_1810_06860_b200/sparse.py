@@ -172,8 +172,12 @@ class DevicePattern:
     def __init__(self, A: "SparseMatrix", prefetch_values=None):
         self.shape = (A.rows, A.cols)
         self.nnz = A.nnz
-        hp = A._host_prep()
-        self.csr = _Side(hp.csr)
+        if A._dev_csr is not None:  # built on the device: only the schedule comes from the host
+            hp = A._host_prep_dev()
+            self.csr = _Side(rows=A.rows, ptr=A._dev_csr[0], idx=A._dev_csr[1], sched=hp.csr_sched)
+        else:
+            hp = A._host_prep()
+            self.csr = _Side(hp.csr)
         # the values' upload (side stream) overlaps the device transpose below
         self._prefetch = None
         if prefetch_values is not None and self.nnz:
@@ -198,6 +202,14 @@ class DevicePattern:
             self._tile_rows = tr
         return tr
 
+    def values_from_device(self, vc):
+        """(csr, csc) device value copies from a device CSR-order vector."""
+        vt = device.vector(self.nnz)
+        if self.nnz:
+            _native.call("lr_gather_f64", device.ptr(vc), device.ptr(self.perm), device.ptr(vt), self.nnz,
+                         device.stream())
+        return vc, vt
+
     def values(self, host_vals: np.ndarray):
         """(csr, csc) device value copies of host values in CSR order."""
         pre = self._prefetch
@@ -221,11 +233,13 @@ class SparseMatrix:
     sanctioned mutation is `update_pattern_values`.
     """
 
+    _dev_csr = None  # (ptr, idx int32, values) when the pattern was built on the device
+
     def __init__(self, rows: int, cols: int, indptr, indices, data):
         self.rows = int(rows)
         self.cols = int(cols)
         self.indptr = np.ascontiguousarray(indptr, dtype=np.int64)
-        self.indices = np.ascontiguousarray(indices, dtype=np.int64)
+        self._indices = np.ascontiguousarray(indices, dtype=np.int64)
         self._data = np.ascontiguousarray(data, dtype=np.float64)
         self._validate()
         self._tperm = self._t_indptr = self._t_indices = self._coo_rows = None
@@ -233,6 +247,79 @@ class SparseMatrix:
         self._dvals = None  # (csr, csc) device values
         self._host_stale = False
         self._csc_stale = False  # CSR copy updated in place; CSC copy refreshed on demand
+
+    @property
+    def indices(self) -> np.ndarray:
+        """Column indices (int64, host); a device-built pattern downloads them
+        on first access."""
+        if self._indices is None:
+            self._indices = device.to_host(self._dev_csr[1]).astype(np.int64)
+        return self._indices
+
+    @indices.setter
+    def indices(self, value):
+        self._indices = value
+
+    @classmethod
+    def from_coo_device(cls, rows: int, cols: int, i, j, v, split=None, tag: int = 0) -> "SparseMatrix":
+        """from_coo on the device (lr_coo_to_csr_i32: bounds, duplicates, row
+        buckets + per-row column sort -- the same CSR as the host lexsort, bit
+        for bit).  The host keeps only indptr (the work schedule needs it);
+        indices and values come back on access.  With `split` (uint8 tags),
+        only the entries tagged `tag` are used (ObservationSet.train_matrix)."""
+        import ctypes
+
+        rows, cols = int(rows), int(cols)
+        if rows < 1 or cols < 1:
+            raise DataError(f"matrix dims must be positive, got {rows}x{cols}")
+        count = int(np.asarray(i).shape[0])
+        if not (np.asarray(j).shape[0] == np.asarray(v).shape[0] == count):
+            raise DataError("coordinate arrays must be 1-D and equal length")
+        if count >= (1 << 31) - 1:
+            return cls.from_coo(rows, cols, *_select(i, j, v, split, tag))
+        dev = device.require_cuda()
+        st = device.stream()
+        di = device.upload_async_i64(i)
+        dj = device.upload_async_i64(j)
+        dv = device.f64_buffer(np.asarray(v, dtype=np.float64))
+        ds = None
+        if split is not None:
+            ds = torch.from_numpy(np.ascontiguousarray(split, dtype=np.uint8)).to(dev, non_blocking=True)
+        i32 = torch.int32
+        ptr = torch.empty(rows + 1, dtype=i32, device=dev)
+        col = torch.empty(max(count, 1), dtype=i32, device=dev)
+        src = torch.empty(max(count, 1), dtype=i32, device=dev)
+        vals = torch.empty(max(count, 1), dtype=torch.float64, device=dev)
+        lib = _native.load()
+        ws = int(lib.lr_coo_to_csr_workspace_ints(rows, count))
+        work = torch.empty(max(ws, 1), dtype=i32, device=dev)
+        status = (ctypes.c_int * 3)()
+        _native.call("lr_coo_to_csr_i32", rows, cols, count, device.ptr(di), device.ptr(dj), device.ptr(ds),
+                     int(tag), device.ptr(dv), device.ptr(ptr), device.ptr(col), device.ptr(src), device.ptr(vals),
+                     device.ptr(work), ws, ctypes.byref(status), st)
+        if status[0] == 1:
+            raise DataError("coordinate out of range")
+        if status[0] == 2:
+            raise DataError("matrix values must be finite")
+        nnz = int(status[2])
+        indptr = device.to_host(ptr).astype(np.int64)
+        if status[1] >= 0:
+            p = int(status[1])
+            r = int(np.searchsorted(indptr, p, side="right") - 1)
+            c = int(device.to_host(col[p:p + 1])[0])
+            raise DataError(f"duplicate entry at ({r}, {c})")
+        out = cls.__new__(cls)
+        out.rows, out.cols = rows, cols
+        out.indptr = indptr
+        out._indices = None
+        out._data = np.empty(nnz)
+        out._tperm = out._t_indptr = out._t_indices = out._coo_rows = None
+        out._pattern = None
+        out._dvals = None
+        out._host_stale = True  # host values download on access
+        out._csc_stale = False
+        out._dev_csr = (ptr, col[:nnz], vals[:nnz])
+        return out
 
     # ------------------------------------------------------------ checks
     def _validate(self) -> None:
@@ -300,7 +387,8 @@ class SparseMatrix:
     @property
     def data(self) -> np.ndarray:
         if self._host_stale:
-            self._data[...] = device.to_host(self._dvals[0])
+            src = self._dvals[0] if self._dvals is not None else self._dev_csr[2]
+            self._data[...] = device.to_host(src)
             self._host_stale = False
         return self._data
 
@@ -325,6 +413,16 @@ class SparseMatrix:
         return out
 
     # ------------------------------------------------------------ device
+    def _host_prep_dev(self):
+        """Host side of a device-built pattern: the CSR work schedule (from
+        indptr) and the CSC schedule cache."""
+        hp = getattr(self, "_hprep_dev", None)
+        if hp is None:
+            hp = self._hprep_dev = type("_DevPrep", (), {})()
+            hp.csr_sched = _schedule(self.indptr)
+            hp.csc_sched = None
+        return hp
+
     def _host_prep(self) -> _HostPrep:
         if getattr(self, "_hprep", None) is None:
             self._hprep = _HostPrep(self)
@@ -334,7 +432,7 @@ class SparseMatrix:
         if self._pattern is None:
             # first device use: the values ride along (uploaded while the
             # transpose index is built) unless they are already resident
-            pre = self._data if (self._dvals is None and not self._host_stale) else None
+            pre = self._data if (self._dvals is None and not self._host_stale and self._dev_csr is None) else None
             self._pattern = DevicePattern(self, prefetch_values=pre)
         return self._pattern
 
@@ -370,7 +468,10 @@ class SparseMatrix:
         (csc[s] = csr[perm[s]]: coalesced perm read and store, one random 8-byte
         read per entry) before anything reads it."""
         if self._dvals is None:
-            self._dvals = self.pattern().values(self._data)
+            if self._dev_csr is not None and self._host_stale:
+                self._dvals = self.pattern().values_from_device(self._dev_csr[2])
+            else:
+                self._dvals = self.pattern().values(self._data)
             self._csc_stale = False
         elif self._csc_stale:
             vc, vt = self._dvals
@@ -389,17 +490,18 @@ class SparseMatrix:
         constructor's finiteness check holds iff scale * max|data| is finite
         (rounding is monotone), so it is decided from one cached scalar."""
         scale = float(scale)
-        if self._host_stale:
-            _ = self.data
         mx = getattr(self, "_maxabs", None)
-        if mx is None:
-            mx = float(np.max(np.abs(self._data))) if self.nnz else 0.0
+        if mx is None:  # max |data| from the resident CSR copy (one device reduction)
+            mx = float(device.to_host(_stats(self.device_values()[0], self.nnz, 1, 1))[1]) if self.nnz else 0.0
             self._maxabs = mx
         if not (np.isfinite(scale) and np.isfinite(scale * mx)):
             raise DataError("matrix values must be finite")
         out = SparseMatrix.__new__(SparseMatrix)
         out.rows, out.cols = self.rows, self.cols
-        out.indptr, out.indices = self.indptr, self.indices
+        out.indptr, out._indices = self.indptr, self._indices
+        if self._dev_csr is not None:  # indices stay on the device until asked for
+            out._dev_csr = (self._dev_csr[0], self._dev_csr[1], None)
+            out._hprep_dev = self._host_prep_dev()
         out._data = np.empty(self.nnz)
         out._tperm = out._t_indptr = out._t_indices = out._coo_rows = None
         out._pattern = None
@@ -441,6 +543,13 @@ class SparseMatrix:
 
 
 # --------------------------------------------------------------- kernels
+
+def _select(i, j, v, split, tag):
+    if split is None:
+        return i, j, v
+    sel = np.asarray(split) == tag
+    return np.asarray(i)[sel], np.asarray(j)[sel], np.asarray(v)[sel]
+
 
 def _spmm_side(side: _Side, vals, X, out=None):
     rows_out = side.rows
@@ -770,5 +879,11 @@ class ObservationSet:
         return self.rows[sel], self.cols[sel], self.values[sel]
 
     def train_matrix(self) -> SparseMatrix:
+        """The train split as CSR: built on the device when one is present
+        (SparseMatrix.from_coo_device: the host lexsort of ~20M cells costs
+        seconds), else on the host."""
+        if device.cuda_ready():
+            return SparseMatrix.from_coo_device(self.m, self.n, self.rows, self.cols, self.values, self.split,
+                                                self.TRAIN)
         r, c, v = self.subset(self.TRAIN)
         return SparseMatrix.from_coo(self.m, self.n, r, c, v)

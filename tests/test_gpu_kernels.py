@@ -556,3 +556,64 @@ def test_svt_step_flat_matches_oracle_and_refreshes_csc(m, n, nnz, long_rows, em
     tperm = np.argsort(jj, kind="stable")
     assert np.array_equal(device.to_host(yt), device.to_host(yc)[tperm])
     assert torch.equal(yc.cpu(), torch.from_numpy(y_dev))
+
+
+@pytest.mark.parametrize("m,n,nnz,long_rows,shuffle", [(1, 1, 1, 0, False), (300, 200, 4000, 0, True),
+                                                       (2000, 9000, 60000, 2, True), (50, 5000, 0, 1, True),
+                                                       (5000, 3000, 200000, 0, True)])
+def test_coo_to_csr_device_matches_host_lexsort(m, n, nnz, long_rows, shuffle):
+    """SparseMatrix.from_coo_device (lr_coo_to_csr_i32) against the host
+    lexsort build (sparse.py:84-104): indptr, indices and values bit-exact,
+    incl. empty rows and dense rows longer than the shared-memory sort (9000
+    columns), entries in arbitrary input order; the split-tag selection of
+    ObservationSet.train_matrix; the device values and the CSC transpose built
+    from the device pattern."""
+    import torch
+
+    from paper_1810_06860_b200 import device
+    from paper_1810_06860_b200.sparse import ObservationSet, SparseMatrix
+
+    i, j, v = rand_pattern(m, n, nnz, seed=m + n, long_rows=long_rows)
+    if shuffle:
+        p = np.random.default_rng(1).permutation(i.size)
+        i, j, v = i[p], j[p], v[p]
+    H = SparseMatrix.from_coo(m, n, i, j, v)
+    D = SparseMatrix.from_coo_device(m, n, i, j, v)
+    assert D._dev_csr is not None
+    assert np.array_equal(D.indptr, H.indptr)
+    assert np.array_equal(D.indices, H.indices)
+    assert np.array_equal(D.data, H.data)
+    vc, vt = D.device_values()
+    assert np.array_equal(device.to_host(vc), H.data)
+    tperm, _, _ = H._transpose_index()
+    assert np.array_equal(device.to_host(vt), H.data[tperm])
+    assert torch.equal(D.pattern().csc.idx[:H.nnz].cpu(), H.pattern().csc.idx[:H.nnz].cpu())
+    split = (np.random.default_rng(2).random(i.size) < 0.3).astype(np.uint8)
+    obs = ObservationSet(m, n, i, j, v, split)
+    T = obs.train_matrix()
+    r, c, vv = obs.subset(0)
+    ref = SparseMatrix.from_coo(m, n, r, c, vv)
+    assert np.array_equal(T.indptr, ref.indptr) and np.array_equal(T.indices, ref.indices)
+    assert np.array_equal(T.data, ref.data)
+
+
+def test_coo_to_csr_device_errors():
+    """The device build raises what the host build raises: out-of-range
+    coordinates, the first duplicate cell in (row, col) order, non-finite
+    values."""
+    from paper_1810_06860_b200.errors import DataError
+    from paper_1810_06860_b200.sparse import SparseMatrix
+
+    with pytest.raises(DataError, match="out of range"):
+        SparseMatrix.from_coo_device(3, 3, [0, 3], [0, 1], [1.0, 2.0])
+    with pytest.raises(DataError, match="out of range"):
+        SparseMatrix.from_coo_device(3, 3, [0, 1], [0, -1], [1.0, 2.0])
+    i = [2, 0, 2, 1, 0, 1]
+    j = [1, 2, 1, 0, 2, 2]
+    with pytest.raises(DataError) as eh:
+        SparseMatrix.from_coo(3, 3, i, j, np.arange(6.0))
+    with pytest.raises(DataError) as ed:
+        SparseMatrix.from_coo_device(3, 3, i, j, np.arange(6.0))
+    assert str(ed.value) == str(eh.value) == "duplicate entry at (0, 2)"
+    with pytest.raises(DataError, match="finite"):
+        SparseMatrix.from_coo_device(3, 3, [0, 1], [0, 1], [1.0, np.inf])

@@ -194,3 +194,19 @@ def test_c_uniforms_and_box_muller_are_bit_exact(rows, cols, seed):
     u = np.empty(11)
     lib.lr_host_uniforms(seed & ((1 << 64) - 1), 5, 11, u.ctypes.data)
     assert np.array_equal(u, R.RngState(seed).uniform(16)[5:])
+
+
+@pytest.mark.parametrize("rows,w_lo,w_hi", [(1, 1, 3), (7, 2, 9), (26744, 9, 17), (1001, 1, 40)])
+def test_superset_draw_is_bit_exact(rows, w_lo, w_hi):
+    """rng.Superset (one draw serving every width in [w_lo, w_hi]) gives, for
+    each width, exactly the one-width draw of the reference (rng.py:38-55)."""
+    from paper_1810_06860_b200 import rng as R
+
+    lib = R._c_draw_lib()
+    assert lib
+    seed = 2 ** 40 + rows
+    sup = R.Superset(lib, seed, rows, w_lo, w_hi, R._pool())
+    for w in range(w_lo, w_hi + 1):
+        ref = R.RngState(seed).normal_pairs(rows * w)
+        out = np.empty(rows * w + 1)
+        assert np.array_equal(sup.normals(w, out, R._pool()), ref), w
