@@ -223,7 +223,7 @@ int lr_scale_columns_f64(const double* V, long long ldv, int rows, const int* co
  * (sparse.py:84-104; ObservationSet.train_matrix, :259-328).  ptr (m+1),
  * col_out / src_out (int32: column, source index, in CSR order), vals_out
  * (values gathered in CSR order, may be NULL).  Bit-exact with the host
- * lexsort.  status_host[0]: 0 ok, 1 a coordinate out of range, 2 a
+ * lexsort.  status_host[0]: 0 ok, 1 a row / 3 a column out of range, 2 a
  * non-finite value; [1] the CSR slot of the first duplicate cell (-1: none);
  * [2] nnz.  Synchronizes the stream (twice). */
 long long lr_coo_to_csr_workspace_ints(int m, long long count);

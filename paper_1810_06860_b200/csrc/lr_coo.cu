@@ -31,12 +31,12 @@ __global__ void coo_hist_kernel(const long long* __restrict__ rows, const long l
     if (split && (int)split[e] != tag) continue;
     const long long i = rows[e], j = cols[e];
     if (i < 0 || i >= m || j < 0 || j >= n) {
-      bad = 1;
+      bad |= (i < 0 || i >= m) ? 1 : 4;  // 1: a row out of range, 4: a column
       continue;
     }
     atomicAdd(row_cnt + i, 1);
   }
-  if (bad) atomicOr(flags, 1);
+  if (bad) atomicOr(flags, bad);
 }
 
 // ptr[0..m] = exclusive scan of cnt[0..m-1]; one CTA of 1024 threads
@@ -204,8 +204,10 @@ int lr_coo_to_csr_i32(int m, int n, long long count, const long long* rows, cons
   LR_CHECK_CUDA(cudaMemcpyAsync(h, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
   LR_CHECK_CUDA(cudaMemcpyAsync(&nnz, ptr + m, sizeof(int), cudaMemcpyDeviceToHost, s));
   LR_CHECK_CUDA(cudaStreamSynchronize(s));
-  if (h[0] & 1) {
-    status_host[0] = 1;  // out of range
+  if (h[0] & 5) {
+    status_host[0] = (h[0] & 1) ? 1 : 3;  // 1: a row out of range, 3: a column out of range
+    status_host[1] = -1;
+    status_host[2] = 0;
     return LR_OK;
   }
   if (nnz > 0) {

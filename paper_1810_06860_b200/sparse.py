@@ -261,7 +261,9 @@ class SparseMatrix:
         self._indices = value
 
     @classmethod
-    def from_coo_device(cls, rows: int, cols: int, i, j, v, split=None, tag: int = 0) -> "SparseMatrix":
+    def from_coo_device(cls, rows: int, cols: int, i, j, v, split=None, tag: int = 0,
+                        range_msg=("coordinate out of range", "coordinate out of range"),
+                        dup_msg=None) -> "SparseMatrix":
         """from_coo on the device (lr_coo_to_csr_i32: bounds, duplicates, row
         buckets + per-row column sort -- the same CSR as the host lexsort, bit
         for bit).  The host keeps only indptr (the work schedule needs it);
@@ -297,13 +299,15 @@ class SparseMatrix:
         _native.call("lr_coo_to_csr_i32", rows, cols, count, device.ptr(di), device.ptr(dj), device.ptr(ds),
                      int(tag), device.ptr(dv), device.ptr(ptr), device.ptr(col), device.ptr(src), device.ptr(vals),
                      device.ptr(work), ws, ctypes.byref(status), st)
-        if status[0] == 1:
-            raise DataError("coordinate out of range")
+        if status[0] in (1, 3):
+            raise DataError(range_msg[0] if status[0] == 1 else range_msg[1])
         if status[0] == 2:
             raise DataError("matrix values must be finite")
         nnz = int(status[2])
         indptr = device.to_host(ptr).astype(np.int64)
         if status[1] >= 0:
+            if dup_msg is not None:
+                raise DataError(dup_msg)
             p = int(status[1])
             r = int(np.searchsorted(indptr, p, side="right") - 1)
             c = int(device.to_host(col[p:p + 1])[0])
@@ -847,6 +851,9 @@ class ObservationSet:
         cnt = self.rows.shape[0]
         if not (self.cols.shape[0] == self.values.shape[0] == self.split.shape[0] == cnt):
             raise DataError("observation arrays must have equal length")
+        if cnt and device.cuda_ready() and cnt < (1 << 31) - 1:
+            self._validate_device()
+            return
         if cnt:
             if self.rows.min() < 0 or self.rows.max() >= self.m:
                 raise DataError("observation row index out of range")
@@ -861,6 +868,27 @@ class ObservationSet:
             key = self.rows[sel] * self.n + self.cols[sel]
             if key.size != np.unique(key).size:
                 raise DataError(f"duplicate (row, col) within {name} split")
+
+    def _validate_device(self) -> None:
+        """The same checks, in the same order, with the duplicate search of
+        each split on the device (lr_coo_to_csr_i32 over the split's cells:
+        the host np.unique of ~20M keys costs seconds).  The train split's
+        device CSR is kept for train_matrix()."""
+        msgs = ("observation row index out of range", "observation col index out of range")
+        if self.rows.min() < 0 or self.rows.max() >= self.m:
+            raise DataError(msgs[0])
+        if self.cols.min() < 0 or self.cols.max() >= self.n:
+            raise DataError(msgs[1])
+        if not np.isfinite(self.values).all():
+            raise DataError("observation values must be finite")
+        if np.any(self.split > 1):
+            raise DataError("split tags must be 0 (train) or 1 (test)")
+        self._train_dev = SparseMatrix.from_coo_device(self.m, self.n, self.rows, self.cols, self.values, self.split,
+                                                       self.TRAIN, range_msg=msgs,
+                                                       dup_msg="duplicate (row, col) within train split")
+        if np.any(self.split == self.TEST):
+            SparseMatrix.from_coo_device(self.m, self.n, self.rows, self.cols, self.values, self.split, self.TEST,
+                                         range_msg=msgs, dup_msg="duplicate (row, col) within test split")
 
     @property
     def count(self) -> int:
@@ -882,6 +910,10 @@ class ObservationSet:
         """The train split as CSR: built on the device when one is present
         (SparseMatrix.from_coo_device: the host lexsort of ~20M cells costs
         seconds), else on the host."""
+        pre = getattr(self, "_train_dev", None)
+        if pre is not None:  # built by the device validation; hand it out once
+            self._train_dev = None
+            return pre
         if device.cuda_ready():
             return SparseMatrix.from_coo_device(self.m, self.n, self.rows, self.cols, self.values, self.split,
                                                 self.TRAIN)

@@ -617,3 +617,36 @@ def test_coo_to_csr_device_errors():
     assert str(ed.value) == str(eh.value) == "duplicate entry at (0, 2)"
     with pytest.raises(DataError, match="finite"):
         SparseMatrix.from_coo_device(3, 3, [0, 1], [0, 1], [1.0, np.inf])
+
+
+def test_observation_set_device_validation_matches_host():
+    """ObservationSet validates on the device when one is present (the
+    duplicate search of each split through lr_coo_to_csr_i32) and raises the
+    reference's errors in the reference's order (sparse.py:259-328); the train
+    split's device CSR is handed to train_matrix() once."""
+    from paper_1810_06860_b200 import device
+    from paper_1810_06860_b200.errors import DataError
+    from paper_1810_06860_b200.sparse import ObservationSet, SparseMatrix
+
+    assert device.cuda_ready()
+    rows, cols = np.array([0, 1, 2, 1, 0]), np.array([1, 2, 0, 2, 1])
+    vals = np.arange(5.0)
+    # (0, 1) twice: in the same split -> error; across splits -> fine
+    with pytest.raises(DataError, match="duplicate \\(row, col\\) within train split"):
+        ObservationSet(3, 3, rows[:2].tolist() + [0], cols[:2].tolist() + [1], vals[:3])
+    with pytest.raises(DataError, match="within test split"):
+        ObservationSet(3, 3, [0, 0, 2], [1, 1, 0], vals[:3], np.array([1, 1, 0], dtype=np.uint8))
+    ok = ObservationSet(3, 3, [0, 0, 2], [1, 1, 0], vals[:3], np.array([0, 1, 0], dtype=np.uint8))
+    T = ok.train_matrix()
+    assert T.indptr.tolist() == [0, 1, 1, 2] and T.indices.tolist() == [1, 0] and T.data.tolist() == [0.0, 2.0]
+    T2 = ok.train_matrix()  # a fresh build the second time
+    assert T2 is not T and np.array_equal(T2.data, T.data)
+    with pytest.raises(DataError, match="row index out of range"):
+        ObservationSet(3, 3, [0, 3], [0, 9], [1.0, 2.0])
+    with pytest.raises(DataError, match="col index out of range"):
+        ObservationSet(3, 3, [0, 1], [0, 9], [1.0, 2.0])
+    with pytest.raises(DataError, match="finite"):
+        ObservationSet(3, 3, [0, 1], [0, 1], [1.0, np.nan])
+    with pytest.raises(DataError, match="split tags"):
+        ObservationSet(3, 3, [0, 1], [0, 1], [1.0, 2.0], np.array([0, 2], dtype=np.uint8))
+    assert isinstance(T, SparseMatrix)
