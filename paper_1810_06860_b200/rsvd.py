@@ -136,6 +136,19 @@ def _omega(seed: int, n: int, w: int, source: str):
     return omega_from_host(seed, n, w)
 
 
+def _overlap_draw_with_upload(A: SparseMatrix, seed: int, n: int, w: int, source: str) -> None:
+    """A call on a matrix whose device mirror is not built yet (the public API
+    from host arrays): start the host draw of Omega in the background, then
+    upload the pattern / values and build the transpose index meanwhile."""
+    if source != "host" or A._pattern is not None:
+        return
+    from .rng import prefetch_normals
+
+    prefetch_normals(seed, n, w)
+    A.pattern()
+    A.device_values()
+
+
 def omega_from_host(seed: int, n: int, w: int):
     """Omega = gaussian_matrix(RngState(seed), n, w) drawn on the HOST with
     numpy's own arithmetic (bit-identical to the reference's draw; threaded,
@@ -368,6 +381,8 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
     spec = SPECULATIVE and _speculate
     use_pre = (pre is not None and spec and not fp32 and (omega or OMEGA_SOURCE) == OMEGA_SOURCE
                and pre.matches(params))
+    if not use_pre:
+        _overlap_draw_with_upload(A, params.seed, n, w, omega or OMEGA_SOURCE)
     Om = None if use_pre else _omega(params.seed, n, w, omega or OMEGA_SOURCE)
     H, Q, lu_status, probe = _krylov_orth(A, Om, params, spec, fp32, lazy, fb, pre=pre if use_pre else None)
     if spec:
@@ -396,6 +411,7 @@ def rsvd_pi_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fals
     fb = _Fallback(allow_fallback, "increase s or reduce k")
     w = params.k + params.s
     m, n = A.shape
+    _overlap_draw_with_upload(A, params.seed, n, w, omega or OMEGA_SOURCE)
     Om = _omega(params.seed, n, w, omega or OMEGA_SOURCE)
     Q = spmm_dev(A, Om)
     T = device.empty(n, w)
