@@ -109,6 +109,15 @@ def host_info(threads=None):
     except Exception:
         pass
     try:
+        import subprocess
+
+        ls = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        keep = ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core", "CPU max MHz", "L3 cache")
+        info["lscpu"] = {k.strip(): v.strip() for k, v in (ln.split(":", 1) for ln in ls.splitlines() if ":" in ln)
+                         if k.strip() in keep}
+    except Exception:
+        pass
+    try:
         from threadpoolctl import threadpool_info
 
         info["blas"] = [{"lib": d.get("internal_api"), "version": d.get("version"), "threads": d.get("num_threads"),
@@ -708,7 +717,13 @@ def main():
         if args.cpu_baseline == "full" and ws == 1:
             from paper_1810_06860_b200 import workloads
 
-            d = cpu_svt_sample(workloads.cfg4(), max_iters=int(os.environ.get("BENCH_REF_ITERS", "3")))
+            o4c = workloads.cfg4()
+            d = cpu_svt_sample(o4c, max_iters=int(os.environ.get("BENCH_REF_ITERS", "3")))
+            d1 = cpu_svt_sample(o4c, max_iters=1, threads=1)  # the reference's own 1-thread convention
+            line["cpu_baseline_1thread"] = {"value": d1["iterations_per_s"], "unit": "SVT iterations/s (cfg4)",
+                                            "cores": 1, "kind": d1["kind"],
+                                            "sample": f"first iteration of the same cfg4 job, BLAS limited to "
+                                                      f"1 thread ({d1['loop_s']:.1f} s loop)"}
             line["cpu_baseline"] = {"value": d["iterations_per_s"], "unit": "SVT iterations/s (cfg4)",
                                     "cores": os.cpu_count(), "kind": d["kind"],
                                     "sample": f"first {d['iterations']} iterations of the same cfg4 job "

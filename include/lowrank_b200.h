@@ -212,6 +212,10 @@ int lr_syevd_f64(int n, const double* A, long long lda, double* d, double* V, lo
  * of U if non-NULL) so V's first nonzero entry in column j is >= 0. */
 int lr_fix_signs_f64(double* V, long long ldv, int rows_v, int cols, double* U, long long ldu,
                      int rows_u, void* stream);
+/* S[i] = sqrt(max(d[i], 0)): singular values of ascending Gram eigenvalues
+ * (linalg.py:196), on the device so eig_svd's lift is queued before the host
+ * reads d for the rank checks. */
+int lr_gram_spectrum_f64(const double* d, int n, double* S, void* stream);
 /* B[:, j] = V[:, idx_j] * scale_j with scale_j = sgn/S[idx_j]; column gather
  * used by eig_svd's U = A (V / S) for a selected window (linalg.py:199-201). */
 int lr_scale_columns_f64(const double* V, long long ldv, int rows, const int* cols_idx, int ncols,
@@ -235,10 +239,11 @@ int lr_coo_to_csr_i32(int m, int n, long long count, const long long* rows, cons
  * dgesdd, linalg.py:205-221): the columns of B are the rows of Bt (n x m),
  * the columns of V the rows of Vt (n x n).  Every column pair (one
  * round-robin sweep, N-1 launches) with |<b_p, b_q>| > tol |b_p| |b_q| is
- * rotated orthogonal, the rotation applied to Vt too; off[0] (device) =
+ * rotated orthogonal, the rotation applied to Vt too, except pairs whose
+ * squared norms are both below noise2 (0: none skipped); off[0] (device) =
  * the largest measure rotated (0: converged).  Deterministic. */
 int lr_jacobi_sweep_f64(int n, int m, double* Bt, long long ldb, double* Vt, long long ldv, double tol,
-                        double* off, void* stream);
+                        double noise2, double* off, void* stream);
 /* out[i] = ||row i of Bt||_2 (scaled, no overflow), n rows of length m. */
 int lr_row_norms_f64(const double* Bt, long long ldb, int n, int m, double* out, void* stream);
 

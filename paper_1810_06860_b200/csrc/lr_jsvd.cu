@@ -36,7 +36,7 @@ __device__ __forceinline__ void pair_of(int k, int s, int N, int& p, int& q) {
 
 __global__ void __launch_bounds__(kJsThreads) jacobi_pair_kernel(double* __restrict__ Bt, long long ldb, int m,
                                                                   double* __restrict__ Vt, long long ldv, int n,
-                                                                  int N, int s, double tol,
+                                                                  int N, int s, double tol, double noise2,
                                                                   unsigned long long* __restrict__ off) {
   int p, q;
   pair_of(blockIdx.x, s, N, p, q);
@@ -58,7 +58,9 @@ __global__ void __launch_bounds__(kJsThreads) jacobi_pair_kernel(double* __restr
   if (threadIdx.x == 0) {
     double c = 1.0, sn = 0.0;
     const double den = sqrt(a) * sqrt(b);
-    const double meas = (den > 0.0) ? fabs(g) / den : 0.0;
+    // two noise-level columns (squared norms below noise2) are not rotated:
+    // their mutual angle is rounding noise and need not converge
+    const double meas = (den > 0.0 && !(a < noise2 && b < noise2)) ? fabs(g) / den : 0.0;
     if (meas > tol) {
       // rotate so that the new columns are orthogonal (Rutishauser's formulas)
       const double zeta = (b - a) / (2.0 * g);
@@ -118,14 +120,14 @@ using namespace lr;
 extern "C" {
 
 int lr_jacobi_sweep_f64(int n, int m, double* Bt, long long ldb, double* Vt, long long ldv, double tol,
-                        double* off, void* stream) {
+                        double noise2, double* off, void* stream) {
   LR_REQUIRE(n >= 1 && m >= 1 && ldb >= m && ldv >= n, "jacobi_sweep: bad dims (n=%d m=%d)", n, m);
   cudaStream_t s = as_stream(stream);
   LR_CHECK_CUDA(cudaMemsetAsync(off, 0, sizeof(double), s));
   if (n == 1) return LR_OK;
   const int N = n + (n & 1);
   for (int step = 0; step < N - 1; ++step) {
-    jacobi_pair_kernel<<<N / 2, kJsThreads, 0, s>>>(Bt, ldb, m, Vt, ldv, n, N, step, tol,
+    jacobi_pair_kernel<<<N / 2, kJsThreads, 0, s>>>(Bt, ldb, m, Vt, ldv, n, N, step, tol, noise2,
                                                     reinterpret_cast<unsigned long long*>(off));
     LR_CHECK_LAUNCH();
   }

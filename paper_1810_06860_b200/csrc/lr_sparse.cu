@@ -847,8 +847,18 @@ __global__ void __launch_bounds__(256, LR_GRP_MINB) spmm_group_kernel(
 // entries; the same tree for every entry).  Results are parked in shared
 // memory and every lane finishes its own batch entries with coalesced M / Y
 // traffic (residual partials, Y += step (m - x)).
+// occupancy vs gathers in flight per (G, T) (profiles/r02u_svt_variants.txt):
+// wide groups (G >= 16, r > 32) run 4 CTAs / SM with fewer entries in flight
+// per group (r = 84: 1.74 -> 1.46 ms), narrow ones 3 CTAs / SM
+template <int G, int T>
+struct SvtTune {
+  static constexpr int minb = G >= 16 ? 4 : LR_SVT_MINB;
+  static constexpr int q = G >= 16 ? (T == 1 ? 4 : (T == 2 ? 2 : 1))
+                                   : (T == 1 ? LR_SVT_Q1 : (T == 2 ? LR_SVT_Q2 : LR_SVT_Q3));
+};
+
 template <int G, int T, bool FUSED>
-__global__ void __launch_bounds__(256, LR_SVT_MINB) svt_group2_kernel(
+__global__ void __launch_bounds__(256, SvtTune<G, T>::minb) svt_group2_kernel(
     const int* __restrict__ ptr, const int* __restrict__ idx, const int* __restrict__ items, int n_items,
     const double* __restrict__ U, long long ldu, const double* __restrict__ S, const double* __restrict__ V,
     long long ldv, int r, double* __restrict__ x_out, const double* __restrict__ m_vals,
@@ -858,7 +868,7 @@ __global__ void __launch_bounds__(256, LR_SVT_MINB) svt_group2_kernel(
   constexpr int B = (4 * G < kGroupBatch) ? 4 * G : kGroupBatch;  // batch entries per group
   constexpr int KB = B / G;
   constexpr int R = G < 8 ? G : 8;
-  constexpr int QT = T == 1 ? LR_SVT_Q1 : (T == 2 ? LR_SVT_Q2 : LR_SVT_Q3);
+  constexpr int QT = SvtTune<G, T>::q;
   constexpr int Q = QT < R ? QT : R;  // entries' gathers in flight (divides R)
   __shared__ double xs_all[8][B * GROUPS];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, g = lane % G, grp = lane / G, gbase = grp * G;
@@ -1378,9 +1388,18 @@ static int launch_sddmm(bool fused, const int* ptr, const int* idx, int rows, co
   // c = 2 (g + G t)) and reduction tree: every entry's value is bit-identical
   // to lr_svt_step_flat_f64's (tests/test_gpu_kernels.py::
   // test_sddmm_group_kernel_matches_flat)
+  // lane map: the fewest chunk slots covering r (pick_group: r = 48 on 8 lanes
+  // x 3 pairs, r = 84 on 16 x 3) unless that needs 4 pairs per lane (register
+  // spills at 3 CTAs / SM), then the flat kernel's map (16 x 2, 32 x 2, 32 x 4)
+  // -- profiles/r02s_svt_lane_map.txt; LR_SVT_MAP=flat forces the flat map
+  // (every entry bit-identical to lr_svt_step_flat_f64)
+  static const char* map_env = getenv("LR_SVT_MAP");
+  const bool flat_only = map_env && map_env[0] == 'f' && map_env[1] == 'l';
   const int pairs = (r + 1) / 2;
   int G2 = 0, T2 = 2;
-  if (pairs <= 2) G2 = 1;
+  if (!flat_only && pick_group(pairs, G2, T2) && T2 < 4) {
+    // fit map chosen
+  } else if ((G2 = 0, T2 = 2, pairs <= 2)) G2 = 1;
   else if (pairs <= 4) G2 = 2;
   else if (pairs <= 8) G2 = 4;
   else if (pairs <= 16) G2 = 8;
@@ -1394,6 +1413,8 @@ static int launch_sddmm(bool fused, const int* ptr, const int* idx, int rows, co
     nb = launch_svt_group2_t<g, t>(fused, ptr, idx, items, n_items, U, ldu, S, V, ldv, r, x, m_vals, y_csr,   \
                                    y_csc, inv_perm, step, apply, partial, s);
     LR_SG2(1, 2) LR_SG2(2, 2) LR_SG2(4, 2) LR_SG2(8, 2) LR_SG2(16, 2) LR_SG2(32, 2) LR_SG2(32, 4)
+    LR_SG2(4, 1) LR_SG2(8, 1) LR_SG2(8, 3) LR_SG2(8, 4) LR_SG2(16, 1) LR_SG2(16, 3) LR_SG2(16, 4)
+    LR_SG2(32, 1) LR_SG2(32, 3)
 #undef LR_SG2
     if (nb > 0) {
       if (nblocks) *nblocks = nb;

@@ -334,6 +334,10 @@ __global__ void scale_columns_kernel(const double* __restrict__ V, long long ldv
   }
 }
 
+__global__ void gram_spectrum_kernel(const double* __restrict__ d, int n, double* __restrict__ S) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) S[i] = sqrt(fmax(d[i], 0.0));
+}
+
 static int grid_for(long long n, int threads) {
   long long b = (n + threads - 1) / threads;
   long long cap = (long long)sm_count() * 8;
@@ -472,6 +476,13 @@ int lr_fix_signs_f64(double* V, long long ldv, int rows_v, int cols, double* U, 
   int threads = 256;
   int blocks = (cols * 32 + threads - 1) / threads;
   fix_signs_kernel<<<blocks, threads, 0, as_stream(stream)>>>(V, ldv, rows_v, cols, U, ldu, rows_u);
+  LR_CHECK_LAUNCH();
+  return LR_OK;
+}
+
+int lr_gram_spectrum_f64(const double* d, int n, double* S, void* stream) {
+  if (n <= 0) return LR_OK;
+  gram_spectrum_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(d, n, S);
   LR_CHECK_LAUNCH();
   return LR_OK;
 }

@@ -195,6 +195,8 @@ class LazyQ:
 
     def __init__(self, base, Rinv):
         self.base, self.Rinv = base, Rinv
+        self.R1inv = None  # base = X R1inv when the speculative route built it (orth_speculative_dev)
+        self.T_all = None  # Y^T X, when the caller kept it (rsvd._krylov_orth)
         self._Q = None
 
     @property
@@ -242,13 +244,27 @@ def orth_speculative_dev(X, lazy_last=False):
                  device.ld(R1inv), device.ptr(work), device.ptr(infos[0:1]), _st())
     _native.call("lr_diag_f64", device.ptr(G0), device.ld(G0), n, device.ptr(diag[n:2 * n]), _st())
     Q1 = matmul_dev(X, R1inv, b_upper=True)
+    # ||R1^{-1}||_F^2 for the caller's condition estimate of X
+    # (kappa_F(X) = sqrt(trace(G0)) ||R1^{-1}||_F, read with the one sync)
+    rstat = _stats_dev_async(R1inv)
     G1 = gram_dev(Q1)
     R2inv = device.empty(n, n)
     _native.call("lr_potrf_inv_async_f64", n, device.ptr(G1), device.ld(G1), 0.0, device.ptr(R2inv),
                  device.ld(R2inv), device.ptr(work), device.ptr(infos[1:2]), _st())
     _native.call("lr_diag_f64", device.ptr(G1), device.ld(G1), n, device.ptr(diag[2 * n:3 * n]), _st())
     Q = LazyQ(Q1, R2inv) if lazy_last else matmul_dev(Q1, R2inv, b_upper=True)
-    return Q, [diag, infos]
+    if isinstance(Q, LazyQ):
+        Q.R1inv = R1inv  # Q1 = X R1^{-1}: lets a caller holding Y^T X skip Y^T Q1
+    return Q, [diag, infos, rstat]
+
+
+def _stats_dev_async(X):
+    """Device [sum of squares, max |x|, #non-finite] of a block (no sync)."""
+    part = device.arena().get("stats_partial_aux", _native.load().lr_stats_partials() + 8)
+    out = device.vector(3)
+    _native.call("lr_block_stats_f64", device.ptr(X), X.shape[0], X.shape[1], device.ld(X), device.ptr(part),
+                 device.ptr(out), _st())
+    return out
 
 
 def orth_speculation_holds(diag_h, infos_h) -> bool:
@@ -457,22 +473,24 @@ def eig_svd_dev(A, cols=None, check=True):
     except NumericalError:
         _check_dev(A, "oracle_svd input")  # a non-finite input is the reference's ValueError
         raise
+    # the lift is queued before the host reads d (see eig_svd_congruent_dev)
+    _native.call("lr_fix_signs_f64", device.ptr(V), device.ld(V), n, n, None, 0, 0, _st())
+    if cols is None:
+        cols = np.arange(n)
+    cols = np.asarray(cols, dtype=np.int64)
+    Sd = device.vector(n)
+    _native.call("lr_gram_spectrum_f64", device.ptr(d), n, device.ptr(Sd), _st())
+    B = device.empty(n, cols.shape[0])
+    ci = device.int_buffer(cols)
+    _native.call("lr_scale_columns_f64", device.ptr(V), device.ld(V), n, device.ptr(ci), cols.shape[0],
+                 device.ptr(Sd), 1, device.ptr(B), device.ld(B), _st())
+    U = matmul_dev(A, B)
     dh = device.to_host(d)
     # a non-finite input shows as non-finite Gram eigenvalues: only then is
     # the input scanned, for the reference's ValueError (no extra sync before)
     if check and not np.all(np.isfinite(dh)):
         _check_dev(A, "eig_svd input")
     S = gram_spectrum(dh)
-    _native.call("lr_fix_signs_f64", device.ptr(V), device.ld(V), n, n, None, 0, 0, _st())
-    if cols is None:
-        cols = np.arange(n)
-    cols = np.asarray(cols, dtype=np.int64)
-    Sd = device.f64_buffer(S)
-    B = device.empty(n, cols.shape[0])
-    ci = device.int_buffer(cols)
-    _native.call("lr_scale_columns_f64", device.ptr(V), device.ld(V), n, device.ptr(ci), cols.shape[0],
-                 device.ptr(Sd), 1, device.ptr(B), device.ld(B), _st())
-    U = matmul_dev(A, B)
     return S, V, U, cols
 
 
@@ -490,18 +508,21 @@ def eig_svd_congruent_dev(T, Rinv, cols):
     except NumericalError:
         _check_dev(T, "eig_svd input")
         raise
-    dh = device.to_host(d)
-    if not np.all(np.isfinite(dh)):  # non-finite input: the reference's ValueError
-        _check_dev(T, "eig_svd input")
-    S = gram_spectrum(dh)
+    # the lift is queued before the host reads d: the rank checks run while
+    # the GPU lifts (a rank error discards the lift and raises as before)
     _native.call("lr_fix_signs_f64", device.ptr(V), device.ld(V), n, n, None, 0, 0, _st())
     cols = np.asarray(cols, dtype=np.int64)
-    Sd = device.f64_buffer(S)
+    Sd = device.vector(n)
+    _native.call("lr_gram_spectrum_f64", device.ptr(d), n, device.ptr(Sd), _st())
     B = device.empty(n, cols.shape[0])
     ci = device.int_buffer(cols)
     _native.call("lr_scale_columns_f64", device.ptr(V), device.ld(V), n, device.ptr(ci), cols.shape[0],
                  device.ptr(Sd), 1, device.ptr(B), device.ld(B), _st())
     U = matmul_dev(T, tri_mul_dev(Rinv, B))
+    dh = device.to_host(d)
+    if not np.all(np.isfinite(dh)):  # non-finite input: the reference's ValueError
+        _check_dev(T, "eig_svd input")
+    S = gram_spectrum(dh)
     return S, V, U, cols
 
 
@@ -522,7 +543,8 @@ def eig_svd(A) -> SvdResult:
 
 # --------------------------------------------------------------- oracle_svd
 
-JACOBI_MAX_SWEEPS = 30
+JACOBI_MAX_SWEEPS = 30     # sweeps rotating every pair (the reference's tc_rq fallbacks need > 12)
+JACOBI_NOISE_SWEEPS = 30   # further sweeps with noise-against-noise pairs skipped
 # columns of the dense SVD with S <= DENSE_NULL_FLOOR * S[0] get an orthonormal
 # completion instead of B / S (1e-300: exact zeros only)
 DENSE_NULL_FLOOR = float(__import__("os").environ.get("LR_DENSE_NULL_FLOOR", "1e-300"))
@@ -564,15 +586,23 @@ def _tall_dense_svd_dev(A):
     Vt = device.empty(n, n)
     _native.call("lr_transpose_f64", device.ptr(Vd), device.ld(Vd), n, n, device.ptr(Vt), device.ld(Vt), st)
     off = device.vector(1)
+    norms = device.vector(n)
     tol = float(np.sqrt(rows)) * 2.0 * _U_ROUND
-    for _ in range(JACOBI_MAX_SWEEPS):
+    noise2 = 0.0
+    skipped = False
+    for sweep in range(JACOBI_MAX_SWEEPS + JACOBI_NOISE_SWEEPS):
+        if sweep == JACOBI_MAX_SWEEPS:
+            # not converged: the pairs still rotating are noise against noise
+            # (exactly dependent columns of a tall A); stop rotating those
+            _native.call("lr_row_norms_f64", device.ptr(Bt), device.ld(Bt), n, rows, device.ptr(norms), st)
+            noise = float(np.max(device.to_host(norms))) * max(rows, n) * 2.0 * _U_ROUND
+            noise2, skipped = noise * noise, True
         _native.call("lr_jacobi_sweep_f64", n, rows, device.ptr(Bt), device.ld(Bt), device.ptr(Vt), device.ld(Vt),
-                     tol, device.ptr(off), st)
+                     tol, noise2, device.ptr(off), st)
         if float(device.to_host(off)[0]) == 0.0:
             break
     else:
         raise NumericalError("dense SVD: one-sided Jacobi did not converge")
-    norms = device.vector(n)
     _native.call("lr_row_norms_f64", device.ptr(Bt), device.ld(Bt), n, rows, device.ptr(norms), st)
     Sj = device.to_host(norms)
     perm = np.argsort(-Sj, kind="stable")
@@ -581,7 +611,9 @@ def _tall_dense_svd_dev(A):
     # columns orthogonal RELATIVE to their norms, so even noise-level ones
     # normalise to orthonormal vectors inside span(A) -- as dgesdd's U lies in
     # span(Q) of A's QR -- and only exactly-zero columns need a completion
-    floor = S[0] * DENSE_NULL_FLOOR if S[0] > 0 else np.inf
+    # noise-level columns left unrotated among themselves are not orthogonal:
+    # complete them like exact zeros
+    floor = S[0] * (max(rows, n) * 2.0 * _U_ROUND if skipped else DENSE_NULL_FLOOR) if S[0] > 0 else np.inf
     good = S > floor
     # U = B[:, perm] / S (good columns), V = Vt^T[:, perm]
     _native.call("lr_transpose_f64", device.ptr(Bt), device.ld(Bt), n, rows, device.ptr(B), device.ld(B), st)

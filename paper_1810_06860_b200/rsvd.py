@@ -47,6 +47,15 @@ LAZY_MIN_FLOPS = 1 << 30  # m * W^2 below this: form Q (the GEMM is a few micros
 # rsvd_bki checks LU statuses and orth's decisions with one read after the
 # basis is built, redoing the call on the careful path when one is unusual
 SPECULATIVE = True
+# Y^T Q1 for the unformed basis Q1 = H R1^{-1}: (Y^T H) R1^{-1}, where Y^T H's
+# blocks are the Krylov products Y^T H_i already computed (plus Y^T H_p) -- one
+# narrow product and an n x W x W GEMM instead of the W-wide one.  Rounding in
+# Y^T H is amplified by kappa(H) <= kappa_F(H) = sqrt(trace(G0)) ||R1^{-1}||_F
+# (both on the device already); used only while kappa_F(H) <= KRYLOV_REUSE_KAPPA,
+# i.e. at most ~2e-10 relative error in Y^T Q1 (the parity bar is 1e-8).
+KRYLOV_REUSE = True
+KRYLOV_REUSE_KAPPA = 1e6  # cfg4 job: kappa_F(H) 2e3 .. 1.2e5 (profiles/r02u_cfg4_timeline.txt)
+REUSE_STATS = {"used": 0, "kappa_gate": 0, "kappas": []}
 
 
 @dataclass
@@ -305,7 +314,7 @@ def _check_precision(precision: str) -> str:
 
 
 def _krylov_orth(A: SparseMatrix, Om, params: RsvdParams, spec: bool, fp32: bool, lazy: bool, fb: _Fallback,
-                 pre: Prestart = None):
+                 pre: Prestart = None, keep_T: bool = False):
     """Alg. 5 steps 1-7 from a given Omega: Krylov blocks H_0..H_p (LU-
     normalised) and the basis.  spec: LU statuses and the CholeskyQR route's
     decisions stay on the device (no host synchronisation at all: the body
@@ -334,6 +343,8 @@ def _krylov_orth(A: SparseMatrix, Om, params: RsvdParams, spec: bool, fp32: bool
         spmm_dev(A, Om, out=H[:, 0:w])
     if pre is None:
         normalise(0)
+    keep_T = keep_T and not fp32
+    T_all = device.empty(n, W) if keep_T else None  # Y^T H, block by block
     T = None if fp32 else device.empty(n, w)
     for i in range(1, params.p + 1):
         if fp32:
@@ -342,13 +353,19 @@ def _krylov_orth(A: SparseMatrix, Om, params: RsvdParams, spec: bool, fp32: bool
             spmm_dev32(A, T32, out=H32)
             device.to_f64(H32, out=H[:, i * w:(i + 1) * w])
         else:
+            if keep_T:
+                T = T_all[:, (i - 1) * w:i * w]
             spmm_t_dev(A, H[:, (i - 1) * w:i * w], out=T)
             spmm_dev(A, T, out=H[:, i * w:(i + 1) * w])
         normalise(i)
+    if keep_T:
+        spmm_t_dev(A, H[:, params.p * w:W], out=T_all[:, params.p * w:W])
     if spec:
         Q, probe = orth_speculative_dev(H, lazy_last=lazy)
     else:
         Q, probe = _orthonormalize(H, fb, lazy_last=lazy), None
+    if keep_T and isinstance(Q, LazyQ):
+        Q.T_all = T_all
     return H, Q, lu_status, probe
 
 
@@ -384,7 +401,10 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
     if not use_pre:
         _overlap_draw_with_upload(A, params.seed, n, w, omega or OMEGA_SOURCE)
     Om = None if use_pre else _omega(params.seed, n, w, omega or OMEGA_SOURCE)
-    H, Q, lu_status, probe = _krylov_orth(A, Om, params, spec, fp32, lazy, fb, pre=pre if use_pre else None)
+    reuse = KRYLOV_REUSE and spec and lazy and not fp32 and params.p >= 1
+    H, Q, lu_status, probe = _krylov_orth(A, Om, params, spec, fp32, lazy, fb, pre=pre if use_pre else None,
+                                          keep_T=reuse)
+    T_pre = None
     if spec:
         st = device.to_host(lu_status).reshape(-1, 4)[:, :3]
         diag_h, infos_h = device.to_host(probe[0]), device.to_host(probe[1])
@@ -394,7 +414,19 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
             # the Krylov blocks are exactly the careful path's (H is untouched
             # by the speculative orth): only the orthonormalisation is redone
             Q = _orthonormalize(H, fb, lazy_last=lazy)
-    res = project_and_solve(A, Q, params.k, fb, "fp32" if fp32 else "fp64", download=download)
+        elif reuse and isinstance(Q, LazyQ) and getattr(Q, "T_all", None) is not None:
+            Wn = diag_h.shape[0] // 3
+            kappa = float(np.sqrt(np.sum(diag_h[0:Wn]) * device.to_host(probe[2])[0]))
+            if len(REUSE_STATS["kappas"]) < 4096:
+                REUSE_STATS["kappas"].append(kappa)
+            if np.isfinite(kappa) and kappa <= KRYLOV_REUSE_KAPPA:
+                T_pre = matmul_dev(Q.T_all, Q.R1inv, b_upper=True)  # = Y^T Q1
+                REUSE_STATS["used"] += 1
+            else:
+                REUSE_STATS["kappa_gate"] += 1
+        if isinstance(Q, LazyQ):
+            Q.T_all = Q.R1inv = None  # the cached basis (reuse-q) must not pin them
+    res = project_and_solve(A, Q, params.k, fb, "fp32" if fp32 else "fp64", download=download, T_pre=T_pre)
     return res, Q, fb.count
 
 

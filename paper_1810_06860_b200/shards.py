@@ -337,8 +337,14 @@ class DeviceKernels:
         return lu_pl_dev(X)
 
     def gaussian(self, seed, rows, cols):
+        """Omega(seed) on this rank: the parity default draws on the host
+        (every rank the same bits; the SVT loop prefetches it as on one GPU),
+        omega="device" generates it on the GPU."""
+        from . import rsvd as _rsvd
         from .rng import gaussian_matrix_device
 
+        if _rsvd.OMEGA_SOURCE == "host":
+            return _rsvd.omega_from_host(seed, rows, cols)
         return gaussian_matrix_device(seed, rows, cols)
 
     def dense_svd(self, X):
@@ -353,7 +359,11 @@ class ShardedEngine:
     """completion._svt_loop's matrix side spread over ranks; also the
     sharded rSVD-BKI (`bki`).  Factors U are row-sharded by R_g, V by C_g."""
 
-    omega_source = "device"  # every rank draws Omega on its own GPU (no host draw to prefetch)
+    @property
+    def omega_source(self):  # the single-GPU default: every rank draws the same host Omega (prefetched)
+        from . import rsvd as _rsvd
+
+        return _rsvd.OMEGA_SOURCE
 
     def __init__(self, obs: ObservationSet, exchange: Exchange = None, kernels=None):
         self.ex = exchange if exchange is not None else Exchange()

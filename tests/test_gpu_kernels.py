@@ -363,6 +363,16 @@ def test_oracle_svd_matches_lapack(golden):
     assert np.max(np.abs(r.S - S_ref)) <= 1e-12 * S_ref[0]
     assert r.S[-1] <= 1e-14 * r.S[0]
     assert rel((r.U * r.S) @ r.V.T, X) <= 1e-13
+    # a tall block with exactly dependent columns (the BKI fallback's case): the
+    # noise-level columns need not converge among themselves
+    rng4 = np.random.default_rng(5)
+    Xt = rng4.standard_normal((60000, 40))
+    Xt[:, 30:] = Xt[:, :10] * 3.0
+    r = oracle_svd(Xt)
+    S_ref = np.linalg.svd(Xt, compute_uv=False)
+    assert np.max(np.abs(r.S - S_ref)) <= 1e-12 * S_ref[0]
+    assert rel(r.U.T @ r.U, np.eye(40)) <= 1e-12 and rel(r.V.T @ r.V, np.eye(40)) <= 1e-12
+    assert rel((r.U * r.S) @ r.V.T, Xt) <= 1e-13
     # graded spectrum down to 1e-14 s_max, tall and wide
     rng = np.random.default_rng(9)
     Uq, _ = np.linalg.qr(rng.standard_normal((400, 30)))
@@ -466,10 +476,11 @@ def test_convert_roundtrip_and_rounding():
 @pytest.mark.parametrize("r", [1, 3, 5, 9, 17, 24, 33, 48, 65, 84, 130, 200, 256])
 def test_sddmm_group_kernel_matches_flat(r):
     """The line-aligned group kernel behind lr_sddmm_f64 / lr_svt_step_f64 (the
-    product default) uses the flat kernel's lane map and reduction tree: every
-    sampled entry, and so every updated value of Y, is bit-identical to
-    lr_sddmm_flat_f64 / lr_svt_step_flat_f64 -- on rows split into items, empty
-    rows and a Zipf-like long row."""
+    product default) against the flat kernel (lr_sddmm_flat_f64 /
+    lr_svt_step_flat_f64) and numpy: sampled entries and updated values of Y
+    agree to rounding (bit-identical where the two lane maps coincide; the
+    group kernel fits its map to r) -- on rows split into items, empty rows
+    and a Zipf-like long row."""
     import torch
 
     from paper_1810_06860_b200 import _native, device
@@ -491,9 +502,9 @@ def test_sddmm_group_kernel_matches_flat(r):
     _native.call("lr_sddmm_f64", device.ptr(dp.csr.ptr), device.ptr(dp.csr.idx), m, device.ptr(dp.csr.items),
                  dp.csr.n_items, device.ptr(U), device.ld(U), device.ptr(S), device.ptr(V), device.ld(V), r,
                  device.ptr(x_grp), st)
-    assert torch.equal(x_flat, x_grp)
     ref = np.einsum("er,er->e", device.to_host(U)[A.coo_rows()] * device.to_host(S), device.to_host(V)[A.indices])
     assert rel(device.to_host(x_grp), ref) <= 1e-14
+    assert rel(device.to_host(x_flat), device.to_host(x_grp)) <= 1e-14
     # fused step through both entry points: identical Y
     m_vals = A.device_values()[0]
     ys = []
@@ -512,7 +523,7 @@ def test_sddmm_group_kernel_matches_flat(r):
                          device.ptr(m_vals), device.ptr(y), None, device.ptr(dp.inv_perm), 0.37, 1, device.ptr(part),
                          npart, device.ptr(out2), st)
         ys.append((y, float(np.sqrt(device.to_host(out2)[0]))))
-    assert torch.equal(ys[0][0], ys[1][0])
+    assert rel(device.to_host(ys[0][0]), device.to_host(ys[1][0])) <= 1e-15
     assert abs(ys[0][1] - ys[1][1]) <= 1e-13 * ys[0][1]
 
 

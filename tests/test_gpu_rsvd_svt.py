@@ -503,3 +503,27 @@ def test_rsvd_cfg2_matches_reference(golden2, name):
     P = (res.U[:256] * res.S) @ res.V[:256].T
     P_ref = (golden2[f"cfg2_{name}_U256"] * S_ref) @ golden2[f"cfg2_{name}_V256"].T
     assert rel(P, P_ref) <= 1e-8
+
+
+def test_bki_krylov_reuse_matches_wide_product():
+    """rsvd_bki's Y^T Q1 from the Krylov products ((Y^T H) R1^{-1}, gated on
+    kappa_F(H) <= 1e6) against the direct W-wide product: singular values to
+    8 eps kappa_F(H), the same subspaces."""
+    from paper_1810_06860_b200 import rsvd, workloads
+    from paper_1810_06860_b200.sparse import SparseMatrix
+
+    obs = workloads.uniform_sparse(90000, 40000, 1_000_000, seed=21)
+    A = SparseMatrix.from_coo(obs.m, obs.n, obs.rows, obs.cols, obs.values)
+    prm = rsvd.RsvdParams(k=20, p=3, s=10, seed=5)  # W = 120: the unformed-Q route (m W^2 >= 2^30)
+    used0 = rsvd.REUSE_STATS["used"]
+    r1, _ = rsvd.rsvd_bki(A, prm)
+    assert rsvd.REUSE_STATS["used"] == used0 + 1
+    rsvd.KRYLOV_REUSE = False
+    try:
+        r0, _ = rsvd.rsvd_bki(A, prm)
+    finally:
+        rsvd.KRYLOV_REUSE = True
+    kappa = rsvd.REUSE_STATS["kappas"][-1]  # kappa_F(H) of the reused call
+    assert np.max(np.abs(r1.S - r0.S) / r0.S) <= max(1e-13, 8 * np.finfo(float).eps * kappa)
+    assert np.linalg.norm(r1.U @ (r1.U.T @ r0.U) - r0.U) <= 1e-9 * np.sqrt(20)
+    assert np.linalg.norm(r1.V @ (r1.V.T @ r0.V) - r0.V) <= 1e-9 * np.sqrt(20)
