@@ -327,7 +327,8 @@ static int choose_splits_t(int M, int N, int K, int flags) {
 // of 32x32 (16 warps/SM keep the DMMA pipe fed through the fragment loads),
 // 2 = 128x128 / 8 warps of 64x32, 3 = 0 with BK 32 / 2 stages (half the
 // barriers per DMMA), 4 = 1 with BK 32 / 2 stages, 5 = 64x128 / 4 warps of
-// 32x64.  Measured (tools/gemm_probe.py, profiles/r01_gemm_variants.txt):
+// 32x64, 6 = the TMA / mbarrier warp-specialised mainloop (lr_gemm_tma.cu).
+// Measured (tools/gemm_probe.py, profiles/r01_gemm_variants.txt):
 // A^T B (Gram) is fastest on 3 (1.95 ms at 100000 x 660; 0: 2.00, 1: 2.15),
 // A B on 4 (H R^{-1} 2.00 -> 1.77 ms, H V 0.70 -> 0.60 ms).  LR_GEMM_TILE
 // overrides.
@@ -337,9 +338,24 @@ static int large_variant(int transA) {
   return transA ? 3 : 4;
 }
 
+bool gemm_tma_launch(int transA, int M, int N, int K, double alpha, const double* A, long long lda,
+                     const double* B, long long ldb, double beta, double* C, long long ldc, int flags, double* work,
+                     int S, int k_chunk, cudaStream_t s);
+int gemm_tma_occupancy();
+
 static int choose_splits(int transA, int M, int N, int K, int flags) {
   if (!transA) return 1;
   if (!use_large(M, N, K, flags)) return choose_splits_t<TileS, true>(M, N, K, flags);
+  if (large_variant(1) == 6) {  // TMA mainloop: 128 x 64 tiles
+    using T = TileL32;
+    long long tiles = (flags & LR_GEMM_SYRK_UPPER) ? upper_tiles<T>(M, N)
+                                                   : (long long)((M + T::BM - 1) / T::BM) * ((N + T::BN - 1) / T::BN);
+    const long long cap = (long long)sm_count() * gemm_tma_occupancy();
+    long long sp = tiles >= cap ? 1 : cap / tiles;
+    const long long smax = (K + 511) / 512;
+    if (sp > smax) sp = smax;
+    return (int)(sp < 1 ? 1 : sp);
+  }
   switch (large_variant(1)) {
     case 1: return choose_splits_t<TileL8, true>(M, N, K, flags);
     case 2: return choose_splits_t<TileW, true>(M, N, K, flags);
@@ -391,7 +407,10 @@ int lr_gemm_f64(int transA, int M, int N, int K, double alpha, const double* A, 
   const bool large = use_large(M, N, K, flags);
   const int variant = large_variant(transA);
 #define LR_GEMM_ARGS M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, flags, work, S, k_chunk, vec16, s
-  if (transA) {
+  if (large && variant == 6 &&
+      gemm_tma_launch(transA, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, flags, work, S, k_chunk, s)) {
+    // TMA + mbarrier mainloop (lr_gemm_tma.cu)
+  } else if (transA) {
     if (!large)
       launch<TileS, true>(LR_GEMM_ARGS);
     else if (variant == 1)

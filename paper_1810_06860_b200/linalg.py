@@ -455,7 +455,7 @@ def gram_spectrum(dh):
     return np.sqrt(np.maximum(dh, 0.0))
 
 
-def eig_svd_dev(A, cols=None, check=True):
+def eig_svd_dev(A, cols=None, check=True, defer=False):
     """Gram-route SVD of tall A (linalg.py:172-202), device in/out.
 
     Returns (S_host ascending (all n), V (n x n, sign rule applied),
@@ -485,16 +485,21 @@ def eig_svd_dev(A, cols=None, check=True):
     _native.call("lr_scale_columns_f64", device.ptr(V), device.ld(V), n, device.ptr(ci), cols.shape[0],
                  device.ptr(Sd), 1, device.ptr(B), device.ld(B), _st())
     U = matmul_dev(A, B)
-    dh = device.to_host(d)
-    # a non-finite input shows as non-finite Gram eigenvalues: only then is
-    # the input scanned, for the reference's ValueError (no extra sync before)
-    if check and not np.all(np.isfinite(dh)):
-        _check_dev(A, "eig_svd input")
-    S = gram_spectrum(dh)
-    return S, V, U, cols
+
+    def finish():
+        dh = device.to_host(d)
+        # a non-finite input shows as non-finite Gram eigenvalues: only then is
+        # the input scanned, for the reference's ValueError (no extra sync before)
+        if check and not np.all(np.isfinite(dh)):
+            _check_dev(A, "eig_svd input")
+        return gram_spectrum(dh)
+
+    if defer:  # the caller queues more work first; finish() reads d and checks the rank
+        return finish, V, U, cols
+    return finish(), V, U, cols
 
 
-def eig_svd_congruent_dev(T, Rinv, cols):
+def eig_svd_congruent_dev(T, Rinv, cols, defer=False):
     """eig_svd_dev of A = T Rinv without forming A (Rinv upper triangular,
     W x W): Gram(A) = Rinv^T Gram(T) Rinv (two W^3 products instead of an
     n x W x W one), U_sel = T (Rinv V[:, cols] / S[cols]).  Same returns as
@@ -519,11 +524,16 @@ def eig_svd_congruent_dev(T, Rinv, cols):
     _native.call("lr_scale_columns_f64", device.ptr(V), device.ld(V), n, device.ptr(ci), cols.shape[0],
                  device.ptr(Sd), 1, device.ptr(B), device.ld(B), _st())
     U = matmul_dev(T, tri_mul_dev(Rinv, B))
-    dh = device.to_host(d)
-    if not np.all(np.isfinite(dh)):  # non-finite input: the reference's ValueError
-        _check_dev(T, "eig_svd input")
-    S = gram_spectrum(dh)
-    return S, V, U, cols
+
+    def finish():
+        dh = device.to_host(d)
+        if not np.all(np.isfinite(dh)):  # non-finite input: the reference's ValueError
+            _check_dev(T, "eig_svd input")
+        return gram_spectrum(dh)
+
+    if defer:
+        return finish, V, U, cols
+    return finish(), V, U, cols
 
 
 def tri_mul_dev(Rinv, B):

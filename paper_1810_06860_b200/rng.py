@@ -237,16 +237,74 @@ def prefetch_normals(seed: int, rows: int, cols: int) -> None:
     from concurrent.futures import Future
 
     fut = Future()
+    dev_index = _current_device_index()
 
     def run():
         try:
             sup = _superset_for(*key)
-            fut.set_result(_pinned_from_superset(sup, key[2]) if sup is not None else _pinned_normals(*key))
+            host = _pinned_from_superset(sup, key[2]) if sup is not None else _pinned_normals(*key)
+            fut.set_result(_Drawn(host, *(_upload_async(host, key[1] * key[2], dev_index)
+                                          if dev_index is not None else (None, None))))
         except BaseException as exc:  # pragma: no cover - surfaced by take_normals
             fut.set_exception(exc)
 
     threading.Thread(target=run, daemon=True, name="lr-omega-prefetch").start()
     _PREFETCH[key] = fut
+
+
+class _Drawn:
+    """A prefetched draw: the pinned host block and, when a GPU is present,
+    its device copy made on the upload stream (event `ready`)."""
+
+    def __init__(self, host, dev, ready):
+        self.host, self.dev, self.ready = host, dev, ready
+
+
+_UPLOAD_STREAM = {}
+
+
+def _current_device_index():
+    try:
+        import torch
+
+        if not torch.cuda.is_available():
+            return None
+        return torch.cuda.current_device()
+    except Exception:
+        return None
+
+
+def _upload_async(host, count: int, dev_index: int):
+    """In the prefetch thread: the draw's host->device copy on a dedicated
+    stream, so it overlaps the GPU's current work instead of following the
+    host's wait for the draw."""
+    import torch
+
+    torch.cuda.set_device(dev_index)
+    st = _UPLOAD_STREAM.get(dev_index)
+    if st is None:
+        st = _UPLOAD_STREAM.setdefault(dev_index, torch.cuda.Stream(device=dev_index))
+    with torch.cuda.stream(st):
+        dev = torch.empty(max(count, 1), dtype=torch.float64, device=torch.device("cuda", dev_index))
+        if count:
+            dev[:count].copy_(host[:count], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(st)
+    return dev, ev
+
+
+def take_normals_device(seed: int, rows: int, cols: int):
+    """(device vector, event) of a prefetched draw already copied to the GPU,
+    or None (nothing prefetched, or no device copy made)."""
+    key = (int(seed), int(rows), int(cols))
+    fut = _PREFETCH.get(key)
+    if fut is None:
+        return None
+    d = fut.result()
+    if d.dev is None:
+        return None
+    _PREFETCH.pop(key, None)
+    return d.dev, d.ready
 
 
 class Superset:
@@ -373,7 +431,7 @@ def take_normals(seed: int, rows: int, cols: int):
     drawn now."""
     fut = _PREFETCH.pop((int(seed), int(rows), int(cols)), None)
     if fut is not None:
-        return fut.result()
+        return fut.result().host
     sup = _superset_for(seed, rows, cols)
     if sup is not None:
         return _pinned_from_superset(sup, cols)

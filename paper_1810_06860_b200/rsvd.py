@@ -164,13 +164,23 @@ def omega_from_host(seed: int, n: int, w: int):
     rng.normals_column_major) into page-locked memory in draw (column-major)
     order, uploaded, and transposed into the row-major device block on the
     GPU (lr_transpose_f64) -- the host never does the strided transpose."""
-    from .rng import take_normals
+    import torch
+
+    from .rng import take_normals, take_normals_device
 
     device.require_cuda()
     count = n * w
-    host = take_normals(seed, n, w)
-    Zt = device.vector(count).view(w, n) if count else device.empty(w, n)
-    Zt.view(-1).copy_(host[:count], non_blocking=True)
+    pre = take_normals_device(seed, n, w)
+    if pre is not None:  # the prefetch thread already copied it (upload stream)
+        dv, ready = pre
+        cur = torch.cuda.current_stream()
+        cur.wait_event(ready)
+        dv.record_stream(cur)
+        Zt = dv[:max(count, 1)].view(w, n) if count else device.empty(w, n)
+    else:
+        host = take_normals(seed, n, w)
+        Zt = device.vector(count).view(w, n) if count else device.empty(w, n)
+        Zt.view(-1).copy_(host[:count], non_blocking=True)
     device.TRAFFIC["h2d"] += 8 * count
     Om = device.empty(n, w)
     _native.call("lr_transpose_f64", device.ptr(Zt), n, w, n, device.ptr(Om), device.ld(Om), device.stream())
@@ -207,37 +217,52 @@ def _orthonormalize(X, fb: _Fallback, lazy_last=False):
         return oracle_svd_dev(X)[0]
 
 
-def _windowed_small_svd(Bt, idx, fb: _Fallback, Rinv=None):
+def _windowed_small_svd(Bt, idx, fb: _Fallback, Rinv=None, defer=False):
     """eig_svd of Bt (n x W) keeping the ascending-order columns idx (given in
     the output order).  Returns (S_sel host, V_small[:, idx] device,
     U_small[:, idx] device).  Falls back to the dense SVD (ascending).
     With Rinv the matrix is Bt @ Rinv, never formed unless the fallback
-    needs it."""
+    needs it.  defer: returns (finish, Vsel, Usel) with the work queued and
+    finish() -> (S_sel, Vsel, Usel) reading the eigenvalues (the rank check
+    and the fallback happen there)."""
     try:
         if Rinv is None:
-            S, V, U, cols = eig_svd_dev(Bt, cols=idx)
+            fin, V, U, cols = eig_svd_dev(Bt, cols=idx, defer=True)
         else:
-            S, V, U, cols = eig_svd_congruent_dev(Bt, Rinv, idx)
+            fin, V, U, cols = eig_svd_congruent_dev(Bt, Rinv, idx, defer=True)
         Vsel = device.empty(V.shape[0], len(idx))
         ci = device.int_buffer(cols)
         _native.call("lr_scale_columns_f64", device.ptr(V), device.ld(V), V.shape[0], device.ptr(ci), len(idx),
                      None, 0, device.ptr(Vsel), device.ld(Vsel), device.stream())
-        return S[cols], Vsel, U
     except RankDeficiencyError as exc:
-        fb.fail(exc)
-        if Rinv is not None:
-            Bt = matmul_dev(Bt, Rinv, b_upper=True)
-        Ud, Sd, Vd = oracle_svd_dev(Bt)  # descending
-        W = Bt.shape[1]
-        desc = W - 1 - np.asarray(idx)  # ascending index -> descending position
-        ci = device.int_buffer(desc)
-        Vsel = device.empty(Vd.shape[0], len(idx))
-        Usel = device.empty(Ud.shape[0], len(idx))
-        _native.call("lr_scale_columns_f64", device.ptr(Vd), device.ld(Vd), Vd.shape[0], device.ptr(ci), len(idx),
-                     None, 0, device.ptr(Vsel), device.ld(Vsel), device.stream())
-        _native.call("lr_scale_columns_f64", device.ptr(Ud), device.ld(Ud), Ud.shape[0], device.ptr(ci), len(idx),
-                     None, 0, device.ptr(Usel), device.ld(Usel), device.stream())
-        return Sd[desc], Vsel, Usel
+        out = _windowed_fallback(Bt, idx, fb, Rinv, exc)
+        return (lambda: out, out[1], out[2]) if defer else out
+
+    def finish():
+        try:
+            return fin()[cols], Vsel, U
+        except RankDeficiencyError as exc:
+            return _windowed_fallback(Bt, idx, fb, Rinv, exc)
+
+    return (finish, Vsel, U) if defer else finish()
+
+
+def _windowed_fallback(Bt, idx, fb: _Fallback, Rinv, exc):
+    """_windowed_small_svd's dense-SVD route after a rank failure."""
+    fb.fail(exc)
+    if Rinv is not None:
+        Bt = matmul_dev(Bt, Rinv, b_upper=True)
+    Ud, Sd, Vd = oracle_svd_dev(Bt)  # descending
+    W = Bt.shape[1]
+    desc = W - 1 - np.asarray(idx)  # ascending index -> descending position
+    ci = device.int_buffer(desc)
+    Vsel = device.empty(Vd.shape[0], len(idx))
+    Usel = device.empty(Ud.shape[0], len(idx))
+    _native.call("lr_scale_columns_f64", device.ptr(Vd), device.ld(Vd), Vd.shape[0], device.ptr(ci), len(idx),
+                 None, 0, device.ptr(Vsel), device.ld(Vsel), device.stream())
+    _native.call("lr_scale_columns_f64", device.ptr(Ud), device.ld(Ud), Ud.shape[0], device.ptr(ci), len(idx),
+                 None, 0, device.ptr(Usel), device.ld(Usel), device.stream())
+    return Sd[desc], Vsel, Usel
 
 
 def _spmm_t_prec(Y: SparseMatrix, X, precision: str):
@@ -248,24 +273,36 @@ def _spmm_t_prec(Y: SparseMatrix, X, precision: str):
 
 
 def project_and_solve(Y: SparseMatrix, Q, k: int, fb: _Fallback, precision: str = "fp64",
-                      download: bool = False, T_pre=None):
+                      download: bool = False, T_pre=None, defer=False):
     """B^T = Y^T Q, small SVD, lift: the shared tail of Alg. 5 steps 8-10,
     recycle_q and rsvd_pi.  Returns the top-k DevSvd (descending).
-    download: V's device->host copy starts (side stream) before U is lifted."""
+    download: V's device->host copy starts (side stream) before U is lifted.
+    defer: everything is queued and a callable returned; calling it reads the
+    eigenvalues (rank check, dense fallback if needed) and gives the DevSvd."""
     W = int(Q.shape[1])
     idx = np.arange(W - 1, W - k - 1, -1)  # top-k of the ascending order, descending
-    if isinstance(Q, LazyQ):
+    lazy = isinstance(Q, LazyQ)
+    if lazy:
         # Q = Q1 Rinv unformed: B^T = (Y^T Q1) Rinv, U = Q1 (Rinv V_small)
         T = T_pre if T_pre is not None else _spmm_t_prec(Y, Q.base, precision)
-        S_sel, Vsel, Usel = _windowed_small_svd(T, idx, fb, Rinv=Q.Rinv)
-        pend = device.to_host_async(Usel) if download else None
-        U = matmul_dev(Q.base, matmul_dev(Q.Rinv, Vsel))
+        fin, Vsel, Usel = _windowed_small_svd(T, idx, fb, Rinv=Q.Rinv, defer=True)
     else:
         Bt = T_pre if T_pre is not None else _spmm_t_prec(Y, Q, precision)
-        S_sel, Vsel, Usel = _windowed_small_svd(Bt, idx, fb)
-        pend = device.to_host_async(Usel) if download else None
-        U = matmul_dev(Q, Vsel)
-    return DevSvd(U, device.f64_buffer(S_sel), Usel, np.asarray(S_sel, dtype=np.float64), pend)
+        fin, Vsel, Usel = _windowed_small_svd(Bt, idx, fb, defer=True)
+
+    def lift(Vs, Us):
+        pend = device.to_host_async(Us) if download else None
+        U = matmul_dev(Q.base, matmul_dev(Q.Rinv, Vs)) if lazy else matmul_dev(Q, Vs)
+        return U, pend
+
+    U, pend = lift(Vsel, Usel)
+
+    def finish():
+        S_sel, Vs, Us = fin()
+        U2, pend2 = (U, pend) if Vs is Vsel else lift(Vs, Us)  # the fallback replaced the small factors
+        return DevSvd(U2, device.f64_buffer(S_sel), Us, np.asarray(S_sel, dtype=np.float64), pend2)
+
+    return finish if defer else finish()
 
 
 class Prestart:
@@ -405,6 +442,13 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
     H, Q, lu_status, probe = _krylov_orth(A, Om, params, spec, fp32, lazy, fb, pre=pre if use_pre else None,
                                           keep_T=reuse)
     T_pre = None
+    fin_spec = None
+    if spec and reuse and isinstance(Q, LazyQ) and getattr(Q, "T_all", None) is not None:
+        # queue the projection on the reused Krylov products before the one
+        # host read of this call (LU statuses, orth decisions, kappa): it
+        # stands when all of them hold (the common case), else it is dropped
+        fin_spec = project_and_solve(A, Q, params.k, fb, "fp64", download=download,
+                                     T_pre=matmul_dev(Q.T_all, Q.R1inv, b_upper=True), defer=True)
     if spec:
         st = device.to_host(lu_status).reshape(-1, 4)[:, :3]
         diag_h, infos_h = device.to_host(probe[0]), device.to_host(probe[1])
@@ -420,12 +464,14 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
             if len(REUSE_STATS["kappas"]) < 4096:
                 REUSE_STATS["kappas"].append(kappa)
             if np.isfinite(kappa) and kappa <= KRYLOV_REUSE_KAPPA:
-                T_pre = matmul_dev(Q.T_all, Q.R1inv, b_upper=True)  # = Y^T Q1
                 REUSE_STATS["used"] += 1
-            else:
-                REUSE_STATS["kappa_gate"] += 1
+                res = fin_spec()  # the speculatively queued projection stands
+                if isinstance(Q, LazyQ):
+                    Q.T_all = Q.R1inv = None  # the cached basis (reuse-q) must not pin them
+                return res, Q, fb.count
+            REUSE_STATS["kappa_gate"] += 1
         if isinstance(Q, LazyQ):
-            Q.T_all = Q.R1inv = None  # the cached basis (reuse-q) must not pin them
+            Q.T_all = Q.R1inv = None
     res = project_and_solve(A, Q, params.k, fb, "fp32" if fp32 else "fp64", download=download, T_pre=T_pre)
     return res, Q, fb.count
 

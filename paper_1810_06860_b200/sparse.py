@@ -263,7 +263,7 @@ class SparseMatrix:
     @classmethod
     def from_coo_device(cls, rows: int, cols: int, i, j, v, split=None, tag: int = 0,
                         range_msg=("coordinate out of range", "coordinate out of range"),
-                        dup_msg=None) -> "SparseMatrix":
+                        dup_msg=None, uploaded=None) -> "SparseMatrix":
         """from_coo on the device (lr_coo_to_csr_i32: bounds, duplicates, row
         buckets + per-row column sort -- the same CSR as the host lexsort, bit
         for bit).  The host keeps only indptr (the work schedule needs it);
@@ -281,12 +281,9 @@ class SparseMatrix:
             return cls.from_coo(rows, cols, *_select(i, j, v, split, tag))
         dev = device.require_cuda()
         st = device.stream()
-        di = device.upload_async_i64(i)
-        dj = device.upload_async_i64(j)
-        dv = device.f64_buffer(np.asarray(v, dtype=np.float64))
-        ds = None
-        if split is not None:
-            ds = torch.from_numpy(np.ascontiguousarray(split, dtype=np.uint8)).to(dev, non_blocking=True)
+        if uploaded is None:
+            uploaded = _upload_coo(i, j, v, split)
+        di, dj, dv, ds = uploaded
         i32 = torch.int32
         ptr = torch.empty(rows + 1, dtype=i32, device=dev)
         col = torch.empty(max(count, 1), dtype=i32, device=dev)
@@ -547,6 +544,19 @@ class SparseMatrix:
 
 
 # --------------------------------------------------------------- kernels
+
+def _upload_coo(i, j, v, split=None):
+    """Device copies of COO triples (+ split tags), asynchronous from pinned
+    host arrays."""
+    dev = device.require_cuda()
+    di = device.upload_async_i64(i)
+    dj = device.upload_async_i64(j)
+    dv = device.f64_buffer(np.asarray(v, dtype=np.float64))
+    ds = None
+    if split is not None:
+        ds = torch.from_numpy(np.ascontiguousarray(split, dtype=np.uint8)).to(dev, non_blocking=True)
+    return di, dj, dv, ds
+
 
 def _select(i, j, v, split, tag):
     if split is None:
@@ -883,12 +893,15 @@ class ObservationSet:
             raise DataError("observation values must be finite")
         if np.any(self.split > 1):
             raise DataError("split tags must be 0 (train) or 1 (test)")
+        up = _upload_coo(self.rows, self.cols, self.values, self.split)  # once for both splits
         self._train_dev = SparseMatrix.from_coo_device(self.m, self.n, self.rows, self.cols, self.values, self.split,
                                                        self.TRAIN, range_msg=msgs,
-                                                       dup_msg="duplicate (row, col) within train split")
+                                                       dup_msg="duplicate (row, col) within train split",
+                                                       uploaded=up)
         if np.any(self.split == self.TEST):
             SparseMatrix.from_coo_device(self.m, self.n, self.rows, self.cols, self.values, self.split, self.TEST,
-                                         range_msg=msgs, dup_msg="duplicate (row, col) within test split")
+                                         range_msg=msgs, dup_msg="duplicate (row, col) within test split",
+                                         uploaded=up)
 
     @property
     def count(self) -> int:

@@ -36,9 +36,26 @@ ref = sub @ X
 err = np.linalg.norm(Yx[rows] - ref) / np.linalg.norm(ref)
 print(f"SpMM spot check (2000 rows, w = 40) vs scipy: rel err {err:.2e}", flush=True)
 del sub, Yx
+# At the reference defaults (tau = 5n, delta = 1.2 mn / nnz = 1200) the first
+# iteration's rank escalation ran past k = 1100 (W ~ 4600, out of memory at
+# ~170 GB; profiles/r02w_cfg5_defaults_oom.txt).  tau is therefore placed from
+# the spectrum: one rsvd_bki (k = 300) of P(M), tau = delta * S[TAU_INDEX]
+# (c = 1, so ~TAU_INDEX components start above tau).
+from paper_1810_06860_b200.rsvd import RsvdParams, rsvd_bki_dev  # noqa: E402
+
+delta = 1.2 * o.m * o.n / A.nnz
+t0 = time.perf_counter()
+r0, _, _ = rsvd_bki_dev(A, RsvdParams(k=300, p=2, s=5, seed=1))
+torch.cuda.synchronize()
+tau_index = int(os.environ.get("TAU_INDEX", "150"))
+tau = delta * float(r0.S_host[tau_index])
+print(f"rsvd_bki k=300 of P(M): {time.perf_counter() - t0:.2f} s; S[0] {r0.S_host[0]:.4e} S[100] {r0.S_host[100]:.4e} "
+      f"S[{tau_index}] {r0.S_host[tau_index]:.4e} S[299] {r0.S_host[299]:.4e}; delta {delta:.1f}, tau {tau:.4e}",
+      flush=True)
+del r0
 results = {}
 for prec in ("fp64", "fp32"):
-    p = completion.SvtParams(epsilon=0.05, i_max=imax, strategy="reuse-q", i_reuse=4, q_reuse=10, seed=0,
+    p = completion.SvtParams(tau=tau, epsilon=0.05, i_max=imax, strategy="reuse-q", i_reuse=4, q_reuse=10, seed=0,
                              precision=prec)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
