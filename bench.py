@@ -84,6 +84,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", choices=["svt", "bki"], default="svt")
     ap.add_argument("--replicas", action="store_true", help="N independent replicas instead of one sharded job")
+    ap.add_argument("--shard", action="store_true", help="the sharded engine even on one rank (collectives forced)")
     ap.add_argument("--cpu-baseline", choices=["full", "skip"], default="full")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--extras", choices=["on", "off"], default="on", help="secondary measurements (cfg2, cfg1)")
@@ -415,7 +416,7 @@ def bench_svt_main(args, ws, rank, local):
     from paper_1810_06860_b200 import _native, completion, device, profiling, workloads
     from paper_1810_06860_b200.sparse import ObservationSet
 
-    sharded = ws > 1 and not args.replicas
+    sharded = (ws > 1 and not args.replicas) or args.shard
     lib = _native.load()
     t_gen = time.perf_counter()
     o4 = workloads.cfg4()
@@ -425,7 +426,7 @@ def bench_svt_main(args, ws, rank, local):
     if sharded:
         from paper_1810_06860_b200.shards import Exchange, ShardedEngine
 
-        ex = Exchange()
+        ex = Exchange(always_collective=args.shard)
 
         def make_engine():
             return ShardedEngine(obs, ex)
@@ -658,7 +659,7 @@ def main():
         return
     import torch
 
-    init_dist(ws, local, need=False)
+    init_dist(ws, local, need=args.shard)
     if args.mode == "svt":
         line = bench_svt_main(args, ws, rank, local)
     else:

@@ -331,6 +331,15 @@ class DeviceKernels:
                      device.stream())
         return B
 
+    def lu_pl_async(self, X, status):
+        """LU-normalise X in place with its status left on the device
+        (status[0] == -1: pivots as usual; anything else: the caller replays
+        the careful path)."""
+        m, n = X.shape
+        work = device.arena().get("lu_work", int(_native.load().lr_lu_workspace_doubles(m, n)))
+        _native.call("lr_lu_pl_async_f64", m, n, device.ptr(X), device.ld(X), device.ptr(work), device.ptr(status),
+                     device.stream())
+
     def lu_pl(self, X):
         from .linalg import lu_pl_dev
 
@@ -581,20 +590,35 @@ class ShardedEngine:
         S_sel = np.asarray(S_sel, dtype=np.float64)
         return DevSvd(U_loc, K.vector(S_sel), Usel, S_sel)
 
-    def bki(self, rp: RsvdParams, allow_fallback: bool = True):
-        """Sharded Alg. 5 -> (DevSvd with local factor rows, Q replicated, fallbacks)."""
+    def bki(self, rp: RsvdParams, allow_fallback: bool = True, _speculate: bool = True):
+        """Sharded Alg. 5 -> (DevSvd with local factor rows, Q replicated, fallbacks).
+        Like the single-GPU route, the Krylov blocks' LU statuses stay on the
+        device and are read once after the loop; an unusual one replays the
+        call on the careful path (every rank reads the same replicated
+        statuses, so the ranks agree)."""
+        from . import rsvd as _rsvd
+
         K = self.K
         rp.check_against(self, krylov=True)
         fb = _Fallback(allow_fallback, "Krylov blocks are near-collinear, reduce p or use a larger matrix")
+        spec = _speculate and _rsvd.SPECULATIVE and hasattr(K, "lu_pl_async")
         w = rp.k + rp.s
         W = w * (rp.p + 1)
         mg, ng = self.r1 - self.r0, self.c1 - self.c0
+        status = K.vector(np.zeros(4 * (rp.p + 1))) if spec else None
+
+        def normalise(i):
+            if spec:
+                K.lu_pl_async(H[:, i * w:(i + 1) * w], status[4 * i:4 * i + 3])
+            else:
+                self._lu_block(H[:, i * w:(i + 1) * w], fb)
+
         Om = K.gaussian(rp.seed, self.n, w)
         H = K.empty(self.m, W)
         H_loc = K.empty(mg, w)
         K.spmm(self.Y_r, Om, out=H_loc)
         self.gather_m(H_loc, out=H[:, 0:w])
-        self._lu_block(H[:, 0:w], fb)
+        normalise(0)
         T_loc = K.empty(ng, w)
         T = K.empty(self.n, w)
         for i in range(1, rp.p + 1):
@@ -602,7 +626,9 @@ class ShardedEngine:
             self.gather_n(T_loc, out=T)
             K.spmm(self.Y_r, T, out=H_loc)
             self.gather_m(H_loc, out=H[:, i * w:(i + 1) * w])
-            self._lu_block(H[:, i * w:(i + 1) * w], fb)
+            normalise(i)
+        if spec and not np.all(K.to_host(status).reshape(-1, 4)[:, 0] == -1.0):
+            return self.bki(rp, allow_fallback, _speculate=False)
         try:
             Q_loc = self._orth_rows(H[self.r0:self.r1])
             Q = self.gather_m(Q_loc, out=K.empty(self.m, W))

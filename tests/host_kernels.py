@@ -175,6 +175,17 @@ class HostKernels:
         X.copy_(torch.from_numpy(PL))
         return X
 
+    def lu_pl_async(self, X, status):
+        """The speculative route's LU: status[0] = -1 when the pivots hold,
+        else the careful path is replayed (lr_lu_pl_async_f64's contract)."""
+        try:
+            PL = odense.pivoted_lower(_np(X))
+        except odense.RankDeficient:
+            status[0] = 0.0
+            return
+        X.copy_(torch.from_numpy(PL))
+        status[0] = -1.0
+
     def gaussian(self, seed, rows, cols):
         return torch.from_numpy(oracle.gaussian_block(oracle.Stream(seed), rows, cols))
 

@@ -210,3 +210,40 @@ def test_superset_draw_is_bit_exact(rows, w_lo, w_hi):
         ref = R.RngState(seed).normal_pairs(rows * w)
         out = np.empty(rows * w + 1)
         assert np.array_equal(sup.normals(w, out, R._pool()), ref), w
+
+
+def test_factor_container_matches_reference_format(tmp_path):
+    """write_factors / read_factors: the reference's LRFC bytes
+    (completion.py:449-492: magic, version, m n r, U S V little-endian),
+    checked against the real reference's writer when it is importable, and its
+    DataError cases."""
+    import os
+    import sys
+
+    rng = np.random.default_rng(0)
+    res = completion.CompletionResult(U=rng.standard_normal((7, 3)), S=np.array([3.0, 2.0, 1.0]),
+                                      V=rng.standard_normal((5, 3)), rank=3, iterations=1, converged=True,
+                                      residual=0.1, trace=[], events=[], svd_time=0.0, update_time=0.0,
+                                      total_time=0.0)
+    p = tmp_path / "f.bin"
+    completion.write_factors(str(p), res)
+    U, S, V = completion.read_factors(str(p))
+    assert np.array_equal(U, res.U) and np.array_equal(S, res.S) and np.array_equal(V, res.V)
+    ref_src = "/root/reference/pkg/src"
+    if os.path.isdir(ref_src):
+        sys.path.insert(0, ref_src)
+        try:
+            from lowrank import completion as rc
+
+            q = tmp_path / "ref.bin"
+            rc.write_factors(str(q), res)
+            assert q.read_bytes() == p.read_bytes()
+        finally:
+            sys.path.remove(ref_src)
+    raw = p.read_bytes()
+    for bad, msg in ((b"XXXX" + raw[4:], "not a factor container"), (raw[:20], "truncated in header"),
+                     (raw[:-8], "truncated"), (raw + b"\0", "trailing bytes")):
+        q = tmp_path / "bad.bin"
+        q.write_bytes(bad)
+        with pytest.raises(DataError, match=msg):
+            completion.read_factors(str(q))
