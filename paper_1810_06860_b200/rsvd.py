@@ -104,8 +104,8 @@ class Subspace:
     def Q_dev(self):
         if isinstance(self._Q, np.ndarray):
             self._Q = device.to_device(self._Q)
-        if isinstance(self._Q, LazyQ):
-            self._Q = self._Q.materialize()
+        if isinstance(self._Q, LazyQ) or hasattr(self._Q, "materialize"):
+            self._Q = self._Q.materialize()  # an unformed product, or a deferred gather (shards._GatheredQ)
         return self._Q
 
     @property

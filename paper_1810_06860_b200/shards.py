@@ -545,7 +545,27 @@ class ShardedEngine:
         info, Rinv = K.potrf_inv(G, shift)
         if info:
             return info, None, None
-        return 0, K.matmul(X, Rinv, b_upper=True), K.diag(G)
+        Q = K.matmul(X, Rinv, b_upper=True)
+        if self._passes is not None:
+            self._passes.append((X, Q, Rinv, shift, G))  # the pass chain, for the Krylov reuse in bki
+        return 0, Q, K.diag(G)
+
+    _passes = None  # a list while bki orthonormalises its Krylov block
+
+    def _chain(self, X, Q):
+        """The Rinv factors of the CholeskyQR passes that turned X into Q
+        (Q = X R_1^{-1} R_2^{-1} ...), and whether the first was unshifted;
+        None when Q is not such a chain of X."""
+        by_out = {id(q): (x, r, sh, g) for x, q, r, sh, g in self._passes}
+        chain, cur, first = [], Q, None
+        while id(cur) in by_out:
+            x, r, sh, g = by_out[id(cur)]
+            chain.append(r)
+            first = (sh, g)
+            cur = x
+        if cur is not X or not chain:
+            return None
+        return chain[::-1], first
 
     def _orth_rows(self, X_loc):
         """orth of the row-sharded block whose local rows are X_loc."""
@@ -580,13 +600,16 @@ class ShardedEngine:
             desc = W - 1 - np.asarray(idx)
             return Sd[desc], K.select_columns(Vd, desc), K.select_columns(Ud, desc)[self.c0:self.c1]
 
-    def _project_and_solve(self, Q, k: int, fb: _Fallback) -> DevSvd:
+    def _project_and_solve(self, Q, k: int, fb: _Fallback, Bt_loc=None, Q_loc=None) -> DevSvd:
+        """Bt_loc / Q_loc given (the Krylov reuse): Y^T Q's rows C_g and Q's
+        rows R_g, the full Q never needed."""
         K = self.K
-        W = int(Q.shape[1])
-        Bt_loc = K.spmm_t(self.Y_c, Q, out=K.empty(self.c1 - self.c0, W))
+        W = int(Q.shape[1]) if Q is not None else int(Q_loc.shape[1])
+        if Bt_loc is None:
+            Bt_loc = K.spmm_t(self.Y_c, Q, out=K.empty(self.c1 - self.c0, W))
         idx = np.arange(W - 1, W - k - 1, -1)
         S_sel, Vsel, Usel = self._windowed(Bt_loc, idx, fb)
-        U_loc = K.matmul(Q[self.r0:self.r1], Vsel)
+        U_loc = K.matmul(Q_loc if Q_loc is not None else Q[self.r0:self.r1], Vsel)
         S_sel = np.asarray(S_sel, dtype=np.float64)
         return DevSvd(U_loc, K.vector(S_sel), Usel, S_sel)
 
@@ -620,8 +643,9 @@ class ShardedEngine:
         self.gather_m(H_loc, out=H[:, 0:w])
         normalise(0)
         T_loc = K.empty(ng, w)
-        T = K.empty(self.n, w)
+        T_all = K.empty(self.n, W)  # Y^T H, block by block (replicated after each allgather)
         for i in range(1, rp.p + 1):
+            T = T_all[:, (i - 1) * w:i * w]
             K.spmm_t(self.Y_c, H[:, (i - 1) * w:i * w], out=T_loc)
             self.gather_n(T_loc, out=T)
             K.spmm(self.Y_r, T, out=H_loc)
@@ -629,12 +653,38 @@ class ShardedEngine:
             normalise(i)
         if spec and not np.all(K.to_host(status).reshape(-1, 4)[:, 0] == -1.0):
             return self.bki(rp, allow_fallback, _speculate=False)
+        self._passes = []
+        X_loc = H[self.r0:self.r1]
         try:
-            Q_loc = self._orth_rows(H[self.r0:self.r1])
-            Q = self.gather_m(Q_loc, out=K.empty(self.m, W))
+            Q_loc = self._orth_rows(X_loc)
         except RankDeficiencyError as exc:
+            self._passes = None
             fb.fail(exc)
             Q = K.dense_svd(H)[0]
+            return self._project_and_solve(Q, rp.k, fb), Q, fb.count
+        # Y^T Q = (Y^T H) R_1^{-1} R_2^{-1} ... from the Krylov products (the
+        # single-GPU route's reuse, rsvd.KRYLOV_REUSE), gated on kappa_F(H)
+        chain = self._chain(X_loc, Q_loc) if _rsvd.KRYLOV_REUSE else None
+        if chain is not None and chain[1][0] == 0.0:
+            R1inv = chain[0][0]
+            kappa = float(np.sqrt(np.sum(K.diag(chain[1][1])) * float(K.to_host(K.stats(R1inv))[0])))
+            if len(_rsvd.REUSE_STATS["kappas"]) < 4096:
+                _rsvd.REUSE_STATS["kappas"].append(kappa)
+            if np.isfinite(kappa) and kappa <= _rsvd.KRYLOV_REUSE_KAPPA:
+                _rsvd.REUSE_STATS["used"] += 1
+                T_loc = K.empty(ng, w)
+                K.spmm_t(self.Y_c, H[:, rp.p * w:W], out=T_loc)
+                self.gather_n(T_loc, out=T_all[:, rp.p * w:W])
+                Bt_loc = T_all[self.c0:self.c1]
+                for Rinv in chain[0]:
+                    Bt_loc = K.matmul(Bt_loc, Rinv, b_upper=True)
+                self._passes = None
+                res = self._project_and_solve(None, rp.k, fb, Bt_loc=Bt_loc, Q_loc=Q_loc)
+                return res, _GatheredQ(self, Q_loc, W), fb.count
+        if chain is not None:
+            _rsvd.REUSE_STATS["kappa_gate"] += 1
+        self._passes = None
+        Q = self.gather_m(Q_loc, out=K.empty(self.m, W))
         res = self._project_and_solve(Q, rp.k, fb)
         return res, Q, fb.count
 
@@ -682,6 +732,22 @@ class ShardedEngine:
     @property
     def cols(self):
         return self.n
+
+
+class _GatheredQ:
+    """A row-sharded basis whose allgather is deferred until a caller needs
+    the full Q (a recycle_q, Subspace.Q): rsvd_bki's own projection uses only
+    the local rows."""
+
+    def __init__(self, eng, Q_loc, W):
+        self.eng, self.Q_loc, self.W = eng, Q_loc, W
+
+    @property
+    def shape(self):
+        return (self.eng.m, self.W)
+
+    def materialize(self):
+        return self.eng.gather_m(self.Q_loc, out=self.eng.K.empty(self.eng.m, self.W))
 
 
 # ------------------------------------------------------------ public API

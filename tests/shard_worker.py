@@ -77,7 +77,11 @@ def run(rank, world, port, outdir, backend, golden_path, cases):
 
         if "bki" in cases:
             A = SparseMatrix.from_coo(300, 200, g["rs_i"], g["rs_j"], g["rs_v"])
+            from paper_1810_06860_b200.rsvd import REUSE_STATS
+
+            used0 = REUSE_STATS["used"]
             res, sub = rsvd_bki_sharded(A, RsvdParams(k=10, p=2, s=5, seed=3), exchange=ex, kernels=K)
+            out["bki_reuse"] = np.array(REUSE_STATS["used"] - used0)
             out["bki_U"], out["bki_S"], out["bki_V"] = res.U, res.S, res.V
             Q = sub.Q if isinstance(sub.Q, np.ndarray) else sub.Q.cpu().numpy()
             out["bki_Q"] = np.asarray(Q)

@@ -86,6 +86,7 @@ def test_gloo_bki_matches_reference(gloo_runs, golden, world):
     _ok(runs)
     r = runs[0]
     S_ref = golden["rs_bki_S"]
+    assert int(r["bki_reuse"]) == 1  # Y^T Q from the Krylov products, Q's allgather deferred
     assert np.max(np.abs(r["bki_S"] - S_ref)) <= 1e-10 * S_ref[0]
     np.testing.assert_allclose(r["bki_U"], golden["rs_bki_U"], atol=1e-9)
     np.testing.assert_allclose(r["bki_V"], golden["rs_bki_V"], atol=1e-9)
