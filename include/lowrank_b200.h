@@ -216,6 +216,15 @@ int lr_fix_signs_f64(double* V, long long ldv, int rows_v, int cols, double* U, 
  * (linalg.py:196), on the device so eig_svd's lift is queued before the host
  * reads d for the rank checks. */
 int lr_gram_spectrum_f64(const double* d, int n, double* S, void* stream);
+/* fp32 mode's eigSVD Gram (linalg.py:189, A.T @ A) on the tcgen05 tensor
+ * cores: G (n x n, fp64, exactly symmetric) = A^T A of the fp32 block A
+ * (K x n, row-major, lda >= n) as 3xTF32 (a = hi + lo, hi.hi + hi.lo +
+ * lo.hi) with fp32 TMEM accumulation over chunks of <= 4096 rows and a
+ * fixed-order fp64 sum of the chunk partials (deterministic).  work: at least
+ * lr_gram_tf32x3_workspace_floats(K, n) floats of device memory. */
+long long lr_gram_tf32x3_workspace_floats(int K, int n);
+int lr_gram_tf32x3(const float* A, long long lda, int K, int n, double* G, long long ldg, float* work,
+                   long long work_floats, void* stream);
 /* B[:, j] = V[:, idx_j] * scale_j with scale_j = sgn/S[idx_j]; column gather
  * used by eig_svd's U = A (V / S) for a selected window (linalg.py:199-201). */
 int lr_scale_columns_f64(const double* V, long long ldv, int rows, const int* cols_idx, int ncols,

@@ -67,6 +67,8 @@ SIGNATURES = {
     "lr_fix_signs_f64": (_I, [_P, _LL, _I, _I, _P, _LL, _I, _P]),
     "lr_scale_columns_f64": (_I, [_P, _LL, _I, _P, _I, _P, _I, _P, _LL, _P]),
     "lr_gram_spectrum_f64": (_I, [_P, _I, _P, _P]),
+    "lr_gram_tf32x3_workspace_floats": (_LL, [_I, _I]),
+    "lr_gram_tf32x3": (_I, [_P, _LL, _I, _I, _P, _LL, _P, _LL, _P]),
     "lr_coo_to_csr_workspace_ints": (_LL, [_I, _LL]),
     "lr_coo_to_csr_i32": (_I, [_I, _I, _LL, _P, _P, _P, _I, _P, _P, _P, _P, _P, _P, _LL, _P, _P]),
     "lr_jacobi_sweep_f64": (_I, [_I, _I, _P, _LL, _P, _LL, _D, _D, _P, _P]),

@@ -117,6 +117,19 @@ def gram_dev(A, out=None):
     return _gemm(1, n, n, rows, 1.0, A, A, 0.0, out, _native.LR_GEMM_SYRK_UPPER)
 
 
+def gram_tf32x3_dev(A32, out=None):
+    """A^T A of an fp32 block on the tcgen05 tensor cores (3xTF32, fp64
+    result, exactly symmetric): the fp32 mode's eigSVD Gram."""
+    rows, n = A32.shape
+    if out is None:
+        out = device.empty(n, n)
+    nf = int(_native.call("lr_gram_tf32x3_workspace_floats", rows, n))
+    work = device.arena().get("gram_tf32x3", (nf + 1) // 2)
+    _native.call("lr_gram_tf32x3", device.ptr(A32), device.ld(A32), rows, n, device.ptr(out), device.ld(out),
+                 device.ptr(work), 2 * int(work.numel()), _st())
+    return out
+
+
 def matmul_dev(A, B, out=None, b_upper=False):
     """A (M x K) @ B (K x N)."""
     M, K = A.shape
@@ -455,8 +468,9 @@ def gram_spectrum(dh):
     return np.sqrt(np.maximum(dh, 0.0))
 
 
-def eig_svd_dev(A, cols=None, check=True, defer=False):
+def eig_svd_dev(A, cols=None, check=True, defer=False, G=None):
     """Gram-route SVD of tall A (linalg.py:172-202), device in/out.
+    G: A's Gram already formed (the fp32 mode's tensor-core Gram).
 
     Returns (S_host ascending (all n), V (n x n, sign rule applied),
     U_sel (rows x len(cols)) = A V[:, cols] / S[cols], cols) with cols an
@@ -467,7 +481,8 @@ def eig_svd_dev(A, cols=None, check=True, defer=False):
     rows, n = A.shape
     if rows < n:
         raise ValueError(f"eig_svd requires m >= n, got {rows}x{n}")
-    G = gram_dev(A)
+    if G is None:
+        G = gram_dev(A)
     try:
         V, d = sym_eig_dev(G, symmetrize=False)
     except NumericalError:
@@ -499,13 +514,14 @@ def eig_svd_dev(A, cols=None, check=True, defer=False):
     return finish(), V, U, cols
 
 
-def eig_svd_congruent_dev(T, Rinv, cols, defer=False):
+def eig_svd_congruent_dev(T, Rinv, cols, defer=False, Gt=None):
     """eig_svd_dev of A = T Rinv without forming A (Rinv upper triangular,
     W x W): Gram(A) = Rinv^T Gram(T) Rinv (two W^3 products instead of an
     n x W x W one), U_sel = T (Rinv V[:, cols] / S[cols]).  Same returns as
-    eig_svd_dev."""
+    eig_svd_dev.  Gt: Gram(T) already formed."""
     rows, n = T.shape
-    Gt = gram_dev(T)
+    if Gt is None:
+        Gt = gram_dev(T)
     H = matmul_dev(Gt, Rinv, b_upper=True)   # Gram(T) Rinv
     G = matmul_tn_dev(Rinv, H)               # Rinv^T Gram(T) Rinv
     try:

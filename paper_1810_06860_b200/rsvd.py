@@ -31,7 +31,7 @@ import numpy as np
 
 from . import _native, device
 from .errors import RankDeficiencyError
-from .linalg import (DevSvd, LazyQ, SvdResult, eig_svd_congruent_dev, eig_svd_dev, lu_pl_dev, matmul_dev,
+from .linalg import (DevSvd, LazyQ, SvdResult, eig_svd_congruent_dev, eig_svd_dev, gram_tf32x3_dev, lu_pl_dev, matmul_dev,
                      oracle_svd_dev, orth_dev, orth_speculation_holds, orth_speculative_dev)
 from .rng import RngState, gaussian_matrix, gaussian_matrix_device
 from .sparse import SparseMatrix, frobenius, spmm_dev, spmm_dev32, spmm_t_dev, spmm_t_dev32
@@ -217,7 +217,7 @@ def _orthonormalize(X, fb: _Fallback, lazy_last=False):
         return oracle_svd_dev(X)[0]
 
 
-def _windowed_small_svd(Bt, idx, fb: _Fallback, Rinv=None, defer=False):
+def _windowed_small_svd(Bt, idx, fb: _Fallback, Rinv=None, defer=False, G=None):
     """eig_svd of Bt (n x W) keeping the ascending-order columns idx (given in
     the output order).  Returns (S_sel host, V_small[:, idx] device,
     U_small[:, idx] device).  Falls back to the dense SVD (ascending).
@@ -227,9 +227,9 @@ def _windowed_small_svd(Bt, idx, fb: _Fallback, Rinv=None, defer=False):
     and the fallback happen there)."""
     try:
         if Rinv is None:
-            fin, V, U, cols = eig_svd_dev(Bt, cols=idx, defer=True)
+            fin, V, U, cols = eig_svd_dev(Bt, cols=idx, defer=True, G=G)
         else:
-            fin, V, U, cols = eig_svd_congruent_dev(Bt, Rinv, idx, defer=True)
+            fin, V, U, cols = eig_svd_congruent_dev(Bt, Rinv, idx, defer=True, Gt=G)
         Vsel = device.empty(V.shape[0], len(idx))
         ci = device.int_buffer(cols)
         _native.call("lr_scale_columns_f64", device.ptr(V), device.ld(V), V.shape[0], device.ptr(ci), len(idx),
@@ -265,11 +265,23 @@ def _windowed_fallback(Bt, idx, fb: _Fallback, Rinv, exc):
     return Sd[desc], Vsel, Usel
 
 
-def _spmm_t_prec(Y: SparseMatrix, X, precision: str):
-    """Y^T X in the requested precision; the fp32 product comes back fp64."""
+# fp32 mode: the eigSVD Gram of the fp32 product on the tcgen05 tensor cores
+# (3xTF32); False: the fp64 DMMA Gram of the widened product
+GRAM_TF32 = __import__("os").environ.get("LR_GRAM_TF32", "1") != "0"
+
+
+def _spmm_t_prec(Y: SparseMatrix, X, precision: str, with_gram: bool = False):
+    """Y^T X in the requested precision; the fp32 product comes back fp64.
+    with_gram: returns (product, its Gram or None) -- the fp32 product's Gram
+    formed from the fp32 values on the tensor cores (GRAM_TF32)."""
     if precision == "fp32" and int(X.shape[1]) >= 2:
-        return device.to_f64(spmm_t_dev32(Y, device.to_f32(X)))
-    return spmm_t_dev(Y, X)
+        T32 = spmm_t_dev32(Y, device.to_f32(X))
+        T = device.to_f64(T32)
+        if with_gram:
+            return T, (gram_tf32x3_dev(T32) if GRAM_TF32 else None)
+        return T
+    T = spmm_t_dev(Y, X)
+    return (T, None) if with_gram else T
 
 
 def project_and_solve(Y: SparseMatrix, Q, k: int, fb: _Fallback, precision: str = "fp64",
@@ -282,13 +294,14 @@ def project_and_solve(Y: SparseMatrix, Q, k: int, fb: _Fallback, precision: str 
     W = int(Q.shape[1])
     idx = np.arange(W - 1, W - k - 1, -1)  # top-k of the ascending order, descending
     lazy = isinstance(Q, LazyQ)
+    G = None
     if lazy:
         # Q = Q1 Rinv unformed: B^T = (Y^T Q1) Rinv, U = Q1 (Rinv V_small)
-        T = T_pre if T_pre is not None else _spmm_t_prec(Y, Q.base, precision)
-        fin, Vsel, Usel = _windowed_small_svd(T, idx, fb, Rinv=Q.Rinv, defer=True)
+        T, G = (T_pre, None) if T_pre is not None else _spmm_t_prec(Y, Q.base, precision, with_gram=True)
+        fin, Vsel, Usel = _windowed_small_svd(T, idx, fb, Rinv=Q.Rinv, defer=True, G=G)
     else:
-        Bt = T_pre if T_pre is not None else _spmm_t_prec(Y, Q, precision)
-        fin, Vsel, Usel = _windowed_small_svd(Bt, idx, fb, defer=True)
+        Bt, G = (T_pre, None) if T_pre is not None else _spmm_t_prec(Y, Q, precision, with_gram=True)
+        fin, Vsel, Usel = _windowed_small_svd(Bt, idx, fb, defer=True, G=G)
 
     def lift(Vs, Us):
         pend = device.to_host_async(Us) if download else None

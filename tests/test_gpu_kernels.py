@@ -661,3 +661,26 @@ def test_observation_set_device_validation_matches_host():
     with pytest.raises(DataError, match="split tags"):
         ObservationSet(3, 3, [0, 1], [0, 1], [1.0, 2.0], np.array([0, 2], dtype=np.uint8))
     assert isinstance(T, SparseMatrix)
+
+
+@pytest.mark.parametrize("K,n", [(1, 1), (37, 5), (3, 260), (1000, 128), (5000, 129), (20000, 300),
+                                 (100000, 660), (300001, 40)])
+def test_gram_tf32x3_tensor_core(K, n):
+    """fp32 mode's eigSVD Gram on tcgen05 (kind::tf32, 3xTF32): within 1e-5
+    of the fp64 Gram of the same fp32 values, entrywise relative to
+    sqrt(G_ii G_jj) (the Cauchy-Schwarz scale of G_ij); exactly symmetric;
+    bitwise reproducible (fixed-order chunk sum)."""
+    from paper_1810_06860_b200 import device, linalg
+
+    rng = np.random.default_rng(K + 7 * n)
+    A = rng.standard_normal((K, n)) * rng.uniform(0.01, 100.0, size=n)
+    A32 = device.to_f32(device.to_device(A))
+    G = device.to_host(linalg.gram_tf32x3_dev(A32))
+    G2 = device.to_host(linalg.gram_tf32x3_dev(A32))
+    A64 = device.to_host(A32).astype(np.float64)
+    ref = A64.T @ A64
+    scale = np.sqrt(np.outer(np.diag(ref), np.diag(ref)))
+    err = float(np.max(np.abs(G - ref) / scale))
+    assert err < 1e-5, err
+    assert np.array_equal(G, G.T)
+    assert np.array_equal(G, G2)

@@ -1,7 +1,7 @@
 """cfg5 scale-up (BASELINE configs[4]: 1e6 x 2e5, 2e8 uniform observations,
 rank-100 Gaussian factor product + N(0, 0.01) noise): the SVT loop itself,
-svt_fast at the reference defaults (tau = 5n, delta = 1.2 mn / nnz) with
-reuse-q recycling, fp64 and the fp32 mode, IMAX iterations each; per
+svt_fast at the reference's delta = 1.2 mn / nnz and a tau that lets the
+rank grow through ~300 (below), reuse-q recycling, fp64 and the fp32 mode; per
 iteration k, r, p, source, residual and wall time, the fp32 mode's residual
 drift against fp64, and a spot check of the CSR product on sampled rows
 against scipy (the reference's own SpMM) on the host."""
@@ -17,7 +17,7 @@ import torch  # noqa: E402
 from paper_1810_06860_b200 import completion, device, workloads  # noqa: E402
 from paper_1810_06860_b200.sparse import ObservationSet, spmm_dev  # noqa: E402
 
-imax = int(os.environ.get("IMAX", "6"))
+imax = int(os.environ.get("IMAX", "40"))
 t0 = time.perf_counter()
 o = workloads.cfg5()
 print(f"generate (host numpy): {time.perf_counter() - t0:.1f} s, nnz {o.rows.size}", flush=True)
@@ -38,37 +38,59 @@ print(f"SpMM spot check (2000 rows, w = 40) vs scipy: rel err {err:.2e}", flush=
 del sub, Yx
 # At the reference defaults (tau = 5n, delta = 1.2 mn / nnz = 1200) the first
 # iteration's rank escalation ran past k = 1100 (W ~ 4600, out of memory at
-# ~170 GB; profiles/r02w_cfg5_defaults_oom.txt).  tau is therefore placed from
-# the spectrum: one rsvd_bki (k = 300) of P(M), tau = delta * S[TAU_INDEX]
-# (c = 1, so ~TAU_INDEX components start above tau).
+# ~170 GB; profiles/r02w_cfg5_defaults_oom.txt): cfg5 sits at the detection
+# threshold -- the signal's singular values in P(M) are p sigma(M) ~ 1e-3 x
+# 4.5e5 ~ 450, the sampling-noise bulk edge is sqrt(p var(M)) (sqrt m + sqrt n)
+# ~ 0.32 x 1447 ~ 457 -- so once Y's bulk crosses tau every direction enters.  With
+# c = ceil(tau / (delta ||P(M)||)) the bulk crosses after ~0.26 c iterations;
+# tau = TAU (default 5e7, c = 76) lets the rank grow through ~300 first.
+# KCAP stops the run (the trace so far is printed) before the escalation
+# outgrows memory.
 from paper_1810_06860_b200.rsvd import RsvdParams, rsvd_bki_dev  # noqa: E402
 
 delta = 1.2 * o.m * o.n / A.nnz
 t0 = time.perf_counter()
 r0, _, _ = rsvd_bki_dev(A, RsvdParams(k=300, p=2, s=5, seed=1))
 torch.cuda.synchronize()
-tau_index = int(os.environ.get("TAU_INDEX", "150"))
-tau = delta * float(r0.S_host[tau_index])
+tau = float(os.environ.get("TAU", "5e7"))
+kcap = int(os.environ.get("KCAP", "420"))
 print(f"rsvd_bki k=300 of P(M): {time.perf_counter() - t0:.2f} s; S[0] {r0.S_host[0]:.4e} S[100] {r0.S_host[100]:.4e} "
-      f"S[{tau_index}] {r0.S_host[tau_index]:.4e} S[299] {r0.S_host[299]:.4e}; delta {delta:.1f}, tau {tau:.4e}",
+      f"S[299] {r0.S_host[299]:.4e}; delta {delta:.1f}, tau {tau:.4e}, c = {int(np.ceil(tau / (delta * r0.S_host[0])))}",
       flush=True)
 del r0
+
+
+class KCap(Exception):
+    pass
+
+
+_bki = completion.DeviceEngine.bki
+
+
+def _capped(self, rp, *a, **kw):
+    if rp.k > kcap:
+        raise KCap(f"rank escalation reached k = {rp.k} > KCAP = {kcap}")
+    return _bki(self, rp, *a, **kw)
+
+
+completion.DeviceEngine.bki = _capped
+completion.VERBOSE = True
 results = {}
 for prec in ("fp64", "fp32"):
     p = completion.SvtParams(tau=tau, epsilon=0.05, i_max=imax, strategy="reuse-q", i_reuse=4, q_reuse=10, seed=0,
                              precision=prec)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    res = completion.svt_fast(obs, p)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
-    results[prec] = res
-    print(f"== {prec}: {res.iterations} iterations in {dt:.1f} s (loop {sum(t.wall_time for t in res.trace):.1f} s), "
-          f"rank {res.rank}, residual {res.residual:.6e}", flush=True)
-    for t in res.trace:
-        print(f"   i={t.iteration} k={t.k} r={t.r} p={t.p} q={t.q} {t.svd_source} resid={t.residual:.9e} "
-              f"{t.wall_time * 1e3:.0f} ms", flush=True)
-a, b = results["fp64"].trace, results["fp32"].trace
-d = [abs(x.residual - y.residual) / x.residual for x, y in zip(a, b)]
-print(f"fp32 vs fp64 residual drift per iteration: max {max(d):.2e}; same (k, r) trajectory: "
-      f"{[(x.k, x.r) for x in a] == [(y.k, y.r) for y in b]}", flush=True)
+    print(f"== {prec}", flush=True)
+    try:
+        res = completion.svt_fast(obs, p)
+        torch.cuda.synchronize()
+        results[prec] = res
+        print(f"== {prec}: {res.iterations} iterations in {time.perf_counter() - t0:.1f} s, rank {res.rank}, "
+              f"residual {res.residual:.6e}", flush=True)
+    except KCap as exc:
+        torch.cuda.synchronize()
+        print(f"== {prec}: stopped after {time.perf_counter() - t0:.1f} s: {exc}", flush=True)
+    torch.cuda.empty_cache()
+    print(f"   peak device memory {torch.cuda.max_memory_allocated() / 2**30:.1f} GiB", flush=True)
+    torch.cuda.reset_peak_memory_stats()

@@ -1,6 +1,7 @@
 #!/bin/bash
 # sharded engine at world size 1 (collectives forced, NCCL) against the single-GPU engine, cfg4 job
 mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_shards.py -x -q > gpurun_out/r02bb_pytest_shards.log 2>&1; echo rc=$? >> gpurun_out/r02bb_pytest_shards.log
 timeout 900 python bench.py --steps 2 --warmup 2 --extras off --cpu-baseline skip --e2e-steps 1 > gpurun_out/r02bb_single.json 2> gpurun_out/r02bb_single.err
 timeout 900 python bench.py --shard --steps 2 --warmup 2 --extras off --cpu-baseline skip --e2e-steps 1 > gpurun_out/r02bb_shard.json 2> gpurun_out/r02bb_shard.err
 python - <<'PY'
