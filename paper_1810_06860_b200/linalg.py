@@ -123,7 +123,7 @@ def gram_tf32x3_dev(A32, out=None):
     rows, n = A32.shape
     if out is None:
         out = device.empty(n, n)
-    nf = int(_native.call("lr_gram_tf32x3_workspace_floats", rows, n))
+    nf = int(_native.load().lr_gram_tf32x3_workspace_floats(rows, n))
     work = device.arena().get("gram_tf32x3", (nf + 1) // 2)
     _native.call("lr_gram_tf32x3", device.ptr(A32), device.ld(A32), rows, n, device.ptr(out), device.ld(out),
                  device.ptr(work), 2 * int(work.numel()), _st())

@@ -21,6 +21,8 @@ cfg4  138493x26744, 20,000,263 ratings: row counts Zipf(1.0) floor 20 capped
       RngState(0)) (ingest.py:141-165; seed 0 = the CLI default)  (seed 4)
 cfg5  1e6x2e5, 2e8 uniform positions, rank-100 product + N(0, 0.01^2) noise
       (sigma = 0.01)                                          (seed 5)
+      cfg5_device: the same distribution drawn on the GPU with torch's
+      generator (a different sample; ~250 s of host numpy -> seconds)
 """
 
 from __future__ import annotations
@@ -204,3 +206,33 @@ def cfg5(seed=5, m=1_000_000, n=200_000, nnz=200_000_000, rank=100, noise=0.01):
         vals[lo:hi] = np.einsum("er,er->e", F[i[lo:hi]], G[j[lo:hi]])
     vals += noise * rng.standard_normal(nnz)
     return Observations(m, n, i, j, vals)
+
+
+def cfg5_device(seed=5, m=1_000_000, n=200_000, nnz=200_000_000, rank=100, noise=0.01, device="cuda"):
+    """cfg5's distribution sampled on the GPU (torch's Philox generator, not
+    numpy's stream): uniform distinct positions (oversampled draws, unique,
+    a random subset), sorted row-major; values = F_i . G_j + noise with
+    F, G ~ N(0, 1).  Returns host Observations (the COO goes through
+    ObservationSet like every other workload)."""
+    import torch
+
+    dev = torch.device(device)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    keys = torch.empty(0, dtype=torch.int64, device=dev)
+    while keys.numel() < nnz:
+        extra = torch.randint(0, m * n, (int((nnz - keys.numel()) * 1.02) + 1024,), generator=g, device=dev)
+        keys = torch.unique(torch.cat([keys, extra]))
+    keys = keys[torch.randperm(keys.numel(), generator=g, device=dev)[:nnz]]
+    keys, _ = torch.sort(keys)
+    i, j = keys // n, keys % n
+    del keys
+    F = torch.randn(m, rank, generator=g, device=dev, dtype=torch.float64)
+    G = torch.randn(n, rank, generator=g, device=dev, dtype=torch.float64)
+    vals = torch.empty(nnz, dtype=torch.float64, device=dev)
+    step = 1 << 23
+    for lo in range(0, nnz, step):
+        hi = min(nnz, lo + step)
+        vals[lo:hi] = (F[i[lo:hi]] * G[j[lo:hi]]).sum(dim=1)
+    vals += noise * torch.randn(nnz, generator=g, device=dev, dtype=torch.float64)
+    return Observations(m, n, i.cpu().numpy(), j.cpu().numpy(), vals.cpu().numpy())

@@ -247,3 +247,16 @@ def test_factor_container_matches_reference_format(tmp_path):
         q.write_bytes(bad)
         with pytest.raises(DataError, match=msg):
             completion.read_factors(str(q))
+
+
+def test_cfg5_device_generator_shape_and_pattern():
+    """workloads.cfg5_device (run here on the CPU generator): distinct,
+    row-major sorted in-range positions, the requested count, finite values
+    of the rank-r product's scale."""
+    from paper_1810_06860_b200 import workloads
+
+    o = workloads.cfg5_device(seed=1, m=3000, n=700, nnz=50000, rank=7, noise=0.01, device="cpu")
+    key = o.rows * o.n + o.cols
+    assert o.rows.size == 50000 and np.all(np.diff(key) > 0)
+    assert o.rows.min() >= 0 and o.rows.max() < 3000 and o.cols.min() >= 0 and o.cols.max() < 700
+    assert np.all(np.isfinite(o.values)) and 1.5 < np.std(o.values) < 4.5  # var = rank

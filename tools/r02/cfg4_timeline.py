@@ -49,7 +49,18 @@ _rng.take_normals = _timed_take
 o4 = workloads.cfg4()
 obs = ObservationSet(o4.m, o4.n, o4.rows, o4.cols, o4.values, o4.split)
 params = bench.cfg4_params()
-eng = completion.DeviceEngine(obs)
+if os.environ.get("SHARD"):  # the sharded engine on one rank, collectives forced (NCCL)
+    import torch.distributed as dist
+
+    from paper_1810_06860_b200.shards import Exchange, ShardedEngine
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    eng = ShardedEngine(obs, Exchange(always_collective=True))
+else:
+    eng = completion.DeviceEngine(obs)
 
 
 def job():

@@ -17,10 +17,15 @@ import torch  # noqa: E402
 from paper_1810_06860_b200 import completion, device, workloads  # noqa: E402
 from paper_1810_06860_b200.sparse import ObservationSet, spmm_dev  # noqa: E402
 
-imax = int(os.environ.get("IMAX", "40"))
+imax = int(os.environ.get("IMAX", "45"))
 t0 = time.perf_counter()
-o = workloads.cfg5()
-print(f"generate (host numpy): {time.perf_counter() - t0:.1f} s, nnz {o.rows.size}", flush=True)
+if os.environ.get("CFG5_GEN", "device") == "device":
+    o = workloads.cfg5_device()
+    print(f"generate (device, workloads.cfg5_device): {time.perf_counter() - t0:.1f} s, nnz {o.rows.size}", flush=True)
+else:
+    o = workloads.cfg5()
+    print(f"generate (host numpy): {time.perf_counter() - t0:.1f} s, nnz {o.rows.size}", flush=True)
+torch.cuda.empty_cache()
 t0 = time.perf_counter()
 obs = ObservationSet(o.m, o.n, o.rows, o.cols, o.values)
 torch.cuda.synchronize()
@@ -41,18 +46,22 @@ del sub, Yx
 # ~170 GB; profiles/r02w_cfg5_defaults_oom.txt): cfg5 sits at the detection
 # threshold -- the signal's singular values in P(M) are p sigma(M) ~ 1e-3 x
 # 4.5e5 ~ 450, the sampling-noise bulk edge is sqrt(p var(M)) (sqrt m + sqrt n)
-# ~ 0.32 x 1447 ~ 457 -- so once Y's bulk crosses tau every direction enters.  With
-# c = ceil(tau / (delta ||P(M)||)) the bulk crosses after ~0.26 c iterations;
-# tau = TAU (default 5e7, c = 76) lets the rank grow through ~300 first.
-# KCAP stops the run (the trace so far is printed) before the escalation
-# outgrows memory.
+# ~ 0.32 x 1447 ~ 457 -- and 2e8 samples are 1.67x the rank-100 degrees of
+# freedom, below what any completion method recovers from.  With delta = 1200
+# and a large tau (5e7) the loop overshoots: residuals 8, 13, 19 with the rank
+# reset to 0 after each (profiles/r02cc_cfg5_delta1200.txt).  The scale-up run
+# therefore uses delta = DELTA (default 1, inside SVT's delta < 2 condition)
+# and tau = TAU_C * delta * S[0] (c ~ TAU_C): Y accumulates P(M - X) and the
+# rank grows through the flat spectrum (S[0] / S[299] = 1.27) toward ~300 in
+# ~TAU_C / 4 iterations.  KCAP stops the run (the trace so far is printed)
+# before the escalation outgrows memory.
 from paper_1810_06860_b200.rsvd import RsvdParams, rsvd_bki_dev  # noqa: E402
 
-delta = 1.2 * o.m * o.n / A.nnz
+delta = float(os.environ.get("DELTA", "1.0"))
 t0 = time.perf_counter()
 r0, _, _ = rsvd_bki_dev(A, RsvdParams(k=300, p=2, s=5, seed=1))
 torch.cuda.synchronize()
-tau = float(os.environ.get("TAU", "5e7"))
+tau = float(os.environ.get("TAU_C", "100")) * delta * float(r0.S_host[0])
 kcap = int(os.environ.get("KCAP", "420"))
 print(f"rsvd_bki k=300 of P(M): {time.perf_counter() - t0:.2f} s; S[0] {r0.S_host[0]:.4e} S[100] {r0.S_host[100]:.4e} "
       f"S[299] {r0.S_host[299]:.4e}; delta {delta:.1f}, tau {tau:.4e}, c = {int(np.ceil(tau / (delta * r0.S_host[0])))}",
@@ -77,7 +86,7 @@ completion.DeviceEngine.bki = _capped
 completion.VERBOSE = True
 results = {}
 for prec in ("fp64", "fp32"):
-    p = completion.SvtParams(tau=tau, epsilon=0.05, i_max=imax, strategy="reuse-q", i_reuse=4, q_reuse=10, seed=0,
+    p = completion.SvtParams(tau=tau, delta=delta, epsilon=0.05, i_max=imax, strategy="reuse-q", i_reuse=4, q_reuse=10, seed=0,
                              precision=prec)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
