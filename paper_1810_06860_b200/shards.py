@@ -214,6 +214,10 @@ class DeviceKernels:
             prep[slot] = A._hprep
         return A
 
+    def scaled_block(self, A, scale):
+        """scale * A's values on A's pattern, formed on the device."""
+        return A.scaled_on_device(scale)
+
     def block_like(self, A, data):
         B = SparseMatrix(A.rows, A.cols, A.indptr, A.indices, data)
         B.share_pattern(A)
@@ -245,15 +249,16 @@ class DeviceKernels:
         npart = int(_native.load().lr_svt_step_partials())
         part = device.arena().get("svt_partial", npart + 8)
         out2 = device.vector(2)
-        yc, yt = A.device_values()
+        yc = A.device_values_csr()
         _native.call("lr_svt_step_f64", device.ptr(dp.csr.ptr), device.ptr(dp.csr.idx), dp.csr.rows,
                      device.ptr(dp.csr.items), dp.csr.n_items, device.ptr(U), device.ld(U) if r else 1,
                      device.ptr(S_dev), device.ptr(V), device.ld(V) if r else 1, r, device.ptr(m_vals),
-                     device.ptr(yc), device.ptr(yt), device.ptr(dp.inv_perm), float(step), 1,
+                     device.ptr(yc), None, device.ptr(dp.inv_perm), float(step), 1,
                      device.ptr(part), npart, device.ptr(out2), device.stream(),
-                     meta={"nnz": A.nnz, "m": A.rows, "n": A.cols, "r": r})
+                     meta={"nnz": A.nnz, "m": A.rows, "n": A.cols, "r": r, "csc_scatter": False})
         A._host_stale = True
         A._dvals32 = None
+        A.mark_csc_stale()
         return out2
 
     def project(self, A, U, S_dev, V, r):
@@ -490,10 +495,18 @@ class ShardedEngine:
             pw.update(z)
         return pw.result()
 
+    @property
+    def _one_block(self) -> bool:
+        """This rank's row block and column block are the same entries (one
+        rank holds the whole matrix): one copy of Y serves both sides."""
+        return (self.r0, self.r1, self.c0, self.c1) == (0, self.m, 0, self.n)
+
     def start(self, scale: float) -> None:
+        """Y = scale * P_Phi(M) on both blocks, formed on the device from the
+        resident value copies (completion.py:335; as DeviceEngine.start)."""
         K = self.K
-        self.Y_r = K.block_like(self.phi_r, scale * K.host_values(self.phi_r))
-        self.Y_c = K.block_like(self.phi_c, scale * K.host_values(self.phi_c))
+        self.Y_r = K.scaled_block(self.phi_r, scale)
+        self.Y_c = self.Y_r if self._one_block else K.scaled_block(self.phi_c, scale)
 
     def step(self, U_s, S_s, V_s, r: int, step: float):
         K = self.K
@@ -503,8 +516,13 @@ class ShardedEngine:
             U_full = self.gather_m(U_s)
         else:
             V_full, U_full = V_s, U_s
+        # the row block's CSR copy serves Y X, the column block's CSC copy Y^T X:
+        # each step updates its block's CSR values (the column block's CSC copy
+        # is refreshed on demand by one gather, as on one GPU); a rank holding
+        # the whole matrix steps its one copy once
         part = K.svt_step(self.Y_r, self.m_r, U_s, S_dev, V_full, r, step)
-        K.svt_step(self.Y_c, self.m_c, U_full, S_dev, V_s, r, step)
+        if self.Y_c is not self.Y_r:
+            K.svt_step(self.Y_c, self.m_c, U_full, S_dev, V_s, r, step)
         st = self.ex.gather_scalars(part)
         sumsq, big = float(np.sum(st[:, 0])), float(np.max(st[:, 1]))
         if big == 0.0:

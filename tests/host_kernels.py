@@ -80,6 +80,9 @@ class HostKernels:
         B._rows, B._t = A._rows, A._t
         return B
 
+    def scaled_block(self, A, scale):
+        return self.block_like(A, float(scale) * A.vals)
+
     def host_values(self, A):
         return A.vals
 
