@@ -2,10 +2,15 @@
 // fp32 block A (K x n, row-major), the eigSVD Gram of linalg.py:189 in the
 // optional fp32 mode (north_star (2)).  tcgen05.mma kind::tf32 with the
 // 3xTF32 split -- a = hi + lo, both tf32, G ~ hi.hi + hi.lo + lo.hi -- so the
-// products carry ~22 mantissa bits; the accumulator lives in TMEM (fp32,
-// 128 lanes x 128 columns), one 128 x 128 tile of G per CTA over a chunk of
-// <= 4096 rows of A, and the chunk partials are summed in fp64 in a fixed
-// order by a second kernel (deterministic, no atomics).  Only tiles with
+// products carry ~22 mantissa bits; the accumulators live in TMEM (fp32,
+// 128 lanes x 128 columns each), one 128 x 128 tile of G per CTA over a chunk
+// of <= 2048 rows of A, and the chunk partials are summed in fp64 in a fixed
+// order by a second kernel (deterministic, no atomics).  The tensor core's
+// fp32 accumulation is not round-to-nearest: every MMA into an accumulator
+// loses ~0.4 ulp of it on average (one accumulator over 4096 rows: 4e-5
+// relative on the diagonal, r02ee), so the hi.hi products rotate over three
+// accumulators and the small hi.lo / lo.hi terms go to a fourth (85
+// roundings per accumulator and chunk, summed in the epilogue).  Only tiles with
 // ti <= tj run; the reduction mirrors them, so G is exactly symmetric.
 //
 // Staging: the fp32 -> (hi, lo) split needs the values in registers, so the
@@ -32,8 +37,9 @@ constexpr int UMMA_K = 8;                   // kind::tf32: K = 32 bytes per inst
 constexpr int OP_BYTES = TILE * BK * 4;     // one operand part (hi or lo): 16 KB
 constexpr int STAGE_BYTES = 4 * OP_BYTES;   // A hi, A lo, B hi, B lo
 constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 64;
-constexpr int MAX_CHUNK = 4096;             // rows per fp32 TMEM accumulation
-constexpr int TMEM_COLS = 128;
+constexpr int MAX_CHUNK = 2048;             // rows per fp32 TMEM accumulation
+constexpr int N_MAIN = 3;                   // rotating hi.hi accumulators (+1 for the hi.lo / lo.hi terms)
+constexpr int TMEM_COLS = 512;              // (N_MAIN + 1) x 128 columns, rounded to a power of two
 
 // instruction descriptor: D f32 (bits 4-5 = 1), A / B tf32 (bits 7-9, 10-12 = 2),
 // both K-major (bits 15, 16 = 0), N >> 3 at bit 17, M >> 4 at bit 24
@@ -212,9 +218,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
       for (int k = 0; k < BK / UMMA_K; ++k) {
         const uint64_t adv = (uint64_t)((k * UMMA_K * 4) >> 4);  // K step inside the 128-byte swizzle row
-        umma_tf32(tmem, a_hi + adv, b_hi + adv, (kb | k) != 0);
-        umma_tf32(tmem, a_hi + adv, b_lo + adv, 1u);
-        umma_tf32(tmem, a_lo + adv, b_hi + adv, 1u);
+        const int step = kb * (BK / UMMA_K) + k;
+        const uint32_t d_main = tmem + (uint32_t)((step % N_MAIN) * TILE);
+        const uint32_t d_corr = tmem + (uint32_t)(N_MAIN * TILE);
+        umma_tf32(d_main, a_hi + adv, b_hi + adv, step >= N_MAIN);
+        umma_tf32(d_corr, a_hi + adv, b_lo + adv, step != 0);
+        umma_tf32(d_corr, a_lo + adv, b_hi + adv, 1u);
       }
       umma_commit(&bars[s]);  // arrives when these MMAs (and all earlier ones) completed
     }
@@ -231,8 +240,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0;
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
-    float v[16];
+    float v[16], w[16];
     tmem_ld16(taddr + 16 * h, v);
+#pragma unroll
+    for (int a = 1; a <= N_MAIN; ++a) {  // fixed order: ((M0 + M1) + M2) + C
+      tmem_ld16(taddr + (uint32_t)(a * TILE) + 16 * h, w);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] += w[q];
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       reinterpret_cast<float4*>(out + 16 * h)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
