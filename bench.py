@@ -69,6 +69,25 @@ def cfg4_params(precision="fp64"):
                                 i_max=c["i_max"], precision=precision)
 
 
+def golden_cfg4_diff(res, mae):
+    """The timed job against the REAL reference's run of the same job
+    (tests/golden/reference_golden_cfg4.npz, tests/golden/make_golden_cfg4.py)."""
+    path = os.path.join(ROOT, "tests", "golden", "reference_golden_cfg4.npz")
+    if not os.path.exists(path):
+        return None
+    g = np.load(path)
+    n = min(len(res.trace), int(g["k"].shape[0]))
+    same_trace = [(t.k, t.r, t.p, t.q, t.svd_source) for t in res.trace[:n]] == [
+        (int(g["k"][i]), int(g["r"][i]), int(g["p"][i]), int(g["q"][i]), str(g["source"][i])) for i in range(n)]
+    out = {"iterations": int(g["k"].shape[0]), "converged": bool(g["converged"]),
+           "residual_abs_diff": abs(res.residual - float(g["residual"][-1])),
+           "heldout_mae_abs_diff": abs(mae - float(g["heldout_mae"])), "trace_identical": same_trace,
+           "reference_wall_s_8_threads": float(g["total_s"])}
+    if res.S.shape == g["S"].shape:
+        out["S_max_rel_diff"] = float(np.max(np.abs(res.S - g["S"]) / g["S"]))
+    return out
+
+
 def workload_svt():
     c = CFG4_SVT
     return (f"cfg4 rating shape 138493x26744, 18,000,237 train / 2,000,026 held out; svt_fast rSVD-BKI reuse-q "
@@ -540,7 +559,8 @@ def bench_svt_main(args, ws, rank, local):
         "job_result": {"iterations": res.iterations, "converged": res.converged, "rank": res.rank,
                        "residual": res.residual, "heldout_mae": mae, "ks": [t.k for t in res.trace][::5],
                        "sources": {s: sum(t.svd_source == s for t in res.trace) for s in
-                                   sorted({t.svd_source for t in res.trace})}},
+                                   sorted({t.svd_source for t in res.trace})},
+                       "vs_reference_run": golden_cfg4_diff(res, mae)},
         "e2e": {"value": e2e_value, "unit": "SVT iterations/s (cfg4 rating shape, svt_fast rSVD-BKI)",
                 "h2d_bytes_per_step": int(np.mean(h2d)) if h2d else 0,
                 "d2h_bytes_per_step": int(np.mean(d2h)) if d2h else 0, "s_per_job": e2e_wall,

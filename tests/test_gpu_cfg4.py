@@ -1,0 +1,69 @@
+"""cfg4 (BASELINE configs[3], the north-star rating workload) end to end on
+the GPU against the REAL reference run on the same inputs
+(tests/golden/make_golden_cfg4.py imports /root/reference/pkg/src and runs
+lowrank.completion.svt_fast to convergence; the fixture is committed).
+
+The job: workloads.cfg4() (138,493 x 26,744, 20,000,263 ratings, 10 % held
+out by the reference's split_observations), svt_fast rSVD-BKI reuse-q with
+bench.CFG4_SVT.  Bars (north_star): iteration count within 1, final relative
+residual on Phi and held-out MAE within 1e-6, singular values within 1e-8
+relative when the iteration counts agree, completed values at 4096 held-out
+cells within 1e-6 of the reference's."""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+lr = pytest.importorskip("paper_1810_06860_b200")
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_golden_cfg4.npz")
+
+
+@pytest.fixture(scope="module")
+def cfg4_job():
+    if not os.path.exists(GOLDEN):
+        pytest.fail(f"missing golden fixture {GOLDEN} (tests/golden/make_golden_cfg4.py)")
+    g = dict(np.load(GOLDEN, allow_pickle=False))
+    from paper_1810_06860_b200 import completion, workloads
+    from paper_1810_06860_b200.sparse import ObservationSet
+
+    tau_div, delta, eps, i_reuse, q_reuse, seed = (float(x) for x in g["cfg"])
+    o = workloads.cfg4()
+    obs = ObservationSet(o.m, o.n, o.rows, o.cols, o.values, o.split)
+    p = completion.SvtParams(tau=5.0 * o.n / tau_div, delta=delta, epsilon=eps, i_reuse=int(i_reuse),
+                             q_reuse=int(q_reuse), strategy="reuse-q", seed=int(seed), i_max=500)
+    res = completion.svt_fast(obs, p)
+    tr, tc, tv = obs.subset(ObservationSet.TEST)
+    pred = res.predict(tr, tc)
+    return g, res, pred, tv
+
+
+def test_cfg4_iterations_residual_and_heldout_mae(cfg4_job):
+    from paper_1810_06860_b200 import completion
+
+    g, res, pred, tv = cfg4_job
+    it_ref = int(g["k"].shape[0])
+    assert abs(res.iterations - it_ref) <= 1, (res.iterations, it_ref)
+    assert bool(res.converged) == bool(g["converged"])
+    assert abs(res.residual - float(g["residual"][-1])) <= 1e-6, (res.residual, float(g["residual"][-1]))
+    mae = completion.mae(pred, tv)
+    assert abs(mae - float(g["heldout_mae"])) <= 1e-6, (mae, float(g["heldout_mae"]))
+
+
+def test_cfg4_trace_spectrum_and_predictions(cfg4_job):
+    g, res, pred, _ = cfg4_job
+    n = min(len(res.trace), int(g["k"].shape[0]))
+    # the routing trace (k, r, p, q, source) is identical over the common prefix
+    got = [(t.k, t.r, t.p, t.q, t.svd_source) for t in res.trace[:n]]
+    exp = [(int(g["k"][i]), int(g["r"][i]), int(g["p"][i]), int(g["q"][i]), str(g["source"][i])) for i in range(n)]
+    assert got == exp
+    resid = np.array([t.residual for t in res.trace[:n]])
+    assert np.max(np.abs(resid - g["residual"][:n])) <= 1e-6
+    if res.iterations == int(g["k"].shape[0]):
+        S_ref = g["S"]
+        assert res.S.shape == S_ref.shape
+        assert float(np.max(np.abs(res.S - S_ref) / S_ref)) <= 1e-8
+    assert float(np.max(np.abs(pred[g["pred_index"]] - g["pred"]))) <= 1e-6
