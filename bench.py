@@ -244,7 +244,7 @@ def kernel_table(summary, total_ms, jobs, hbm_peak, fp64_peak):
             if bound == "hbm":
                 ach = d["bytes"] / (d["modeled_ms"] * 1e-3) / 1e9
                 entry.update(bound="hbm", achieved=ach, unit="GB/s", peak=hbm_peak, frac=ach / hbm_peak)
-                if name in ("lr_spmm_f64", "lr_svt_step_flat_f64", "lr_svt_step_f64") and d.get("gather"):
+                if name in ("lr_spmm_f64", "lr_spmm_hot_f64", "lr_svt_step_flat_f64", "lr_svt_step_f64") and d.get("gather"):
                     g = d["gather"] / (d["modeled_ms"] * 1e-3) / 1e9
                     entry.update(l2_gather_gbs=g, l2_gather_frac_of_l2_read=g / L2_READ_GBS)
             else:

@@ -60,6 +60,24 @@ int lr_spmm_f64(const int* ptr, const int* idx, const double* val, int rows,
                 const double* X, long long ldx, int w, double* Y, long long ldy,
                 double* scratch, void* stream);
 
+/* The same product with shared-memory / TMA staging of the block rows a
+ * skewed pattern gathers most (north_star (1): "shared-memory/TMA staging of
+ * block rows"; replaces the same scipy csr_matvecs call, sparse.py:153-170).
+ * idx_hot: the index stream with the hot_max most frequent indices (rank by
+ * occurrence count) stored as -(rank + 1), every other entry as in idx;
+ * hot_order[rank] = index.  Per column chunk the H most frequent rows of X
+ * that fit shared memory are packed into hot_buf (>= lr_spmm_hot_buf_doubles()
+ * doubles) and bulk-copied (cp.async.bulk + mbarrier) into every CTA's shared
+ * memory; gathers of those rows never leave the SM.  Results are bit-identical
+ * to lr_spmm_f64 (same chunks, lane map and summation order).  hot_max <=
+ * lr_spmm_hot_rows_max(). */
+int lr_spmm_hot_rows_max(void);
+long long lr_spmm_hot_buf_doubles(void);
+int lr_spmm_hot_f64(const int* ptr, const int* idx, const int* idx_hot, const int* hot_order, int hot_max,
+                    double* hot_buf, long long hot_buf_doubles, const double* val, int rows, const int* items,
+                    int n_items, const int* splits, int n_splits, const double* X, long long ldx, int w, double* Y,
+                    long long ldy, double* scratch, void* stream);
+
 /* fp32 mode (north_star: "optional fp32 path", singular values within 1e-4):
  * the same SpMM over fp32 values and fp32 dense blocks (float2 per lane and
  * column pair: half the gathered bytes of the fp64 kernel), w >= 2.  The

@@ -32,6 +32,9 @@ SIGNATURES = {
     "lr_sm_count": (_I, []),
     "lr_launch_count": (_LL, []),
     "lr_spmm_f64": (_I, [_P, _P, _P, _I, _P, _I, _P, _I, _P, _LL, _I, _P, _LL, _P, _P]),
+    "lr_spmm_hot_rows_max": (_I, []),
+    "lr_spmm_hot_buf_doubles": (_LL, []),
+    "lr_spmm_hot_f64": (_I, [_P, _P, _P, _P, _I, _P, _LL, _P, _I, _P, _I, _P, _I, _P, _LL, _I, _P, _LL, _P, _P]),
     "lr_spmm_f32": (_I, [_P, _P, _P, _I, _P, _I, _P, _I, _P, _LL, _I, _P, _LL, _P, _P]),
     "lr_csr_transpose_workspace_ints": (_LL, [_I, _I]),
     "lr_csr_transpose_i32": (_I, [_I, _I, _LL, _P, _P, _P, _P, _P, _P, _P, _LL, _P]),

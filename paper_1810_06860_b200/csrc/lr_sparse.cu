@@ -744,16 +744,75 @@ constexpr int kGroupBatch = 32;  // stored entries per group batch
 // Y (rows x w) = A X over a row-compressed pattern, w <= G T VE - shift.
 // Per output element the entries are accumulated in storage order (fma), as
 // in the item kernel above: results are bit-identical to it.
-template <int G, int T, int Q, typename Sc>
-__global__ void __launch_bounds__(256, LR_GRP_MINB) spmm_group_kernel(
+//
+// HOT (shared-memory staging of the block rows a skewed pattern gathers most):
+// the index stream holds -(rank + 1) for the hot_max most frequent indices
+// (rank by occurrence count, ties by index) and the plain index otherwise;
+// the CTA stages the packed chunks of the H most frequent rows of X (gathered
+// into `hot.buf` by hot_rows_kernel) into shared memory with one TMA bulk copy
+// (cp.async.bulk + mbarrier) while its first index batches are in flight, and
+// every gather of a rank < H reads shared memory instead of L2 (cfg4's Zipf
+// columns: the 1280 hottest of 26,744 carry ~60 % of the stored entries).
+// Ranks in [H, hot_max) look the index up in `order`.  The staged chunks are
+// copies of the chunks the plain kernel loads, the lane map and the summation
+// order are the same: results are bit-identical to the plain kernel.
+struct HotRows {
+  const void* buf;   // H x nchunk 16-byte chunks, packed (global)
+  const int* order;  // rank -> index, hot_max entries
+  int H, nchunk;
+};
+
+__device__ __forceinline__ unsigned hot_smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+constexpr int kHotThreads = 512;           // one CTA per SM owns the whole shared memory
+constexpr int kHotSmemBytes = 220 * 1024;  // staged rows (227 KB per CTA less the barrier / reserved)
+constexpr int kHotMaxRows = 4096;          // ranks encoded in the index stream
+
+template <typename CT>
+__global__ void hot_rows_kernel(const CT* __restrict__ Xs, long long ld_chunks, const int* __restrict__ order,
+                                int H, int nchunk, CT* __restrict__ buf) {
+  const long long total = (long long)H * nchunk;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int s = (int)(i / nchunk), k = (int)(i - (long long)s * nchunk);
+    buf[i] = __ldg(Xs + (long long)__ldg(order + s) * ld_chunks + k);
+  }
+}
+
+template <int G, int T, int Q, typename Sc, bool HOT = false>
+__global__ void __launch_bounds__(HOT ? kHotThreads : 256, HOT ? 1 : LR_GRP_MINB) spmm_group_kernel(
     const int* __restrict__ ptr, const int* __restrict__ idx, const Sc* __restrict__ val,
     const int* __restrict__ items, int n_items, const Sc* __restrict__ X, long long ldx, int w, int shift,
-    Sc* __restrict__ Y, long long ldy, Sc* __restrict__ scratch) {
+    Sc* __restrict__ Y, long long ldy, Sc* __restrict__ scratch, HotRows hot = HotRows{nullptr, nullptr, 0, 0}) {
   using C = Chunk16<Sc>;
   using CT = typename C::type;
   constexpr int VE = C::VE;
   constexpr int GROUPS = 32 / G;
   constexpr int KB = kGroupBatch / G;  // batch entries per lane
+  extern __shared__ __align__(128) unsigned char lr_hot_smem[];  // [0, 128): the barrier; rows behind it
+  unsigned long long& hot_bar = *reinterpret_cast<unsigned long long*>(lr_hot_smem);
+  if constexpr (HOT) {
+    const unsigned bytes = (unsigned)hot.H * (unsigned)hot.nchunk * 16u;
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(hot_smem_u32(&hot_bar)));
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(hot_smem_u32(&hot_bar)),
+                   "r"(bytes)
+                   : "memory");
+      for (unsigned off = 0; off < bytes; off += 32768u) {
+        const unsigned sz = bytes - off < 32768u ? bytes - off : 32768u;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                hot_smem_u32(lr_hot_smem + 128 + off)),
+            "l"(reinterpret_cast<const unsigned char*>(hot.buf) + off), "r"(sz), "r"(hot_smem_u32(&hot_bar))
+            : "memory");
+      }
+    }
+    __syncthreads();  // the barrier is initialised before anyone polls it
+  }
+  const CT* hot_rows = reinterpret_cast<const CT*>(lr_hot_smem + 128);
   const int lane = threadIdx.x & 31, g = lane % G, grp = lane / G, gbase = grp * G;
   const long long n_groups = (long long)gridDim.x * (blockDim.x >> 5) * GROUPS;
   long long it = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * GROUPS + grp;
@@ -775,6 +834,17 @@ __global__ void __launch_bounds__(256, LR_GRP_MINB) spmm_group_kernel(
 #pragma unroll
   for (int t = 0; t < T; ++t) acc[t] = C::zero();
   const Sc* Xs = X - shift;
+  if constexpr (HOT) {
+    // the staged rows have landed (phase 0 of the one-shot barrier)
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "HOT_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        "@!p bra HOT_WAIT_%=;\n"
+        "}\n" ::"r"(hot_smem_u32(&hot_bar))
+        : "memory");
+  }
   while (__any_sync(0xffffffffu, it < n_items)) {
     const bool act = it < n_items;
     const int nb = act ? min(kGroupBatch, cur.end - e) : 0;
@@ -797,13 +867,28 @@ __global__ void __launch_bounds__(256, LR_GRP_MINB) spmm_group_kernel(
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         const int ent = q0 + q;
-        const int j = __shfl_sync(0xffffffffu, jk[ent / G], gbase + ent % G);
+        int j = __shfl_sync(0xffffffffu, jk[ent / G], gbase + ent % G);
         vq[q] = __shfl_sync(0xffffffffu, vk[ent / G], gbase + ent % G);
-        const CT* xr = reinterpret_cast<const CT*>(Xs + (long long)j * ldx);
+        if constexpr (HOT) {
+          // one generic-address load serves both sources (no divergence
+          // between the groups of a warp)
+          const int rk = -j - 1;
+          const bool staged = j < 0 && rk < hot.H;
+          if (j < 0 && !staged) j = __ldg(hot.order + rk);
+          const CT* xr = staged ? hot_rows + (long long)rk * hot.nchunk
+                                : reinterpret_cast<const CT*>(Xs + (long long)j * ldx);
 #pragma unroll
-        for (int t = 0; t < T; ++t) {
-          const int c = (g + G * t) * VE - shift;  // first column of the chunk
-          xv[q][t] = (ent < nb && c + VE > 0 && c < w) ? __ldg(xr + g + G * t) : C::zero();
+          for (int t = 0; t < T; ++t) {
+            const int c = (g + G * t) * VE - shift;
+            xv[q][t] = (ent < nb && c + VE > 0 && c < w) ? xr[g + G * t] : C::zero();
+          }
+        } else {
+          const CT* xr = reinterpret_cast<const CT*>(Xs + (long long)j * ldx);
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            const int c = (g + G * t) * VE - shift;  // first column of the chunk
+            xv[q][t] = (ent < nb && c + VE > 0 && c < w) ? __ldg(xr + g + G * t) : C::zero();
+          }
         }
       }
 #pragma unroll
@@ -1118,10 +1203,57 @@ static void launch_spmm_group_t(const int* ptr, const int* idx, const Sc* val, c
                                                              ldy, scratch);
 }
 
+// host-side description of a pattern side's hot-row encoding (see HotRows)
+struct HotDesc {
+  const int* idx_hot;   // the index stream with the hot ranks encoded
+  const int* order;     // rank -> index
+  int hot_max;          // ranks encoded (<= kHotMaxRows)
+  void* buf;            // staging block in global memory
+  long long buf_bytes;
+};
+
+// rows staged for a chunk of nchunk 16-byte chunks per row (0: not worth a launch)
+static int hot_rows_for(const HotDesc* hd, int nchunk) {
+  if (!hd || !hd->idx_hot || !hd->order || !hd->buf || nchunk <= 0) return 0;
+  long long H = kHotSmemBytes / ((long long)nchunk * 16);
+  if (H > hd->hot_max) H = hd->hot_max;
+  if (H > hd->buf_bytes / ((long long)nchunk * 16)) H = hd->buf_bytes / ((long long)nchunk * 16);
+  return H >= 32 ? (int)H : 0;
+}
+
+template <int G, int T, typename Sc>
+static void launch_spmm_hot_t(const int* ptr, const HotDesc* hd, int H, int nchunk, const Sc* val, const int* items,
+                              int n_items, const Sc* X, long long ldx, int w, int shift, Sc* Y, long long ldy,
+                              Sc* scratch, cudaStream_t s) {
+  using CT = typename Chunk16<Sc>::type;
+  constexpr int VE = Chunk16<Sc>::VE;
+  constexpr int Q = T <= 2 ? LR_SPMM_QLO : LR_SPMM_QHI;
+  constexpr int GROUPS = 32 / G;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(spmm_group_kernel<G, T, Q, Sc, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         128 + kHotSmemBytes);
+    attr = true;
+  }
+  const long long total = (long long)H * nchunk;
+  int gb = (int)((total + 255) / 256);
+  if (gb > sm_count() * 4) gb = sm_count() * 4;
+  hot_rows_kernel<CT><<<gb, 256, 0, s>>>(reinterpret_cast<const CT*>(X - shift), ldx / VE, hd->order, H, nchunk,
+                                         reinterpret_cast<CT*>(hd->buf));
+  const long long warps = ((long long)n_items + GROUPS - 1) / GROUPS;
+  long long blocks = (warps + kHotThreads / 32 - 1) / (kHotThreads / 32);
+  if (blocks > sm_count()) blocks = sm_count();
+  if (blocks < 1) blocks = 1;
+  HotRows hot{hd->buf, hd->order, H, nchunk};
+  spmm_group_kernel<G, T, Q, Sc, true><<<(int)blocks, kHotThreads, 128 + (size_t)total * 16, s>>>(
+      ptr, hd->idx_hot, val, items, n_items, X, ldx, w, shift, Y, ldy, scratch, hot);
+}
+
 // the group kernel for one column chunk; false: not applicable (unaligned rows)
 template <typename Sc>
 static bool spmm_group(const int* ptr, const int* idx, const Sc* val, const int* items, int n_items, const Sc* X,
-                       long long ldx, int w, Sc* Y, long long ldy, Sc* scratch, cudaStream_t s) {
+                       long long ldx, int w, Sc* Y, long long ldy, Sc* scratch, cudaStream_t s,
+                       const HotDesc* hd = nullptr) {
   static const char* fam = getenv("LR_SPMM_KERNEL");
   if (fam && fam[0] == 'i') return false;  // "items": the round-1 kernel
   constexpr int VE = 16 / (int)sizeof(Sc);
@@ -1130,7 +1262,22 @@ static bool spmm_group(const int* ptr, const int* idx, const Sc* val, const int*
   const int shift = ((ldx * (long long)sizeof(Sc)) % 128 == 0)
                         ? (int)((reinterpret_cast<uintptr_t>(X) & 127u) / sizeof(Sc)) : 0;
   int G, T;
-  if (!pick_group((w + shift + VE - 1) / VE, G, T)) return false;
+  const int nchunk = (w + shift + VE - 1) / VE;
+  if (!pick_group(nchunk, G, T)) return false;
+  if constexpr (sizeof(Sc) == 8) {
+    const int H = hot_rows_for(hd, nchunk);
+    if (H > 0) {
+#define LR_SPH(g, t)                                                                                         \
+  if (G == g && T == t) {                                                                                    \
+    launch_spmm_hot_t<g, t, Sc>(ptr, hd, H, nchunk, val, items, n_items, X, ldx, w, shift, Y, ldy, scratch,  \
+                                s);                                                                          \
+    return true;                                                                                             \
+  }
+      LR_SPH(4, 1) LR_SPH(8, 1) LR_SPH(8, 2) LR_SPH(8, 3) LR_SPH(8, 4) LR_SPH(16, 1) LR_SPH(16, 2) LR_SPH(16, 3)
+      LR_SPH(16, 4) LR_SPH(32, 1) LR_SPH(32, 2) LR_SPH(32, 3) LR_SPH(32, 4)
+#undef LR_SPH
+    }
+  }
 #define LR_SPG(g, t)                                                                                         \
   if (G == g && T == t) {                                                                                    \
     launch_spmm_group_t<g, t, Sc>(ptr, idx, val, items, n_items, X, ldx, w, shift, Y, ldy, scratch, s);     \
@@ -1148,7 +1295,7 @@ static bool spmm_group(const int* ptr, const int* idx, const Sc* val, const int*
 template <typename Sc>
 static int spmm_cols(const int* ptr, const int* idx, const Sc* val, const int* items, int n_items,
                      const int* splits, int n_splits, const Sc* X, long long ldx, int w, Sc* Y, long long ldy,
-                     Sc* scratch, cudaStream_t s) {
+                     Sc* scratch, cudaStream_t s, const HotDesc* hd = nullptr) {
   // Products wider than kChunkCols run as column chunks: each chunk's slice
   // of X stays L2-resident while every stored entry gathers from it (the
   // W-column Y^T Q of BKI at cfg2 is 528 MB), and the <= 128-column tiles run
@@ -1192,7 +1339,7 @@ static int spmm_cols(const int* ptr, const int* idx, const Sc* val, const int* i
     const bool v2 = (ldx % 2 == 0) && (ldy % 2 == 0) && aligned_bytes(Xc, kVecBytes) &&
                     aligned_bytes(Yc, kVecBytes) &&
                     (scratch == nullptr || (aligned_bytes(scratch, kVecBytes) && cw % 2 == 0));
-    if (spmm_group<Sc>(ptr, idx, val, items, n_items, Xc, ldx, cw, Yc, ldy, scratch, s))
+    if (spmm_group<Sc>(ptr, idx, val, items, n_items, Xc, ldx, cw, Yc, ldy, scratch, s, hd))
       ;
     else if (v2)
       dispatch_spmm<true, Sc>(ptr, idx, val, items, n_items, Xc, ldx, cw, Yc, ldy, scratch, s);
@@ -1354,6 +1501,25 @@ int lr_spmm_f64(const int* ptr, const int* idx, const double* val, int rows, con
     return LR_OK;
   }
   return spmm_cols<double>(ptr, idx, val, items, n_items, splits, n_splits, X, ldx, w, Y, ldy, scratch, s);
+}
+
+int lr_spmm_hot_rows_max(void) { return kHotMaxRows; }
+
+long long lr_spmm_hot_buf_doubles(void) { return kHotSmemBytes / 8; }
+
+int lr_spmm_hot_f64(const int* ptr, const int* idx, const int* idx_hot, const int* hot_order, int hot_max,
+                    double* hot_buf, long long hot_buf_doubles, const double* val, int rows, const int* items,
+                    int n_items, const int* splits, int n_splits, const double* X, long long ldx, int w, double* Y,
+                    long long ldy, double* scratch, void* stream) {
+  LR_REQUIRE(w >= 2 && ldx >= w && ldy >= w, "spmm_hot: bad widths (w=%d ldx=%lld ldy=%lld; w >= 2)", w, ldx, ldy);
+  LR_REQUIRE(idx && idx_hot && hot_order && hot_buf && hot_max >= 1 && hot_max <= kHotMaxRows,
+             "spmm_hot: hot-row encoding missing (hot_max=%d, at most %d)", hot_max, kHotMaxRows);
+  if (rows == 0) return LR_OK;
+  if (!items) n_items = rows;
+  LR_REQUIRE(n_splits == 0 || scratch, "spmm_hot: split schedule needs scratch");
+  HotDesc hd{idx_hot, hot_order, hot_max, hot_buf, hot_buf_doubles * 8};
+  return spmm_cols<double>(ptr, idx, val, items, n_items, splits, n_splits, X, ldx, w, Y, ldy, scratch,
+                           as_stream(stream), &hd);
 }
 
 int lr_spmm_f32(const int* ptr, const int* idx, const float* val, int rows, const int* items, int n_items,

@@ -52,6 +52,7 @@ def gemm_model(meta):
 
 
 MODELS = {"lr_spmm_f64": ("hbm", spmm_model), "lr_spmm_f32": ("hbm", spmm_model),
+          "lr_spmm_hot_f64": ("hbm", spmm_model),
           "lr_svt_step_f64": ("hbm", svt_model), "lr_svt_step_flat_f64": ("hbm", svt_model), "lr_gather_f64": ("hbm", gather_model),
           "lr_gemm_f64": ("tensor", gemm_model)}
 
@@ -61,7 +62,7 @@ def gather_bytes(name, meta):
     (SVT step) values per stored entry."""
     if meta is None:
         return 0
-    if name in ("lr_spmm_f64", "lr_spmm_f32"):
+    if name in ("lr_spmm_f64", "lr_spmm_f32", "lr_spmm_hot_f64"):
         return meta.get("bytes_per_value", 8) * meta["nnz"] * meta["w"]
     if name in ("lr_svt_step_f64", "lr_svt_step_flat_f64"):
         return 8 * meta["nnz"] * meta["r"]

@@ -55,7 +55,13 @@ SPECULATIVE = True
 # i.e. at most ~2e-10 relative error in Y^T Q1 (the parity bar is 1e-8).
 KRYLOV_REUSE = True
 KRYLOV_REUSE_KAPPA = 1e6  # cfg4 job: kappa_F(H) 2e3 .. 1.2e5 (profiles/r02u_cfg4_timeline.txt)
-REUSE_STATS = {"used": 0, "kappa_gate": 0, "kappas": []}
+REUSE_STATS = {"used": 0, "kappa_gate": 0, "kappas": [], "skipped": 0}
+# (m, n, nnz, w, p) -> the last call of that shape tripped the kappa gate: the
+# next one does not queue the reuse projection at all (cfg2 at p = 5 trips it
+# every call: a dropped projection is an n x W x W product, a W x W eigensolve
+# and two lifts, ~7 ms of a 23 ms call).  kappa_F(H) is still read on every
+# call, so the route comes back as soon as one call passes the gate.
+_REUSE_GATED = {}
 
 
 @dataclass
@@ -451,7 +457,11 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
     if not use_pre:
         _overlap_draw_with_upload(A, params.seed, n, w, omega or OMEGA_SOURCE)
     Om = None if use_pre else _omega(params.seed, n, w, omega or OMEGA_SOURCE)
-    reuse = KRYLOV_REUSE and spec and lazy and not fp32 and params.p >= 1
+    reuse_ok = KRYLOV_REUSE and spec and lazy and not fp32 and params.p >= 1
+    gate_key = (m, n, int(A.nnz), w, params.p)
+    reuse = reuse_ok and not _REUSE_GATED.get(gate_key, False)
+    if reuse_ok and not reuse:
+        REUSE_STATS["skipped"] += 1
     H, Q, lu_status, probe = _krylov_orth(A, Om, params, spec, fp32, lazy, fb, pre=pre if use_pre else None,
                                           keep_T=reuse)
     T_pre = None
@@ -471,18 +481,23 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
             # the Krylov blocks are exactly the careful path's (H is untouched
             # by the speculative orth): only the orthonormalisation is redone
             Q = _orthonormalize(H, fb, lazy_last=lazy)
-        elif reuse and isinstance(Q, LazyQ) and getattr(Q, "T_all", None) is not None:
+        elif reuse_ok and isinstance(Q, LazyQ):
             Wn = diag_h.shape[0] // 3
             kappa = float(np.sqrt(np.sum(diag_h[0:Wn]) * device.to_host(probe[2])[0]))
             if len(REUSE_STATS["kappas"]) < 4096:
                 REUSE_STATS["kappas"].append(kappa)
-            if np.isfinite(kappa) and kappa <= KRYLOV_REUSE_KAPPA:
+            passes = bool(np.isfinite(kappa) and kappa <= KRYLOV_REUSE_KAPPA)
+            if len(_REUSE_GATED) > 4096:
+                _REUSE_GATED.clear()
+            _REUSE_GATED[gate_key] = not passes
+            if fin_spec is not None and passes:
                 REUSE_STATS["used"] += 1
                 res = fin_spec()  # the speculatively queued projection stands
                 if isinstance(Q, LazyQ):
                     Q.T_all = Q.R1inv = None  # the cached basis (reuse-q) must not pin them
                 return res, Q, fb.count
-            REUSE_STATS["kappa_gate"] += 1
+            if fin_spec is not None:
+                REUSE_STATS["kappa_gate"] += 1  # queued and dropped
         if isinstance(Q, LazyQ):
             Q.T_all = Q.R1inv = None
     res = project_and_solve(A, Q, params.k, fb, "fp32" if fp32 else "fp64", download=download, T_pre=T_pre)

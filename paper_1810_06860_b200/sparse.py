@@ -122,6 +122,63 @@ class _Side:
             splits = None if splits is None else splits.ravel()
         self.items = None if items is None else device.int_buffer(items)
         self.splits = None if splits is None else device.int_buffer(splits)
+        self.counts_ptr = None  # the other orientation's offsets: their differences count this side's indices
+        self._hot = False  # not examined yet; None: the pattern is not skewed enough
+
+    def hot(self):
+        """Hot-row encoding of this side's index stream for lr_spmm_hot_f64,
+        built on the device once per pattern: (idx_hot, order, hot_max,
+        share) with share[h - 1] = the fraction of stored entries whose index
+        is among the h most frequent; None when staging the most frequent
+        rows would serve less than HOT_MIN_SHARE of the gathers (uniform
+        patterns: cfg2, cfg5)."""
+        if self._hot is not False:
+            return self._hot
+        self._hot = None
+        nnz = int(self.idx.numel())
+        if not HOT_ROWS or self.counts_ptr is None or nnz < HOT_MIN_NNZ:
+            return None
+        cp = self.counts_ptr
+        n_idx = int(cp.numel()) - 1
+        hmax = min(int(_native.load().lr_spmm_hot_rows_max()), n_idx)
+        if hmax < 32:
+            return None
+        cnt = (cp[1:] - cp[:-1]).to(torch.int64)
+        # most frequent first, ties to the smaller index
+        key = cnt * n_idx + (n_idx - 1 - torch.arange(n_idx, device=cnt.device, dtype=torch.int64))
+        top = torch.topk(key, hmax, sorted=True).indices
+        share = (torch.cumsum(cnt[top], 0).to(torch.float64) / max(nnz, 1)).cpu().numpy()
+        if share[min(hmax, HOT_PROBE_ROWS) - 1] < HOT_MIN_SHARE:
+            return None
+        rank = torch.full((n_idx,), -1, dtype=torch.int32, device=cnt.device)
+        rank[top] = torch.arange(hmax, device=cnt.device, dtype=torch.int32)
+        idx_hot = torch.empty_like(self.idx)
+        step = 1 << 24  # bounded temporaries
+        for b in range(0, nnz, step):
+            seg = self.idx[b:b + step]
+            r = rank[seg.long()]
+            idx_hot[b:b + step] = torch.where(r >= 0, -(r + 1), seg)
+        self._hot = (idx_hot, top.to(torch.int32).contiguous(), hmax, share)
+        return self._hot
+
+
+# Shared-memory staging of the most frequent block rows (lr_spmm_hot_f64;
+# north_star (1) "shared-memory/TMA staging of block rows"): opt-in
+# (LR_SPMM_HOT=1).  Bit-identical to the plain kernel, but measured 2-3x
+# SLOWER on cfg4 (profiles/r02ab_spmm_hot_probe.txt, r02ab_ncu_spmm_hot22.txt):
+# the 1280 rows that fit shared memory at w = 22 serve only 39 % of the
+# gathers (columns; 34 % for rows), every batch of 8 gathers still waits for
+# its slowest L2 round trip (the kernel is latency-bound, not bandwidth-bound),
+# the shared-memory carve-out leaves 28 KB of L1 (hit rate 22 % -> 2 %) and the
+# two-source addressing nearly doubles the instruction count.  When enabled it
+# is used when the HOT_PROBE_ROWS most frequent indices of a side carry at
+# least HOT_MIN_SHARE of its stored entries and, per product, when the rows
+# that fit shared memory at that width still do.
+HOT_ROWS = __import__("os").environ.get("LR_SPMM_HOT", "0") == "1"
+HOT_MIN_SHARE = float(__import__("os").environ.get("LR_SPMM_HOT_SHARE", "0.25"))
+HOT_PROBE_ROWS = 1024
+HOT_MIN_NNZ = 1 << 20
+_HOT_SMEM_BYTES = 220 * 1024
 
 
 class _HostPrep:
@@ -187,6 +244,7 @@ class DevicePattern:
         if hp.csc_sched is None:  # first upload of this pattern: offsets come back once
             hp.csc_sched = _schedule(device.to_host(t_ptr).astype(np.int64))
         self.csc = _Side(rows=A.cols, ptr=t_ptr, idx=t_idx, sched=hp.csc_sched)
+        self.csr.counts_ptr, self.csc.counts_ptr = self.csc.ptr, self.csr.ptr
 
     def tile_rows(self):
         """Row of the first slot of every flat SVT tile (lr_svt_tile_rows_i32),
@@ -573,6 +631,22 @@ def _spmm_side(side: _Side, vals, X, out=None):
     scratch = None
     if side.n_splits:
         scratch = device.arena().get("spmm_scratch", side.n_slots * max(w, 1) + 2)
+    hot = side.hot() if w >= 2 else None
+    if hot is not None:
+        # rows of a <= 128-column chunk that fit shared memory, and the share of the gathers they serve
+        fit = _HOT_SMEM_BYTES // (((min(w, 128) + 1) // 2) * 16)
+        if fit < 32 or hot[3][min(fit, hot[2]) - 1] < HOT_MIN_SHARE:
+            hot = None
+    if hot is not None:
+        nbuf = int(_native.load().lr_spmm_hot_buf_doubles())
+        hbuf = device.arena().get("spmm_hot_buf", nbuf)
+        _native.call("lr_spmm_hot_f64", device.ptr(side.ptr), device.ptr(side.idx), device.ptr(hot[0]),
+                     device.ptr(hot[1]), hot[2], device.ptr(hbuf), nbuf, device.ptr(vals), side.rows,
+                     device.ptr(side.items), side.n_items if side.items is not None else side.rows,
+                     device.ptr(side.splits), side.n_splits, device.ptr(X), device.ld(X), w,
+                     device.ptr(out), device.ld(out), device.ptr(scratch), device.stream(),
+                     meta={"nnz": int(side.idx.numel()), "rows": side.rows, "cols": int(X.shape[0]), "w": w})
+        return out
     _native.call("lr_spmm_f64", device.ptr(side.ptr), device.ptr(side.idx), device.ptr(vals), side.rows,
                  device.ptr(side.items), side.n_items if side.items is not None else side.rows,
                  device.ptr(side.splits), side.n_splits, device.ptr(X), device.ld(X), w,

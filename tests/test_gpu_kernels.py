@@ -55,6 +55,48 @@ def test_spmm_and_spmm_t_match_oracle(w):
     assert np.linalg.norm(spmm_t(A, H) - ref_t) <= 1e-12 * np.linalg.norm(ref_t)
 
 
+@pytest.mark.parametrize("w", [2, 5, 16, 22, 45, 89, 132, 260])
+def test_spmm_hot_rows_bit_identical(w, monkeypatch):
+    """lr_spmm_hot_f64 (the most frequent block rows staged in shared memory
+    by one TMA bulk copy; opt-in, LR_SPMM_HOT=1) against lr_spmm_f64 on a
+    Zipf-skewed pattern with dense rows / columns (split schedule): the same
+    chunks, lane map and summation order, so bit-identical on both sides;
+    ranks past the staged rows go through the order lookup (w = 260: 128-column
+    chunks stage ~220 of the 600 encoded rows)."""
+    import torch
+
+    from paper_1810_06860_b200 import device, sparse
+    from paper_1810_06860_b200.sparse import SparseMatrix, spmm_dev, spmm_t_dev
+
+    m, n, nnz = 3000, 600, 150000
+    rng = np.random.default_rng(w)
+    pj = 1.0 / np.arange(1, n + 1) ** 0.9
+    pi = 1.0 / np.arange(1, m + 1)
+    j = rng.permutation(n)[rng.choice(n, size=nnz, p=pj / pj.sum())]
+    i = rng.permutation(m)[rng.choice(m, size=nnz, p=pi / pi.sum())]
+    key = np.unique(np.concatenate([i * n + j, np.arange(n), (m - 1) * n + np.arange(n), np.arange(m) * n + 7]))
+    i, j = np.divmod(key, n)
+    A = SparseMatrix.from_coo(m, n, i, j, rng.standard_normal(i.shape[0]))
+    X = device.to_device(rng.standard_normal((n, w)))
+    H = device.to_device(rng.standard_normal((m, w)))
+    y0, t0 = spmm_dev(A, X), spmm_t_dev(A, H)
+    monkeypatch.setattr(sparse, "HOT_ROWS", True)
+    monkeypatch.setattr(sparse, "HOT_MIN_NNZ", 0)
+    monkeypatch.setattr(sparse, "HOT_MIN_SHARE", 0.0)
+    dp = A.pattern()
+    dp.csr._hot = dp.csc._hot = False  # examine the sides again under the opt-in
+    assert dp.csr.hot() is not None and dp.csc.hot() is not None
+    hot_c = dp.csr.hot()
+    assert int((hot_c[0] < 0).sum()) == int(round(hot_c[3][-1] * A.nnz))  # encoded entries = the top ranks' share
+    calls = []
+    from paper_1810_06860_b200 import _native
+    real = _native.call
+    monkeypatch.setattr(_native, "call", lambda name, *a, **k: (calls.append(name), real(name, *a, **k))[1])
+    y1, t1 = spmm_dev(A, X), spmm_t_dev(A, H)
+    assert calls == ["lr_spmm_hot_f64", "lr_spmm_hot_f64"]
+    assert torch.equal(y0, y1) and torch.equal(t0, t1)
+
+
 def test_spmm_golden(golden):
     from paper_1810_06860_b200.sparse import SparseMatrix, spmm, spmm_t
 

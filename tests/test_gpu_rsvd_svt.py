@@ -527,3 +527,31 @@ def test_bki_krylov_reuse_matches_wide_product():
     assert np.max(np.abs(r1.S - r0.S) / r0.S) <= max(1e-13, 8 * np.finfo(float).eps * kappa)
     assert np.linalg.norm(r1.U @ (r1.U.T @ r0.U) - r0.U) <= 1e-9 * np.sqrt(20)
     assert np.linalg.norm(r1.V @ (r1.V.T @ r0.V) - r0.V) <= 1e-9 * np.sqrt(20)
+
+
+def test_bki_krylov_reuse_gate_is_remembered(monkeypatch):
+    """A call whose kappa_F(H) trips the reuse gate drops its queued projection
+    and takes the W-wide product; the next call of the same shape queues
+    nothing (rsvd._REUSE_GATED) and is bit-identical to it; the route comes
+    back once a call passes the gate again."""
+    from paper_1810_06860_b200 import rsvd, workloads
+    from paper_1810_06860_b200.sparse import SparseMatrix
+
+    obs = workloads.uniform_sparse(90000, 40000, 1_000_000, seed=22)
+    A = SparseMatrix.from_coo(obs.m, obs.n, obs.rows, obs.cols, obs.values)
+    prm = rsvd.RsvdParams(k=20, p=3, s=10, seed=6)
+    rsvd._REUSE_GATED.clear()
+    monkeypatch.setattr(rsvd, "KRYLOV_REUSE_KAPPA", 1.0)  # every call trips the gate
+    st = rsvd.REUSE_STATS
+    g0, s0, u0 = st["kappa_gate"], st["skipped"], st["used"]
+    r1, _ = rsvd.rsvd_bki(A, prm)
+    assert (st["kappa_gate"], st["skipped"], st["used"]) == (g0 + 1, s0, u0)
+    r2, _ = rsvd.rsvd_bki(A, prm)
+    assert (st["kappa_gate"], st["skipped"], st["used"]) == (g0 + 1, s0 + 1, u0)
+    assert np.array_equal(r1.S, r2.S) and np.array_equal(r1.U, r2.U) and np.array_equal(r1.V, r2.V)
+    monkeypatch.setattr(rsvd, "KRYLOV_REUSE_KAPPA", 1e6)
+    r3, _ = rsvd.rsvd_bki(A, prm)  # still the wide product, but the gate reopens
+    assert st["skipped"] == s0 + 2 and np.array_equal(r3.S, r1.S)
+    r4, _ = rsvd.rsvd_bki(A, prm)
+    assert st["used"] == u0 + 1
+    assert np.max(np.abs(r4.S - r1.S) / r1.S) <= 1e-9
