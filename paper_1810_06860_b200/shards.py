@@ -383,10 +383,22 @@ class ShardedEngine:
         self.ex = exchange if exchange is not None else Exchange()
         self.K = kernels if kernels is not None else DeviceKernels()
         self.rank, self.world = self.ex.rank, self.ex.world
-        r, c, v = obs.subset(ObservationSet.TRAIN)
-        phi = SparseMatrix.from_coo(obs.m, obs.n, r, c, v)  # host: same ordering / validation everywhere
-        if phi.nnz == 0:
-            raise DataError("no observed entries to complete from")
+        if isinstance(self.K, DeviceKernels):
+            # every rank builds the train CSR on its own device (the same
+            # validation and bit-exact ordering as the single-GPU engine; the
+            # host lexsort of cfg4's 18M cells costs seconds) and cuts its two
+            # blocks out of it there
+            phi = obs.train_matrix()
+            if phi.nnz == 0:
+                raise DataError("no observed entries to complete from")
+            if phi._dev_csr is not None:
+                self._setup_device(phi)
+                return
+        else:
+            r, c, v = obs.subset(ObservationSet.TRAIN)
+            phi = SparseMatrix.from_coo(obs.m, obs.n, r, c, v)  # host: same ordering / validation everywhere
+            if phi.nnz == 0:
+                raise DataError("no observed entries to complete from")
         self._setup(phi)
 
     @classmethod
@@ -434,6 +446,52 @@ class ShardedEngine:
         self.m_r = K.values(self.phi_r)
         self.m_c = K.values(self.phi_c)
         self.Y_r, self.Y_c = self.phi_r, self.phi_c  # rsvd on the observed matrix itself until start()
+        self.m_norm = None
+
+    def _setup_device(self, phi: SparseMatrix) -> None:
+        """_setup for a device-built CSR (ObservationSet.train_matrix): the
+        plan from the host offsets and the device column counts, the row block
+        as a slice of the CSR arrays, the column block by one masked selection
+        in CSR order (the entries a host `flatnonzero` would pick, in the same
+        order).  A rank that holds the whole matrix keeps one block."""
+        import torch
+
+        K = self.K
+        self.m, self.n = phi.shape
+        self.nnz = phi.nnz
+        ptr_d, idx_d, vals_d = phi._dev_csr
+        if vals_d is None:
+            vals_d = phi.device_values()[0]
+        ip = phi.indptr
+        counts = torch.bincount(idx_d.long(), minlength=self.n)
+        t_indptr = np.zeros(self.n + 1, dtype=np.int64)
+        np.cumsum(counts.cpu().numpy(), out=t_indptr[1:])
+        self.plan = plan = ShardPlan(ip, t_indptr, self.world)
+        self.r0, self.r1 = r0, r1 = plan.rows(self.rank)
+        self.c0, self.c1 = c0, c1 = plan.cols(self.rank)
+        if (r0, r1, c0, c1) == (0, self.m, 0, self.n):
+            self.phi_r = self.phi_c = phi
+        else:
+            lo, hi = int(ip[r0]), int(ip[r1])
+            # fresh allocations: every array of a block starts on an allocation boundary
+            self.phi_r = SparseMatrix.from_device_csr(
+                r1 - r0, self.n, ip[r0:r1 + 1] - lo, (ptr_d[r0:r1 + 1] - lo).contiguous(), idx_d[lo:hi].clone(),
+                vals_d[lo:hi].clone())
+            sel = torch.nonzero((idx_d >= c0) & (idx_d < c1)).view(-1)  # CSR order
+            row_of = torch.searchsorted(ptr_d[1:].long().contiguous(), sel, right=True)
+            ccount = torch.bincount(row_of, minlength=self.m)
+            cptr_h = np.zeros(self.m + 1, dtype=np.int64)
+            np.cumsum(ccount.cpu().numpy(), out=cptr_h[1:])
+            self.phi_c = SparseMatrix.from_device_csr(
+                self.m, c1 - c0, cptr_h, torch.from_numpy(cptr_h.astype(np.int32)).to(idx_d.device),
+                (idx_d[sel] - c0).to(torch.int32), vals_d[sel].contiguous())
+            del sel, row_of, ccount
+        self.phi_r.device_values()
+        if self.phi_c is not self.phi_r:
+            self.phi_c.device_values()
+        self.m_r = K.values(self.phi_r)
+        self.m_c = K.values(self.phi_c)
+        self.Y_r, self.Y_c = self.phi_r, self.phi_c
         self.m_norm = None
 
     # ------------------------------------------------------------ helpers

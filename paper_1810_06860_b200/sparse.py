@@ -380,6 +380,27 @@ class SparseMatrix:
         out._dev_csr = (ptr, col[:nnz], vals[:nnz])
         return out
 
+    @classmethod
+    def from_device_csr(cls, rows: int, cols: int, indptr_host, ptr, idx, vals) -> "SparseMatrix":
+        """A matrix whose CSR arrays already sit on the device (int32 ptr of
+        rows + 1 offsets, int32 idx, float64 vals: e.g. a row or column block
+        cut out of a device-built CSR, shards.py): the host keeps indptr (the
+        work schedule needs it); indices and values come back on access.  The
+        arrays are trusted (they come from a validated matrix)."""
+        out = cls.__new__(cls)
+        out.rows, out.cols = int(rows), int(cols)
+        out.indptr = np.ascontiguousarray(indptr_host, dtype=np.int64)
+        nnz = int(out.indptr[-1]) if out.indptr.size else 0
+        out._indices = None
+        out._data = np.empty(nnz)
+        out._tperm = out._t_indptr = out._t_indices = out._coo_rows = None
+        out._pattern = None
+        out._dvals = None
+        out._host_stale = True
+        out._csc_stale = False
+        out._dev_csr = (ptr, idx, vals)
+        return out
+
     # ------------------------------------------------------------ checks
     def _validate(self) -> None:
         if self.rows < 1 or self.cols < 1:

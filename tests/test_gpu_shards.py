@@ -85,3 +85,48 @@ def test_sharded_world1_equals_single_engine():
     assert [t.r for t in a.trace] == [t.r for t in b.trace]
     np.testing.assert_allclose([t.residual for t in b.trace], [t.residual for t in a.trace], rtol=1e-10)
     np.testing.assert_allclose(b.S, a.S, rtol=1e-10)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_device_cut_blocks_match_host_cut(world):
+    """ShardedEngine's device setup (the train CSR built on the device, the
+    row block sliced and the column block selected there) against the host
+    setup (lexsort + flatnonzero) for every rank of a `world`-rank plan:
+    identical plans, offsets, indices, values and split tags honoured; the
+    blocks' products agree bit for bit."""
+    import torch
+
+    from paper_1810_06860_b200 import device
+    from paper_1810_06860_b200.shards import DeviceKernels, Exchange, ShardedEngine
+    from paper_1810_06860_b200.sparse import ObservationSet, SparseMatrix
+
+    rng = np.random.default_rng(world)
+    m, n, nnz = 900, 700, 40000
+    flat = rng.choice(m * n, size=nnz, replace=False)
+    i, j = np.divmod(flat, n)
+    v = rng.standard_normal(nnz)
+    split = (rng.random(nnz) < 0.1).astype(np.uint8)  # 10 % held out
+    X = device.to_device(rng.standard_normal((n, 7)))
+    H = device.to_device(rng.standard_normal((m, 7)))
+    for rank in range(world):
+        ex = Exchange()
+        ex.rank, ex.world = rank, world  # a plan for `world` ranks; no collective runs in the setup
+        eng = ShardedEngine(ObservationSet(m, n, i, j, v, split), ex)
+        assert eng.phi_r._dev_csr is not None  # the device path ran
+        keep = split == 0
+        ref = ShardedEngine.__new__(ShardedEngine)
+        ref.ex, ref.K, ref.rank, ref.world = ex, DeviceKernels(), rank, world
+        ref._setup(SparseMatrix.from_coo(m, n, i[keep], j[keep], v[keep]))
+        assert (eng.r0, eng.r1, eng.c0, eng.c1) == (ref.r0, ref.r1, ref.c0, ref.c1)
+        assert np.array_equal(eng.plan.row_bounds, ref.plan.row_bounds)
+        assert np.array_equal(eng.plan.col_bounds, ref.plan.col_bounds)
+        for a, b in ((eng.phi_r, ref.phi_r), (eng.phi_c, ref.phi_c)):
+            assert a.shape == b.shape
+            assert np.array_equal(a.indptr, b.indptr)
+            assert np.array_equal(a.indices, b.indices)
+            assert np.array_equal(a.data, b.data)
+            assert np.array_equal(device.to_host(a.pattern().csr.ptr), b.indptr.astype(np.int32))
+        Xc = X[eng.c0:eng.c1].contiguous()
+        assert torch.equal(eng.K.spmm(eng.phi_r, X, None), ref.K.spmm(ref.phi_r, X, None))
+        assert torch.equal(eng.K.spmm_t(eng.phi_c, H, None), ref.K.spmm_t(ref.phi_c, H, None))
+        assert torch.equal(eng.K.spmm(eng.phi_c, Xc, None), ref.K.spmm(ref.phi_c, Xc, None))
