@@ -283,6 +283,17 @@ int lr_row_norms_f64(const double* Bt, long long ldb, int n, int m, double* out,
 int lr_gaussian_f64(unsigned long long seed, int rows, int cols, double* omega, long long ldo,
                     void* stream);
 
+/* The parity Omega assembled on the device from host-computed halves
+ * (rng.py:38-55's Box-Muller, split as rng.Superset splits it): R[i] =
+ * sqrt(-2 log(1 - u[i])) and cs[2j], cs[2j+1] = cos / sin(2 pi u[p_lo + j])
+ * computed on the host with numpy's own log and libm's cos / sin and uploaded
+ * once for a range of widths; for the width whose pair count is P = ceil(rows
+ * cols / 2), off = P - p_lo and z[2i] = R[i] cs[2 (off + i)], z[2i+1] = R[i]
+ * cs[2 (off + i) + 1] fill Omega (rows x cols, row-major, ldo) column-major:
+ * one IEEE multiply per entry, so bit-identical to the host draw. */
+int lr_omega_assemble_f64(const double* R, const double* cs, long long off, int rows, int cols, double* omega,
+                          long long ldo, void* stream);
+
 /* Host functions (no device work): the C pieces of the parity Omega's host
  * draw (rng.py:38-55 of the reference).  lr_host_uniforms: out[i] = uniform
  * start + i of numpy's Philox(key=seed) stream ((x >> 11) 2^-53).

@@ -77,6 +77,7 @@ SIGNATURES = {
     "lr_jacobi_sweep_f64": (_I, [_I, _I, _P, _LL, _P, _LL, _D, _D, _P, _P]),
     "lr_row_norms_f64": (_I, [_P, _LL, _I, _I, _P, _P]),
     "lr_gaussian_f64": (_I, [_ULL, _I, _I, _P, _LL, _P]),
+    "lr_omega_assemble_f64": (_I, [_P, _P, _LL, _I, _I, _P, _LL, _P]),
     "lr_host_uniforms": (None, [_ULL, _LL, _LL, _P]),
     "lr_host_box_muller": (None, [_P, _P, _LL, _P]),
     "lr_host_cossin": (None, [_P, _LL, _P]),

@@ -75,9 +75,37 @@ __global__ void gaussian_kernel(unsigned long long seed, int rows, int cols, dou
   }
 }
 
+// Omega (rows x cols, row-major) from the host-computed Box-Muller halves of a
+// rng.Superset: z[2i] = R[i] * cs[2 (off + i)], z[2i + 1] = R[i] * cs[2 (off + i) + 1]
+// (one IEEE multiply each, __dmul_rn: the bits of lr_host_bm_assemble), z filling
+// Omega column-major.  A thread per element, column fastest (coalesced stores).
+__global__ void omega_assemble_kernel(const double* __restrict__ R, const double* __restrict__ cs, long long off,
+                                      int rows, int cols, double* __restrict__ omega, long long ldo) {
+  const long long count = (long long)rows * cols;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(e / cols), col = (int)(e - (long long)row * cols);
+    const long long t = (long long)col * rows + row;
+    const long long i = t >> 1;
+    omega[(long long)row * ldo + col] = __dmul_rn(__ldg(R + i), __ldg(cs + 2 * (off + i) + (t & 1)));
+  }
+}
+
 }  // namespace lr
 
 using namespace lr;
+
+extern "C" int lr_omega_assemble_f64(const double* R, const double* cs, long long off, int rows, int cols,
+                                     double* omega, long long ldo, void* stream) {
+  LR_REQUIRE(rows >= 1 && cols >= 1, "omega_assemble needs rows, cols >= 1, got %dx%d", rows, cols);
+  LR_REQUIRE(ldo >= cols && off >= 0 && R && cs, "omega_assemble: bad arguments (ldo=%lld off=%lld)", ldo, off);
+  const long long count = (long long)rows * cols;
+  long long blocks = (count + 255) / 256;
+  if (blocks > sm_count() * 16) blocks = sm_count() * 16;
+  omega_assemble_kernel<<<(int)blocks, 256, 0, as_stream(stream)>>>(R, cs, off, rows, cols, omega, ldo);
+  LR_CHECK_LAUNCH();
+  return LR_OK;
+}
 
 extern "C" int lr_gaussian_f64(unsigned long long seed, int rows, int cols, double* omega, long long ldo,
                                void* stream) {

@@ -231,6 +231,8 @@ def prefetch_normals(seed: int, rows: int, cols: int) -> None:
     key = (int(seed), int(rows), int(cols))
     if key in _PREFETCH or rows < 1 or cols < 1:
         return
+    if superset_pending_on_device(*key):
+        return  # assembled on the GPU from the Superset's uploaded halves
     while len(_PREFETCH) >= PREFETCH_KEEP:
         _PREFETCH.pop(next(iter(_PREFETCH)))
     import threading
@@ -318,14 +320,24 @@ class Superset:
     loop builds one at the top of each iteration for the next iteration's
     plausible ranks, while the GPU runs the current inner SVD."""
 
-    def __init__(self, lib, seed: int, rows: int, w_lo: int, w_hi: int, pool=None):
+    def __init__(self, lib, seed: int, rows: int, w_lo: int, w_hi: int, pool=None, pinned: bool = False):
         self.lib, self.seed, self.rows, self.w_lo, self.w_hi = lib, int(seed), int(rows), int(w_lo), int(w_hi)
         self.p_lo = (rows * w_lo + 1) // 2
         self.p_hi = (rows * w_hi + 1) // 2
         seed64 = self.seed & ((1 << 64) - 1)
-        self.R = np.empty(self.p_hi)
         na = 2 * self.p_hi - self.p_lo
-        self.cs = np.empty(2 * na)
+        self.dev = None  # (R, cs device copies, ready event) once uploaded (upload_async)
+        self.counted = False  # its upload added to device.TRAFFIC
+        if pinned:  # page-locked halves: uploaded once, every width assembled on the GPU
+            import torch
+
+            self._pin = (torch.empty(self.p_hi, dtype=torch.float64, pin_memory=True),
+                         torch.empty(2 * na, dtype=torch.float64, pin_memory=True))
+            self.R, self.cs = self._pin[0].numpy(), self._pin[1].numpy()
+        else:
+            self._pin = None
+            self.R = np.empty(self.p_hi)
+            self.cs = np.empty(2 * na)
         ua = np.empty(na)
         nt = 1 if pool is None else max(1, min(pool._max_workers, self.p_hi // (1 << 15)))
 
@@ -351,6 +363,27 @@ class Superset:
 
     def covers(self, rows: int, cols: int) -> bool:
         return int(rows) == self.rows and self.w_lo <= int(cols) <= self.w_hi
+
+    def upload_async(self, dev_index: int) -> None:
+        """In the drawing thread: copy R and cs to the GPU on the upload
+        stream (overlapping the current inner SVD); lr_omega_assemble_f64 then
+        forms any covered width's Omega on the device with no host work after
+        the rank is known."""
+        import torch
+
+        torch.cuda.set_device(dev_index)
+        st = _UPLOAD_STREAM.get(dev_index)
+        if st is None:
+            st = _UPLOAD_STREAM.setdefault(dev_index, torch.cuda.Stream(device=dev_index))
+        dv = torch.device("cuda", dev_index)
+        with torch.cuda.stream(st):
+            R = torch.empty(self._pin[0].numel(), dtype=torch.float64, device=dv)
+            cs = torch.empty(self._pin[1].numel(), dtype=torch.float64, device=dv)
+            R.copy_(self._pin[0], non_blocking=True)
+            cs.copy_(self._pin[1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(st)
+        self.dev = (R, cs, ev)
 
     def normals(self, cols: int, out: np.ndarray, pool=None) -> np.ndarray:
         """Column-major Omega(seed, rows, cols) into out (>= 2 P entries)."""
@@ -392,15 +425,48 @@ def prefetch_superset(seed: int, rows: int, w_lo: int, w_hi: int) -> None:
     from concurrent.futures import Future
 
     fut = Future()
+    dev_index = _current_device_index() if SUPERSET_ON_DEVICE else None
 
     def run():
         try:
-            fut.set_result(Superset(lib, seed, rows, w_lo, w_hi, _pool()))
+            sup = Superset(lib, seed, rows, w_lo, w_hi, _pool(), pinned=dev_index is not None)
+            if dev_index is not None:
+                sup.upload_async(dev_index)
+            fut.set_result(sup)
         except BaseException as exc:  # pragma: no cover - surfaced on use
             fut.set_exception(exc)
 
     threading.Thread(target=run, daemon=True, name="lr-omega-superset").start()
     _SUPERSETS[key] = ((int(rows), int(w_lo), int(w_hi)), fut)
+
+
+# Opt-in (LR_SUPERSET_DEVICE=1): a Superset's halves are uploaded as soon as
+# they are drawn and Omega is assembled on the GPU (lr_omega_assemble_f64,
+# bit-identical), so no host assembly or upload follows the rank read.  On
+# the cfg4 job 95 % of the draws then come from the device assembly, but the
+# job is not faster (667 vs 651 ms, profiles/r02aj_omega_variants.txt): the
+# host's launch path, not the draw, bounds the idle time.  Default: the width
+# is assembled on the host and uploaded by the prefetch thread.
+SUPERSET_ON_DEVICE = __import__("os").environ.get("LR_SUPERSET_DEVICE", "0") == "1"
+
+
+def superset_pending_on_device(seed: int, rows: int, cols: int) -> bool:
+    """A Superset covering (seed, rows, cols) is drawn or being drawn with a
+    device copy: the exact-width host draw is not needed."""
+    ent = _SUPERSETS.get(int(seed))
+    if ent is None or not SUPERSET_ON_DEVICE or _current_device_index() is None:
+        return False
+    (r, lo, hi), _ = ent
+    return r == int(rows) and lo <= int(cols) <= hi
+
+
+def superset_on_device(seed: int, rows: int, cols: int):
+    """The Superset covering (seed, rows, cols) once its device copy exists
+    (waits for the drawing thread), else None."""
+    if not superset_pending_on_device(seed, rows, cols):
+        return None
+    sup = _superset_for(seed, rows, cols)
+    return sup if (sup is not None and sup.dev is not None) else None
 
 
 def _superset_for(seed: int, rows: int, cols: int):

@@ -164,6 +164,9 @@ def _overlap_draw_with_upload(A: SparseMatrix, seed: int, n: int, w: int, source
     A.device_values()
 
 
+OMEGA_STATS = {"assembled_on_device": 0, "prefetched_upload": 0, "host_draw": 0}
+
+
 def omega_from_host(seed: int, n: int, w: int):
     """Omega = gaussian_matrix(RngState(seed), n, w) drawn on the HOST with
     numpy's own arithmetic (bit-identical to the reference's draw; threaded,
@@ -172,11 +175,30 @@ def omega_from_host(seed: int, n: int, w: int):
     GPU (lr_transpose_f64) -- the host never does the strided transpose."""
     import torch
 
-    from .rng import take_normals, take_normals_device
+    from .rng import superset_on_device, take_normals, take_normals_device
 
     device.require_cuda()
     count = n * w
     pre = take_normals_device(seed, n, w)
+    sup = superset_on_device(seed, n, w) if (pre is None and count) else None
+    OMEGA_STATS["assembled_on_device" if sup is not None else ("prefetched_upload" if pre is not None
+                                                                else "host_draw")] += 1
+    if sup is not None:
+        # the Box-Muller halves of a range of widths are on the GPU already:
+        # this width's Omega is one multiply per entry there (bit-identical
+        # to the host draw), written row-major directly
+        R, cs, ready = sup.dev
+        cur = torch.cuda.current_stream()
+        cur.wait_event(ready)
+        R.record_stream(cur)
+        cs.record_stream(cur)
+        if not sup.counted:
+            sup.counted = True
+            device.TRAFFIC["h2d"] += 8 * (int(R.numel()) + int(cs.numel()))
+        Om = device.empty(n, w)
+        _native.call("lr_omega_assemble_f64", device.ptr(R), device.ptr(cs), (count + 1) // 2 - sup.p_lo, n, w,
+                     device.ptr(Om), device.ld(Om), device.stream())
+        return Om
     if pre is not None:  # the prefetch thread already copied it (upload stream)
         dv, ready = pre
         cur = torch.cuda.current_stream()

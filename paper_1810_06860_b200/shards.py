@@ -567,6 +567,13 @@ class ShardedEngine:
         self.Y_c = self.Y_r if self._one_block else K.scaled_block(self.phi_c, scale)
 
     def step(self, U_s, S_s, V_s, r: int, step: float):
+        return self.step_launch(U_s, S_s, V_s, r, step)(), None
+
+    def step_launch(self, U_s, S_s, V_s, r: int, step: float):
+        """The fused step of both blocks queued on the stream; returns a
+        callable that gathers the ranks' partial sums and returns the
+        residual (DeviceEngine.step_launch: the SVT loop queues the next inner
+        SVD's first product behind the step before it waits for the residual)."""
         K = self.K
         S_dev = K.vector(S_s) if r else K.vector(np.zeros(0))
         if r:
@@ -581,14 +588,40 @@ class ShardedEngine:
         part = K.svt_step(self.Y_r, self.m_r, U_s, S_dev, V_full, r, step)
         if self.Y_c is not self.Y_r:
             K.svt_step(self.Y_c, self.m_c, U_full, S_dev, V_s, r, step)
-        st = self.ex.gather_scalars(part)
-        sumsq, big = float(np.sum(st[:, 0])), float(np.max(st[:, 1]))
-        if big == 0.0:
-            return 0.0, None
-        if np.isfinite(sumsq) and 1e-150 < big < 1e150:
-            return float(np.sqrt(sumsq)) / self.m_norm, None
-        x = K.project(self.Y_r, U_s, S_dev, V_full, r)
-        return self._global_norm(x - self.m_r) / self.m_norm, None
+
+        def finish():
+            st = self.ex.gather_scalars(part)
+            sumsq, big = float(np.sum(st[:, 0])), float(np.max(st[:, 1]))
+            if big == 0.0:
+                return 0.0
+            if np.isfinite(sumsq) and 1e-150 < big < 1e150:
+                return float(np.sqrt(sumsq)) / self.m_norm
+            # partial sums out of range: the scaled norm of x - m, x recomputed from the factors
+            x = K.project(self.Y_r, U_s, S_dev, V_full, r)
+            return self._global_norm(x - self.m_r) / self.m_norm
+
+        return finish
+
+    def prestart(self, plan):
+        """Queue the first product of the next iteration's fresh BKI call
+        behind the fused step (DeviceEngine.prestart): Omega, H_0 = Y Omega
+        (local rows, allgather) and its LU with the status left on the device.
+        None for a recycle or on a kernel set without the asynchronous LU."""
+        from . import rsvd as _rsvd
+
+        K = self.K
+        if plan[0] != "bki" or not (_rsvd.SPECULATIVE and hasattr(K, "lu_pl_async")):
+            return None
+        _, k, s, seed, p_max = plan
+        w = k + s
+        Om = K.gaussian(seed, self.n, w)
+        H = K.empty(self.m, w * (p_max + 1))
+        status = K.vector(np.zeros(4 * (p_max + 1)))
+        H_loc = K.empty(self.r1 - self.r0, w)
+        K.spmm(self.Y_r, Om, out=H_loc)
+        self.gather_m(H_loc, out=H[:, 0:w])
+        K.lu_pl_async(H[:, 0:w], status[0:3])
+        return _rsvd.Prestart("bki", k=k, s=s, seed=seed, p_max=p_max, H=H, lu_status=status)
 
     def factors_host(self, U_s, V_s, r: int):
         if not r:
@@ -689,7 +722,7 @@ class ShardedEngine:
         S_sel = np.asarray(S_sel, dtype=np.float64)
         return DevSvd(U_loc, K.vector(S_sel), Usel, S_sel)
 
-    def bki(self, rp: RsvdParams, allow_fallback: bool = True, _speculate: bool = True):
+    def bki(self, rp: RsvdParams, allow_fallback: bool = True, _speculate: bool = True, pre=None):
         """Sharded Alg. 5 -> (DevSvd with local factor rows, Q replicated, fallbacks).
         Like the single-GPU route, the Krylov blocks' LU statuses stay on the
         device and are read once after the loop; an unusual one replays the
@@ -704,7 +737,10 @@ class ShardedEngine:
         w = rp.k + rp.s
         W = w * (rp.p + 1)
         mg, ng = self.r1 - self.r0, self.c1 - self.c0
-        status = K.vector(np.zeros(4 * (rp.p + 1))) if spec else None
+        use_pre = pre is not None and spec and pre.kind == "bki" and pre.matches(rp)
+        status = None
+        if spec:
+            status = pre.lu_status[:4 * (rp.p + 1)] if use_pre else K.vector(np.zeros(4 * (rp.p + 1)))
 
         def normalise(i):
             if spec:
@@ -712,12 +748,15 @@ class ShardedEngine:
             else:
                 self._lu_block(H[:, i * w:(i + 1) * w], fb)
 
-        Om = K.gaussian(rp.seed, self.n, w)
-        H = K.empty(self.m, W)
         H_loc = K.empty(mg, w)
-        K.spmm(self.Y_r, Om, out=H_loc)
-        self.gather_m(H_loc, out=H[:, 0:w])
-        normalise(0)
+        if use_pre:  # H_0 and its LU were queued behind the last fused step (prestart)
+            H = pre.H[:, :W]
+        else:
+            Om = K.gaussian(rp.seed, self.n, w)
+            H = K.empty(self.m, W)
+            K.spmm(self.Y_r, Om, out=H_loc)
+            self.gather_m(H_loc, out=H[:, 0:w])
+            normalise(0)
         T_loc = K.empty(ng, w)
         T_all = K.empty(self.n, W)  # Y^T H, block by block (replicated after each allgather)
         for i in range(1, rp.p + 1):

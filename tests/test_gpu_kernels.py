@@ -726,3 +726,34 @@ def test_gram_tf32x3_tensor_core(K, n):
     assert err < 1e-5, err
     assert np.array_equal(G, G.T)
     assert np.array_equal(G, G2)
+
+
+@pytest.mark.parametrize("n,w_lo,w_hi", [(2677, 7, 15), (26744, 20, 28), (1000, 6, 6), (333, 1, 9)])
+def test_omega_assembled_on_device_from_superset_is_bit_exact(n, w_lo, w_hi, monkeypatch):
+    """The parity Omega through the device assembly (rng.Superset's Box-Muller
+    halves uploaded once, lr_omega_assemble_f64 forming each width: one IEEE
+    multiply per entry) against the reference draw (numpy, rng.py:38-55),
+    bit for bit for every width in the range; a width outside the range takes
+    the host draw."""
+    from paper_1810_06860_b200 import _native, device, rng, rsvd
+
+    seed = 1234567 + n
+    rng._SUPERSETS.clear()
+    rng._PREFETCH.clear()
+    monkeypatch.setattr(rng, "SUPERSET_ON_DEVICE", True)  # opt-in (LR_SUPERSET_DEVICE=1)
+    rng.prefetch_superset(seed, n, w_lo, w_hi)
+    calls = []
+    real = _native.call
+    monkeypatch.setattr(_native, "call", lambda name, *a, **k: (calls.append(name), real(name, *a, **k))[1])
+    for w in sorted({w_lo, (w_lo + w_hi) // 2, w_hi}):
+        rng.prefetch_normals(seed, n, w)  # what the SVT loop calls once the rank is known: nothing to draw
+        assert (seed, n, w) not in rng._PREFETCH
+        del calls[:]
+        Om = rsvd.omega_from_host(seed, n, w)
+        assert calls == ["lr_omega_assemble_f64"]
+        ref = rng.gaussian_matrix(rng.RngState(seed), n, w)
+        assert np.array_equal(device.to_host(Om), ref)
+    del calls[:]
+    Om = rsvd.omega_from_host(seed, n, w_hi + 1)
+    assert "lr_omega_assemble_f64" not in calls
+    assert np.array_equal(device.to_host(Om), rng.gaussian_matrix(rng.RngState(seed), n, w_hi + 1))

@@ -126,6 +126,7 @@ print(f"take_normals: {len(_TN)} calls, {sum(1 for t in _TN if t[1])} prefetched
       f"{1e3 * sum(t[0] for t in _TN):.1f} ms total, {1e3 * sum(t[0] for t in _TN if not t[1]):.1f} ms on misses")
 from paper_1810_06860_b200 import rsvd as _rsvd  # noqa: E402
 
+print(f"Omega sources over all jobs of this process: {_rsvd.OMEGA_STATS}")
 _k = np.array(_rsvd.REUSE_STATS["kappas"])
 print(f"Krylov reuse: used {_rsvd.REUSE_STATS['used']}, kappa-gated {_rsvd.REUSE_STATS['kappa_gate']}; kappa_F(H) "
       f"quantiles 10/50/90/max: {np.quantile(_k, [0.1, 0.5, 0.9, 1.0]) if _k.size else None}")
