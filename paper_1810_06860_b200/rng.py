@@ -309,6 +309,43 @@ def take_normals_device(seed: int, rows: int, cols: int):
     return d.dev, d.ready
 
 
+class _StagingSlot:
+    """Page-locked host buffers a device-backed Superset is drawn into and
+    uploaded from.  A few slots are allocated once and handed out in turn
+    (cudaHostAlloc inside the drawing thread stalls the main thread's kernel
+    launches); `gen` tells a Superset whether the slot is still its own."""
+
+    def __init__(self):
+        self.R = self.cs = None
+        self.gen = 0
+        self.uploaded = None  # event of the last upload read from this slot
+
+
+_STAGING = []
+_STAGING_NEXT = [0]
+_STAGING_SLOTS = 4  # two Supersets are kept; a slot is reused two draws after its Superset was dropped
+
+
+def _staging_slot(n_r: int, n_cs: int) -> _StagingSlot:
+    import torch
+
+    if len(_STAGING) < _STAGING_SLOTS:
+        _STAGING.append(_StagingSlot())
+        slot = _STAGING[-1]
+    else:
+        slot = _STAGING[_STAGING_NEXT[0] % _STAGING_SLOTS]
+    _STAGING_NEXT[0] += 1
+    if slot.uploaded is not None:
+        slot.uploaded.synchronize()  # its last upload has left the buffer
+        slot.uploaded = None
+    slot.gen += 1
+    if slot.R is None or slot.R.numel() < n_r:
+        slot.R = torch.empty(int(n_r * 1.5) + 1024, dtype=torch.float64, pin_memory=True)
+    if slot.cs is None or slot.cs.numel() < n_cs:
+        slot.cs = torch.empty(int(n_cs * 1.5) + 1024, dtype=torch.float64, pin_memory=True)
+    return slot
+
+
 class Superset:
     """One seed's draws for every width in [w_lo, w_hi] at ~the cost of one:
     Box-Muller pairs uniform i with uniform P + i (P = ceil(rows w / 2)), so
@@ -320,7 +357,7 @@ class Superset:
     loop builds one at the top of each iteration for the next iteration's
     plausible ranks, while the GPU runs the current inner SVD."""
 
-    def __init__(self, lib, seed: int, rows: int, w_lo: int, w_hi: int, pool=None, pinned: bool = False):
+    def __init__(self, lib, seed: int, rows: int, w_lo: int, w_hi: int, pool=None, slot: "_StagingSlot" = None):
         self.lib, self.seed, self.rows, self.w_lo, self.w_hi = lib, int(seed), int(rows), int(w_lo), int(w_hi)
         self.p_lo = (rows * w_lo + 1) // 2
         self.p_hi = (rows * w_hi + 1) // 2
@@ -328,14 +365,12 @@ class Superset:
         na = 2 * self.p_hi - self.p_lo
         self.dev = None  # (R, cs device copies, ready event) once uploaded (upload_async)
         self.counted = False  # its upload added to device.TRAFFIC
-        if pinned:  # page-locked halves: uploaded once, every width assembled on the GPU
-            import torch
-
-            self._pin = (torch.empty(self.p_hi, dtype=torch.float64, pin_memory=True),
-                         torch.empty(2 * na, dtype=torch.float64, pin_memory=True))
-            self.R, self.cs = self._pin[0].numpy(), self._pin[1].numpy()
+        if slot is not None:  # page-locked halves: uploaded once, every width assembled on the GPU
+            self._slot = slot
+            self._gen = slot.gen
+            self.R, self.cs = self._slot.R.numpy()[:self.p_hi], self._slot.cs.numpy()[:2 * na]
         else:
-            self._pin = None
+            self._slot = None
             self.R = np.empty(self.p_hi)
             self.cs = np.empty(2 * na)
         ua = np.empty(na)
@@ -376,14 +411,21 @@ class Superset:
         if st is None:
             st = _UPLOAD_STREAM.setdefault(dev_index, torch.cuda.Stream(device=dev_index))
         dv = torch.device("cuda", dev_index)
+        nR, ncs = int(self.R.shape[0]), int(self.cs.shape[0])
         with torch.cuda.stream(st):
-            R = torch.empty(self._pin[0].numel(), dtype=torch.float64, device=dv)
-            cs = torch.empty(self._pin[1].numel(), dtype=torch.float64, device=dv)
-            R.copy_(self._pin[0], non_blocking=True)
-            cs.copy_(self._pin[1], non_blocking=True)
+            R = torch.empty(nR, dtype=torch.float64, device=dv)
+            cs = torch.empty(ncs, dtype=torch.float64, device=dv)
+            R.copy_(self._slot.R[:nR], non_blocking=True)
+            cs.copy_(self._slot.cs[:ncs], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(st)
+        self._slot.uploaded = ev
         self.dev = (R, cs, ev)
+
+    def host_valid(self) -> bool:
+        """The host halves are still this Superset's (a staged Superset's
+        page-locked slot is handed to a later one after two more draws)."""
+        return self._slot is None or self._slot.gen == self._gen
 
     def normals(self, cols: int, out: np.ndarray, pool=None) -> np.ndarray:
         """Column-major Omega(seed, rows, cols) into out (>= 2 P entries)."""
@@ -426,10 +468,14 @@ def prefetch_superset(seed: int, rows: int, w_lo: int, w_hi: int) -> None:
 
     fut = Future()
     dev_index = _current_device_index() if SUPERSET_ON_DEVICE else None
+    slot = None
+    if dev_index is not None:  # chosen here, in the caller's thread: a fixed rotation
+        p_hi = (int(rows) * int(w_hi) + 1) // 2
+        slot = _staging_slot(p_hi, 2 * (2 * p_hi - (int(rows) * int(w_lo) + 1) // 2))
 
     def run():
         try:
-            sup = Superset(lib, seed, rows, w_lo, w_hi, _pool(), pinned=dev_index is not None)
+            sup = Superset(lib, seed, rows, w_lo, w_hi, _pool(), slot=slot)
             if dev_index is not None:
                 sup.upload_async(dev_index)
             fut.set_result(sup)
@@ -477,9 +523,10 @@ def _superset_for(seed: int, rows: int, cols: int):
     if r != int(rows) or not lo <= int(cols) <= hi:
         return None
     try:
-        return fut.result()
+        sup = fut.result()
     except Exception:
         return None
+    return sup if sup.host_valid() else None
 
 
 def _pinned_from_superset(sup: Superset, cols: int):

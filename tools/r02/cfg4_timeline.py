@@ -134,3 +134,18 @@ print("trace (i, source, k, r, p):", [(t.iteration, t.svd_source[0], t.k, t.r, t
 print("largest 15 gaps (ms, next call, gpu t, host t):")
 for g in sorted(gaps, reverse=True)[:15]:
     print(f"  {g[0]:7.3f} {g[1]:28s} gpu {g[2]:9.2f} host {g[3]:9.2f}")
+
+# LR_TL_DUMP=a:b -- every native call whose host start lies in [a, b) ms: host start / end, GPU start /
+# end, and the GPU gap before it (where does the host spend the time the GPU idles?)
+if os.environ.get("LR_TL_DUMP"):
+    a, b = (float(x) for x in os.environ["LR_TL_DUMP"].split(":"))
+    prev_end = 0.0
+    prev_h1 = 0.0
+    for name, meta, e0, e1, h0, h1 in tl.records:
+        g0, g1 = base.elapsed_time(e0), base.elapsed_time(e1)
+        hs, he = 1e3 * (h0 - h_base), 1e3 * (h1 - h_base)
+        if a <= hs < b:
+            print(f"{name:26s} host {hs:8.3f}..{he:8.3f} (since prev call {hs - prev_h1:6.3f})  gpu {g0:8.3f}..{g1:8.3f} "
+                  f"gap {max(0.0, g0 - prev_end):6.3f}  lead {g0 - hs:7.3f}")
+        prev_end = max(prev_end, g1)
+        prev_h1 = he
