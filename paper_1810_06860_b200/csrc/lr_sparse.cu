@@ -1257,10 +1257,13 @@ static bool spmm_group(const int* ptr, const int* idx, const Sc* val, const int*
   static const char* fam = getenv("LR_SPMM_KERNEL");
   if (fam && fam[0] == 'i') return false;  // "items": the round-1 kernel
   constexpr int VE = 16 / (int)sizeof(Sc);
-  if (!aligned_bytes(X, 16) || (ldx * (long long)sizeof(Sc)) % 16 != 0) return false;
-  // rows share one offset from their 128-byte line only if the row stride is whole lines
-  const int shift = ((ldx * (long long)sizeof(Sc)) % 128 == 0)
-                        ? (int)((reinterpret_cast<uintptr_t>(X) & 127u) / sizeof(Sc)) : 0;
+  // rows share one offset from their 128-byte line only if the row stride is whole lines; then
+  // the chunks are read from the line start and X itself may sit at any element (a column slice
+  // of a Krylov block at an odd column offset); otherwise column 0 must start a 16-byte chunk
+  const bool lines = (ldx * (long long)sizeof(Sc)) % 128 == 0;
+  if (!aligned_bytes(X, (unsigned)sizeof(Sc)) || (ldx * (long long)sizeof(Sc)) % 16 != 0) return false;
+  if (!lines && !aligned_bytes(X, 16)) return false;
+  const int shift = lines ? (int)((reinterpret_cast<uintptr_t>(X) & 127u) / sizeof(Sc)) : 0;
   int G, T;
   const int nchunk = (w + shift + VE - 1) / VE;
   if (!pick_group(nchunk, G, T)) return false;

@@ -97,6 +97,35 @@ def test_spmm_hot_rows_bit_identical(w, monkeypatch):
     assert torch.equal(y0, y1) and torch.equal(t0, t1)
 
 
+@pytest.mark.parametrize("w,off", [(5, 1), (11, 3), (22, 7), (45, 45), (45, 90), (89, 1), (131, 5)])
+def test_spmm_column_slice_at_odd_offset_is_bit_identical(w, off):
+    """Y X and Y^T X with X a column slice of a wider block starting at an
+    odd column (the Krylov blocks H_i of rsvd_bki for odd k + s): the
+    line-aligned group kernel reads the chunks from the row's 128-byte line,
+    so the slice need not start a 16-byte chunk; same bits as the product with
+    a contiguous copy of the slice."""
+    import torch
+
+    from paper_1810_06860_b200 import device
+    from paper_1810_06860_b200.sparse import SparseMatrix, spmm_dev, spmm_t_dev
+
+    m, n = 1500, 900
+    i, j, v = rand_pattern(m, n, 40000, seed=w + off, long_rows=1, long_cols=1)
+    A = SparseMatrix.from_coo(m, n, i, j, v)
+    rng = np.random.default_rng(off)
+    Xw = device.to_device(rng.standard_normal((n, off + w + 3)))
+    Hw = device.to_device(rng.standard_normal((m, off + w + 3)))
+    Xs, Hs = Xw[:, off:off + w], Hw[:, off:off + w]
+    Xc, Hc = device.empty(n, w), device.empty(m, w)
+    Xc.copy_(Xs)
+    Hc.copy_(Hs)
+    assert torch.equal(spmm_dev(A, Xs), spmm_dev(A, Xc))
+    assert torch.equal(spmm_t_dev(A, Hs), spmm_t_dev(A, Hc))
+    out = device.empty(m, off + w + 3)  # and into a column slice of a wider block
+    spmm_dev(A, Xs, out=out[:, off:off + w])
+    assert torch.equal(out[:, off:off + w], spmm_dev(A, Xc))
+
+
 def test_spmm_golden(golden):
     from paper_1810_06860_b200.sparse import SparseMatrix, spmm, spmm_t
 

@@ -16,10 +16,4 @@ timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --l
   python bench.py --steps 1 --warmup 1 --cpu-baseline skip --extras off --e2e-steps 0 > gpurun_out/${tag}_launches.log 2>&1; echo "launch list rc=$?"
 python tools/launch_summary.py gpurun_out/${tag}_launches.csv > gpurun_out/${tag}_launches_summary.txt 2>&1; head -12 gpurun_out/${tag}_launches_summary.txt
 gzip -f gpurun_out/${tag}_launches.csv
-# full captures
-timeout 600 python tools/spmm_cfg4_probe.py 22,45 > gpurun_out/${tag}_spmm_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm_group -s 4 -c 1 -o gpurun_out/${tag}_spmm22 python tools/spmm_cfg4_probe.py 22 > gpurun_out/${tag}_ncu1.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm_group -s 4 -c 1 -o gpurun_out/${tag}_spmm45 python tools/spmm_cfg4_probe.py 45 > gpurun_out/${tag}_ncu1b.log 2>&1
-NCU=1 RANKS=10,48,84 timeout 600 python tools/r02/svt_step_probe.py > gpurun_out/${tag}_svt_plain.log 2>&1 && \
-NCU=1 RANKS=10,48,84 timeout 900 ncu --set full --clock-control none --import-source on -k regex:svt_group2 -c 6 -o gpurun_out/${tag}_svt python tools/r02/svt_step_probe.py > gpurun_out/${tag}_ncu2.log 2>&1
 ls -la gpurun_out | grep ${tag}
