@@ -169,8 +169,19 @@ __global__ void spmm_split_reduce_kernel(const int* __restrict__ splits, int n_s
        t += (long long)gridDim.x * blockDim.x) {
     const int s = (int)(t / w), c = (int)(t - (long long)s * w);
     const int4 sp = reinterpret_cast<const int4*>(splits)[s];
+    // the partial rows are added in slot order (a fixed, sequential sum); the loads do not
+    // depend on the sum, so 16 of them are in flight at a time (a Zipf-hot column of cfg4 has
+    // ~200 slots: one L2 round trip per slot otherwise)
     Sc acc = Sc(0);
-    for (int k = sp.y; k < sp.z; ++k) acc += scratch[(long long)k * w + c];
+    int k = sp.y;
+    for (; k + 16 <= sp.z; k += 16) {
+      Sc v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = __ldg(scratch + (long long)(k + u) * w + c);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc += v[u];
+    }
+    for (; k < sp.z; ++k) acc += __ldg(scratch + (long long)k * w + c);
     Y[(long long)sp.x * ldy + c] = acc;
   }
 }
