@@ -317,8 +317,10 @@ class _StagingSlot:
 
     def __init__(self):
         self.R = self.cs = None
+        self.R_dev = self.cs_dev = None  # device copies, grown rarely (no cudaMalloc per draw: it stalls the GPU)
         self.gen = 0
         self.uploaded = None  # event of the last upload read from this slot
+        self.consumed = None  # event after the last kernel that read the device copies
 
 
 _STAGING = []
@@ -412,15 +414,31 @@ class Superset:
             st = _UPLOAD_STREAM.setdefault(dev_index, torch.cuda.Stream(device=dev_index))
         dv = torch.device("cuda", dev_index)
         nR, ncs = int(self.R.shape[0]), int(self.cs.shape[0])
+        slot = self._slot
         with torch.cuda.stream(st):
-            R = torch.empty(nR, dtype=torch.float64, device=dv)
-            cs = torch.empty(ncs, dtype=torch.float64, device=dv)
-            R.copy_(self._slot.R[:nR], non_blocking=True)
-            cs.copy_(self._slot.cs[:ncs], non_blocking=True)
+            if slot.R_dev is None or slot.R_dev.numel() < nR:
+                slot.R_dev = torch.empty(int(nR * 1.5) + 1024, dtype=torch.float64, device=dv)
+            if slot.cs_dev is None or slot.cs_dev.numel() < ncs:
+                slot.cs_dev = torch.empty(int(ncs * 1.5) + 1024, dtype=torch.float64, device=dv)
+            if slot.consumed is not None:  # the slot's previous Superset may still be read by a queued kernel
+                st.wait_event(slot.consumed)
+                slot.consumed = None
+            R, cs = slot.R_dev[:nR], slot.cs_dev[:ncs]
+            R.copy_(slot.R[:nR], non_blocking=True)
+            cs.copy_(slot.cs[:ncs], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(st)
-        self._slot.uploaded = ev
+        slot.uploaded = ev
         self.dev = (R, cs, ev)
+
+    def mark_consumed(self, stream) -> None:
+        """A kernel reading the device copies was just queued on `stream`."""
+        import torch
+
+        if self._slot is not None and self._slot.gen == self._gen:
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            self._slot.consumed = ev
 
     def host_valid(self) -> bool:
         """The host halves are still this Superset's (a staged Superset's

@@ -190,14 +190,13 @@ def omega_from_host(seed: int, n: int, w: int):
         R, cs, ready = sup.dev
         cur = torch.cuda.current_stream()
         cur.wait_event(ready)
-        R.record_stream(cur)
-        cs.record_stream(cur)
         if not sup.counted:
             sup.counted = True
             device.TRAFFIC["h2d"] += 8 * (int(R.numel()) + int(cs.numel()))
         Om = device.empty(n, w)
         _native.call("lr_omega_assemble_f64", device.ptr(R), device.ptr(cs), (count + 1) // 2 - sup.p_lo, n, w,
                      device.ptr(Om), device.ld(Om), device.stream())
+        sup.mark_consumed(cur)  # the staging slot's device copies are rewritten only after this kernel
         return Om
     if pre is not None:  # the prefetch thread already copied it (upload stream)
         dv, ready = pre
