@@ -26,6 +26,21 @@ __global__ void k2(int iters, volatile unsigned* arrive, volatile unsigned* rele
     __syncthreads();
   }
 }
+// single-counter barrier: every CTA's thread 0 adds (release) and polls the same word (acquire)
+__global__ void k3(int iters, unsigned* ctr) {
+  for (int i = 1; i <= iters; ++i) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned v;
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+      const unsigned target = gridDim.x * (unsigned)i;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      } while (v < target);
+    }
+    __syncthreads();
+  }
+}
 int main() {
   int* out; cudaMalloc(&out, 4);
   unsigned* flags; cudaMalloc(&flags, 64); 
@@ -48,7 +63,14 @@ int main() {
       cudaLaunchCooperativeKernel((void*)k2, G, threads, args3, 0, 0);
       cudaEventRecord(b); cudaEventSynchronize(b);
       float ms2; cudaEventElapsedTime(&ms2, a, b);
-      printf("G=%d threads=%d: cg grid.sync %.3f us, flag barrier %.3f us  (%s)\n", G, threads, ms * 1000 / iters, ms2 * 1000 / iters, cudaGetErrorString(cudaGetLastError()));
+      cudaMemset(flags, 0, 64);
+      unsigned* ctr = flags + 4;
+      void* args4[] = {&iters, (void*)&ctr};
+      cudaEventRecord(a);
+      cudaLaunchCooperativeKernel((void*)k3, G, threads, args4, 0, 0);
+      cudaEventRecord(b); cudaEventSynchronize(b);
+      float ms3; cudaEventElapsedTime(&ms3, a, b);
+      printf("G=%d threads=%d: cg grid.sync %.3f us, flag barrier %.3f us, single counter (red.release + ld.acquire) %.3f us  (%s)\n", G, threads, ms * 1000 / iters, ms2 * 1000 / iters, ms3 * 1000 / iters, cudaGetErrorString(cudaGetLastError()));
       (void)args2;
     }
   }
