@@ -509,6 +509,7 @@ def eig_svd_dev(A, cols=None, check=True, defer=False, G=None):
             _check_dev(A, "eig_svd input")
         return gram_spectrum(dh)
 
+    finish.reads = [d]  # what finish() will read (device.prefetch_host batches it with the caller's reads)
     if defer:  # the caller queues more work first; finish() reads d and checks the rank
         return finish, V, U, cols
     return finish(), V, U, cols
@@ -547,6 +548,7 @@ def eig_svd_congruent_dev(T, Rinv, cols, defer=False, Gt=None):
             _check_dev(T, "eig_svd input")
         return gram_spectrum(dh)
 
+    finish.reads = [d]
     if defer:
         return finish, V, U, cols
     return finish(), V, U, cols

@@ -271,6 +271,7 @@ def _windowed_small_svd(Bt, idx, fb: _Fallback, Rinv=None, defer=False, G=None):
         except RankDeficiencyError as exc:
             return _windowed_fallback(Bt, idx, fb, Rinv, exc)
 
+    finish.reads = getattr(fin, "reads", [])
     return (finish, Vsel, U) if defer else finish()
 
 
@@ -342,6 +343,7 @@ def project_and_solve(Y: SparseMatrix, Q, k: int, fb: _Fallback, precision: str 
         U2, pend2 = (U, pend) if Vs is Vsel else lift(Vs, Us)  # the fallback replaced the small factors
         return DevSvd(U2, device.f64_buffer(S_sel), Us, np.asarray(S_sel, dtype=np.float64), pend2)
 
+    finish.reads = getattr(fin, "reads", [])
     return finish if defer else finish()
 
 
@@ -494,33 +496,39 @@ def rsvd_bki_dev(A: SparseMatrix, params: RsvdParams, allow_fallback: bool = Fal
         fin_spec = project_and_solve(A, Q, params.k, fb, "fp64", download=download,
                                      T_pre=matmul_dev(Q.T_all, Q.R1inv, b_upper=True), defer=True)
     if spec:
-        st = device.to_host(lu_status).reshape(-1, 4)[:, :3]
-        diag_h, infos_h = device.to_host(probe[0]), device.to_host(probe[1])
-        if not np.all(st[:, 0] == -1.0):  # an LU decision differed: redo the whole call
-            return rsvd_bki_dev(A, params, allow_fallback, omega, precision, download, _speculate=False)
-        if not orth_speculation_holds(diag_h, infos_h):
-            # the Krylov blocks are exactly the careful path's (H is untouched
-            # by the speculative orth): only the orthonormalisation is redone
-            Q = _orthonormalize(H, fb, lazy_last=lazy)
-        elif reuse_ok and isinstance(Q, LazyQ):
-            Wn = diag_h.shape[0] // 3
-            kappa = float(np.sqrt(np.sum(diag_h[0:Wn]) * device.to_host(probe[2])[0]))
-            if len(REUSE_STATS["kappas"]) < 4096:
-                REUSE_STATS["kappas"].append(kappa)
-            passes = bool(np.isfinite(kappa) and kappa <= KRYLOV_REUSE_KAPPA)
-            if len(_REUSE_GATED) > 4096:
-                _REUSE_GATED.clear()
-            _REUSE_GATED[gate_key] = not passes
-            if fin_spec is not None and passes:
-                REUSE_STATS["used"] += 1
-                res = fin_spec()  # the speculatively queued projection stands
-                if isinstance(Q, LazyQ):
-                    Q.T_all = Q.R1inv = None  # the cached basis (reuse-q) must not pin them
-                return res, Q, fb.count
-            if fin_spec is not None:
-                REUSE_STATS["kappa_gate"] += 1  # queued and dropped
-        if isinstance(Q, LazyQ):
-            Q.T_all = Q.R1inv = None
+        # one batched device -> host transfer for everything this call reads (LU statuses, orth's
+        # decisions, ||R1^{-1}||, the small eigenvalues): one wait, then plain host arrays
+        device.prefetch_host([lu_status, probe[0], probe[1], probe[2]] + list(getattr(fin_spec, "reads", [])))
+        try:
+            st = device.to_host(lu_status).reshape(-1, 4)[:, :3]
+            diag_h, infos_h = device.to_host(probe[0]), device.to_host(probe[1])
+            if not np.all(st[:, 0] == -1.0):  # an LU decision differed: redo the whole call
+                return rsvd_bki_dev(A, params, allow_fallback, omega, precision, download, _speculate=False)
+            if not orth_speculation_holds(diag_h, infos_h):
+                # the Krylov blocks are exactly the careful path's (H is untouched
+                # by the speculative orth): only the orthonormalisation is redone
+                Q = _orthonormalize(H, fb, lazy_last=lazy)
+            elif reuse_ok and isinstance(Q, LazyQ):
+                Wn = diag_h.shape[0] // 3
+                kappa = float(np.sqrt(np.sum(diag_h[0:Wn]) * device.to_host(probe[2])[0]))
+                if len(REUSE_STATS["kappas"]) < 4096:
+                    REUSE_STATS["kappas"].append(kappa)
+                passes = bool(np.isfinite(kappa) and kappa <= KRYLOV_REUSE_KAPPA)
+                if len(_REUSE_GATED) > 4096:
+                    _REUSE_GATED.clear()
+                _REUSE_GATED[gate_key] = not passes
+                if fin_spec is not None and passes:
+                    REUSE_STATS["used"] += 1
+                    res = fin_spec()  # the speculatively queued projection stands
+                    if isinstance(Q, LazyQ):
+                        Q.T_all = Q.R1inv = None  # the cached basis (reuse-q) must not pin them
+                    return res, Q, fb.count
+                if fin_spec is not None:
+                    REUSE_STATS["kappa_gate"] += 1  # queued and dropped
+            if isinstance(Q, LazyQ):
+                Q.T_all = Q.R1inv = None
+        finally:
+            device.clear_prefetched()  # nothing prefetched outlives the tensors it mirrors
     res = project_and_solve(A, Q, params.k, fb, "fp32" if fp32 else "fp64", download=download, T_pre=T_pre)
     return res, Q, fb.count
 
