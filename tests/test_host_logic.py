@@ -260,3 +260,37 @@ def test_cfg5_device_generator_shape_and_pattern():
     assert o.rows.size == 50000 and np.all(np.diff(key) > 0)
     assert o.rows.min() >= 0 and o.rows.max() < 3000 and o.cols.min() >= 0 and o.cols.max() < 700
     assert np.all(np.isfinite(o.values)) and 1.5 < np.std(o.values) < 4.5  # var = rank
+
+
+def test_superset_after_escalation_covers_the_next_calls(monkeypatch):
+    """completion._speculate_after_escalation: after an escalation k_old ->
+    k_new the call after the redo (svd_calls + 2) is iteration i+1's first
+    call at k = r + 1, r in [k_old, k_new - 1], or another escalation at
+    k_new + l: one Superset over widths [k_old + 1 + s, k_new + l + s] with
+    that call's seed; nothing when a width would exceed the BKI width budget
+    or the draws are not on the host."""
+    from paper_1810_06860_b200 import completion, rng
+
+    calls = []
+    monkeypatch.setattr(rng, "prefetch_superset", lambda seed, rows, lo, hi: calls.append((seed, rows, lo, hi)))
+
+    class Eng:
+        m, n, omega_source = 5000, 3000, "host"
+
+    params = completion.SvtParams(seed=7)
+    state = completion.SvtState(Y=None, seed_rng=rng.RngState(7))
+    state.svd_calls = 4
+    completion._speculate_after_escalation(state, params, "none", Eng(), 10, 10 + params.l)
+    s, l = params.s, params.l
+    assert calls == [(rng.RngState(7).spawn(6).seed, 3000, 11 + s, 10 + 2 * l + s)]
+    del calls[:]
+    Eng.omega_source = "device"
+    completion._speculate_after_escalation(state, params, "none", Eng(), 10, 10 + l)
+    assert calls == []
+    Eng.omega_source = "host"
+    # widths past the BKI budget (min_dim // (k + s) - 1 < 1) are left out; none left -> no draw
+    completion._speculate_after_escalation(state, params, "none", Eng(), 1490, 1490 + l)
+    assert calls == [(rng.RngState(7).spawn(6).seed, 3000, 1491 + s, 1500)]
+    del calls[:]
+    completion._speculate_after_escalation(state, params, "none", Eng(), 1600, 1600 + l)
+    assert calls == []
