@@ -67,3 +67,39 @@ def test_cfg4_trace_spectrum_and_predictions(cfg4_job):
         assert res.S.shape == S_ref.shape
         assert float(np.max(np.abs(res.S - S_ref) / S_ref)) <= 1e-8
     assert float(np.max(np.abs(pred[g["pred_index"]] - g["pred"]))) <= 1e-6
+
+
+def test_cfg4_device_csr_and_csc_are_bit_exact_at_full_size():
+    """The observed-index sets at the north-star size (north_star: "sparsity
+    pattern, CSR/CSC construction and the observed-index sets must be
+    bit-exact"): the device COO -> CSR build of the 18,000,237 training cells
+    against the host lexsort (sparse.py:84-104), and the device CSC index,
+    permutation and inverse permutation against the reference's stable
+    argsort (sparse.py:129-139)."""
+    from paper_1810_06860_b200 import device, workloads
+    from paper_1810_06860_b200.sparse import ObservationSet
+
+    o = workloads.cfg4()
+    obs = ObservationSet(o.m, o.n, o.rows, o.cols, o.values, o.split)
+    A = obs.train_matrix()
+    assert A._dev_csr is not None  # built on the device
+    keep = o.split == ObservationSet.TRAIN
+    i, j, v = o.rows[keep], o.cols[keep], o.values[keep]
+    order = np.lexsort((j, i))
+    indptr = np.zeros(o.m + 1, dtype=np.int64)
+    np.cumsum(np.bincount(i, minlength=o.m), out=indptr[1:])
+    assert A.nnz == 18_000_237
+    assert np.array_equal(A.indptr, indptr)
+    assert np.array_equal(A.indices, j[order])
+    assert np.array_equal(A.data, v[order])
+    dp = A.pattern()
+    jj = j[order]
+    tperm = np.argsort(jj, kind="stable")
+    t_indptr = np.zeros(o.n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(jj, minlength=o.n), out=t_indptr[1:])
+    assert np.array_equal(device.to_host(dp.csc.ptr).astype(np.int64), t_indptr)
+    assert np.array_equal(device.to_host(dp.perm).astype(np.int64), tperm)
+    assert np.array_equal(device.to_host(dp.csc.idx).astype(np.int64), i[order][tperm])
+    inv = np.empty_like(tperm)
+    inv[tperm] = np.arange(tperm.shape[0])
+    assert np.array_equal(device.to_host(dp.inv_perm).astype(np.int64), inv)
