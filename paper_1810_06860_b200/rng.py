@@ -88,7 +88,8 @@ def gaussian_matrix(rng: RngState, rows: int, cols: int) -> np.ndarray:
 # the normals, in place, into a caller-provided (pinned) buffer -- the numpy
 # ufuncs and the Philox fill release the GIL.
 
-HOST_THREADS = None  # None: os.cpu_count()
+# draw pool size; None: os.cpu_count() (LR_HOST_THREADS limits it, e.g. to study a slower host)
+HOST_THREADS = int(__import__("os").environ.get("LR_HOST_THREADS") or 0) or None
 _POOL = None
 
 
@@ -309,6 +310,14 @@ def take_normals_device(seed: int, rows: int, cols: int):
     return d.dev, d.ready
 
 
+# Threads a Superset draw is cut into.  It runs beside the SVT loop's main
+# thread, which launches the current inner SVD meanwhile: cut over every core
+# it slows that thread more than it gains (cfg4 job with the device assembly:
+# 627 ms on 16 threads, 612 ms on 6; profiles/r02bb_host_sensitivity.txt).
+# Single draws on the critical path (a standalone rsvd call) use the whole pool.
+SUPERSET_THREADS = int(__import__("os").environ.get("LR_SUPERSET_THREADS") or 6)
+
+
 class _StagingSlot:
     """Page-locked host buffers a device-backed Superset is drawn into and
     uploaded from.  A few slots are allocated once and handed out in turn
@@ -376,7 +385,7 @@ class Superset:
             self.R = np.empty(self.p_hi)
             self.cs = np.empty(2 * na)
         ua = np.empty(na)
-        nt = 1 if pool is None else max(1, min(pool._max_workers, self.p_hi // (1 << 15)))
+        nt = 1 if pool is None else max(1, min(pool._max_workers, SUPERSET_THREADS, self.p_hi // (1 << 15)))
 
         def part(t):
             a, b = (self.p_hi * t) // nt, (self.p_hi * (t + 1)) // nt
@@ -504,14 +513,17 @@ def prefetch_superset(seed: int, rows: int, w_lo: int, w_hi: int) -> None:
     _SUPERSETS[key] = ((int(rows), int(w_lo), int(w_hi)), fut)
 
 
-# Opt-in (LR_SUPERSET_DEVICE=1): a Superset's halves are uploaded as soon as
-# they are drawn and Omega is assembled on the GPU (lr_omega_assemble_f64,
-# bit-identical), so no host assembly or upload follows the rank read.  On
-# the cfg4 job 95 % of the draws then come from the device assembly, but the
-# job is not faster (667 vs 651 ms, profiles/r02aj_omega_variants.txt): the
-# host's launch path, not the draw, bounds the idle time.  Default: the width
-# is assembled on the host and uploaded by the prefetch thread.
-SUPERSET_ON_DEVICE = __import__("os").environ.get("LR_SUPERSET_DEVICE", "0") == "1"
+# A Superset's halves are uploaded as soon as they are drawn and Omega is
+# assembled on the GPU (lr_omega_assemble_f64, bit-identical), so no host
+# draw, assembly or upload follows the rank read: 95 % of the cfg4 job's
+# draws.  With the Superset cut into SUPERSET_THREADS = 6 pieces the job runs
+# in 605 ms against 614 ms for the host assembly (628 ms for either on 16
+# threads), and it does not depend on the host's draw throughput: with the
+# draw pool limited to 3 threads 629 ms against 756 ms
+# (profiles/r02bb_host_sensitivity.txt, r02bc_superset_threads.txt).
+# LR_SUPERSET_DEVICE=0: the width is assembled on the host and uploaded by the
+# prefetch thread.
+SUPERSET_ON_DEVICE = __import__("os").environ.get("LR_SUPERSET_DEVICE", "1") != "0"
 
 
 def superset_pending_on_device(seed: int, rows: int, cols: int) -> bool:
