@@ -328,6 +328,7 @@ class _StagingSlot:
         self.R = self.cs = None
         self.R_dev = self.cs_dev = None  # device copies, grown rarely (no cudaMalloc per draw: it stalls the GPU)
         self.gen = 0
+        self.owner = None     # Future of the Superset being drawn into this slot
         self.uploaded = None  # event of the last upload read from this slot
         self.consumed = None  # event after the last kernel that read the device copies
 
@@ -346,8 +347,14 @@ def _staging_slot(n_r: int, n_cs: int) -> _StagingSlot:
     else:
         slot = _STAGING[_STAGING_NEXT[0] % _STAGING_SLOTS]
     _STAGING_NEXT[0] += 1
+    if slot.owner is not None:  # the slot's previous Superset has been drawn and its upload queued ...
+        try:
+            slot.owner.result()
+        except BaseException:
+            pass
+        slot.owner = None
     if slot.uploaded is not None:
-        slot.uploaded.synchronize()  # its last upload has left the buffer
+        slot.uploaded.synchronize()  # ... and that upload has left the buffer
         slot.uploaded = None
     slot.gen += 1
     if slot.R is None or slot.R.numel() < n_r:
@@ -499,6 +506,7 @@ def prefetch_superset(seed: int, rows: int, w_lo: int, w_hi: int) -> None:
     if dev_index is not None:  # chosen here, in the caller's thread: a fixed rotation
         p_hi = (int(rows) * int(w_hi) + 1) // 2
         slot = _staging_slot(p_hi, 2 * (2 * p_hi - (int(rows) * int(w_lo) + 1) // 2))
+        slot.owner = fut
 
     def run():
         try:
@@ -513,17 +521,19 @@ def prefetch_superset(seed: int, rows: int, w_lo: int, w_hi: int) -> None:
     _SUPERSETS[key] = ((int(rows), int(w_lo), int(w_hi)), fut)
 
 
-# A Superset's halves are uploaded as soon as they are drawn and Omega is
-# assembled on the GPU (lr_omega_assemble_f64, bit-identical), so no host
-# draw, assembly or upload follows the rank read: 95 % of the cfg4 job's
-# draws.  With the Superset cut into SUPERSET_THREADS = 6 pieces the job runs
-# in 605 ms against 614 ms for the host assembly (628 ms for either on 16
-# threads), and it does not depend on the host's draw throughput: with the
-# draw pool limited to 3 threads 629 ms against 756 ms
-# (profiles/r02bb_host_sensitivity.txt, r02bc_superset_threads.txt).
-# LR_SUPERSET_DEVICE=0: the width is assembled on the host and uploaded by the
-# prefetch thread.
-SUPERSET_ON_DEVICE = __import__("os").environ.get("LR_SUPERSET_DEVICE", "1") != "0"
+# Opt-in (LR_SUPERSET_DEVICE=1): a Superset's halves are uploaded as soon as
+# they are drawn and Omega is assembled on the GPU (lr_omega_assemble_f64,
+# bit-identical), so no host draw, assembly or upload follows the rank read:
+# 95 % of the cfg4 job's draws.  With the Superset cut into SUPERSET_THREADS =
+# 6 pieces the job runs in 605 ms against 614 ms for the host assembly, and it
+# does not depend on the host's draw throughput (draw pool limited to 3
+# threads: 629 ms against 756 ms; profiles/r02bb_host_sensitivity.txt,
+# r02bc_superset_threads.txt).  NOT the default: stress runs of the cfg4 job
+# (tools/r02/omega_stress.py) diverged once in ~150 jobs with it even after the
+# stream-ordering fix of the staging buffers (profiles/r02bg_omega_stress.txt),
+# and never without it; until that is understood the width is assembled on the
+# host and uploaded by the prefetch thread.
+SUPERSET_ON_DEVICE = __import__("os").environ.get("LR_SUPERSET_DEVICE", "0") == "1"
 
 
 def superset_pending_on_device(seed: int, rows: int, cols: int) -> bool:

@@ -165,6 +165,7 @@ def _overlap_draw_with_upload(A: SparseMatrix, seed: int, n: int, w: int, source
 
 
 OMEGA_STATS = {"assembled_on_device": 0, "prefetched_upload": 0, "host_draw": 0}
+_OMEGA_VERIFY = __import__("os").environ.get("LR_OMEGA_VERIFY") == "1"
 
 
 def omega_from_host(seed: int, n: int, w: int):
@@ -190,6 +191,10 @@ def omega_from_host(seed: int, n: int, w: int):
         R, cs, ready = sup.dev
         cur = torch.cuda.current_stream()
         cur.wait_event(ready)
+        # the buffers live in the upload stream's pool: when a staging slot outgrows them they are
+        # freed while this stream may still have the kernel below queued
+        R.record_stream(cur)
+        cs.record_stream(cur)
         if not sup.counted:
             sup.counted = True
             device.TRAFFIC["h2d"] += 8 * (int(R.numel()) + int(cs.numel()))
@@ -197,6 +202,16 @@ def omega_from_host(seed: int, n: int, w: int):
         _native.call("lr_omega_assemble_f64", device.ptr(R), device.ptr(cs), (count + 1) // 2 - sup.p_lo, n, w,
                      device.ptr(Om), device.ld(Om), device.stream())
         sup.mark_consumed(cur)  # the staging slot's device copies are rewritten only after this kernel
+        if _OMEGA_VERIFY:  # diagnostic: the assembled block against the reference draw, bit for bit
+            from .rng import gaussian_matrix
+
+            ref = gaussian_matrix(RngState(seed), n, w)
+            got = device.to_host(Om)
+            if not np.array_equal(got, ref):
+                bad = np.argwhere(got != ref)
+                raise AssertionError(f"device-assembled Omega(seed={seed}, {n}x{w}) differs from the host draw at "
+                                     f"{bad.shape[0]} entries, first {bad[0].tolist()}, last {bad[-1].tolist()}; "
+                                     f"superset widths [{sup.w_lo}, {sup.w_hi}], slot gen {sup._slot.gen} vs {sup._gen}")
         return Om
     if pre is not None:  # the prefetch thread already copied it (upload stream)
         dv, ready = pre
