@@ -9,16 +9,17 @@ o4 = workloads.cfg4()
 A = ObservationSet(o4.m, o4.n, o4.rows, o4.cols, o4.values, o4.split).train_matrix()
 A.pattern(); A.device_values()
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1500
-prm = rsvd.RsvdParams(k=27, p=2, s=5, seed=1261)
+w = int(sys.argv[2]) if len(sys.argv) > 2 else 32
+prm = rsvd.RsvdParams(k=w - 5, p=2, s=5, seed=1261)
 fb = rsvd._Fallback(True, "x")
 ref = None
 bad = {}
 for rep in range(n):
-    Om = rsvd._omega(prm.seed, A.cols, 32, "device")
+    Om = rsvd._omega(prm.seed, A.cols, w, "device")
     H, Q, lu, probe = rsvd._krylov_orth(A, Om, prm, True, False, True, fb, keep_T=True)
     T = Q.T_all
-    st = [("Om", Om), ("H0 = LU(Y Om)", H[:, 0:32]), ("T0 = Y^T H0", T[:, 0:32]), ("H1 = LU(Y T0)", H[:, 32:64]),
-          ("T1 = Y^T H1", T[:, 32:64]), ("H2 = LU(Y T1)", H[:, 64:96]), ("T2", T[:, 64:96]), ("Q.base", Q.base), ("Q.Rinv", Q.Rinv)]
+    st = [("Om", Om), ("H0 = LU(Y Om)", H[:, 0:w]), ("T0 = Y^T H0", T[:, 0:w]), ("H1 = LU(Y T0)", H[:, w:2 * w]),
+          ("T1 = Y^T H1", T[:, w:2 * w]), ("H2 = LU(Y T1)", H[:, 2 * w:3 * w]), ("T2", T[:, 2 * w:3 * w]), ("Q.base", Q.base), ("Q.Rinv", Q.Rinv)]
     st = [(a_, b_.clone()) for a_, b_ in st]
     lus = device.to_host(lu).reshape(-1, 4)
     if ref is None:
@@ -28,4 +29,4 @@ for rep in range(n):
             if not torch.equal(a, b):
                 bad.setdefault(name, []).append((rep, float((a - b).abs().max()), lus[:, 0].tolist()))
                 break
-print("krylov_orth with a fresh Omega per repetition, first differing output:", {k_: (len(v), v[:4]) for k_, v in bad.items()})
+print(f"w={w}: krylov_orth with a fresh Omega per repetition, first differing output:", {k_: (len(v), v[:4]) for k_, v in bad.items()})
