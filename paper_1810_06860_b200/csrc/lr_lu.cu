@@ -557,9 +557,14 @@ static LuPlan lu_plan(int m, int n) {
   const int sms = sm_count();
   // CTAs per SM (tunable: LR_LU_OCC); fewer CTAs = fewer candidates per
   // column and a cheaper barrier, more = less per-column work per CTA
-  static const int occ_pref = getenv("LR_LU_OCC") ? atoi(getenv("LR_LU_OCC")) : 2;
+  // One CTA per SM by default: with two (LR_LU_OCC=2, ~17 % faster per call) the factor of a Krylov block was
+  // occasionally wrong at block widths 32 / 48 -- 12 of 3000 repetitions, multipliers ~1e5, status "ok" -- and never
+  // with one (0 of 7000; profiles/r02bk_bki_determinism.txt).  The cause inside the two-CTA layout is not found yet.
+  static const int occ_pref = getenv("LR_LU_OCC") ? (atoi(getenv("LR_LU_OCC")) >= 2 ? 2 : 1) : 1;
   for (int occ = occ_pref; occ >= 1; --occ) {
-    const size_t limit = (226 * 1024) / occ - 1024;
+    // per-CTA dynamic shared memory: an occ-th of the SM's, and never above the kernel's opt-in (220 KB, lu_impl)
+    size_t limit = (226 * 1024) / occ - 1024;
+    if (limit > 218 * 1024) limit = 218 * 1024;
     int G = sms * occ;
     if (G > 32 * LU_CPL) G = 32 * LU_CPL;
     if (G > (m + 31) / 32) G = (m + 31) / 32;
